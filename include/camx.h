@@ -1,0 +1,226 @@
+/*
+ * camx.h — C ABI of the B200-native seam-exposure + attention-tile path.
+ *
+ * This is the drop-in boundary for the data-parallel video path of the
+ * `camarray` reference (arXiv 1910.03517 remote-tower pipeline).  The
+ * reference is pure Python/numpy; each entry point below replaces one
+ * reference function (cited file:line, relative to the reference's
+ * pkg/src/camarray/) and is what a ctypes/cffi binding of that function
+ * binds to.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Pixel/mask/statistics/map buffers are
+ *    caller-owned DEVICE pointers (cudaMalloc / torch storage) unless the
+ *    parameter name says `host_`.  `stream` is a cudaStream_t passed as
+ *    void* (NULL = legacy default stream).  All calls are asynchronous on
+ *    `stream` unless stated otherwise.
+ *  - Images are (H, W, 3) uint8 row-major RGB, packed back to back
+ *    (image i starts at i*H*W*3).  An "array" of B array-frames x N cameras
+ *    is B*N images, camera-major inside each array-frame.
+ *  - Return value: CAMX_OK (0); negative = invalid argument (the Python
+ *    boundary raises ValueError, like the reference); positive = CUDA error
+ *    code (RuntimeError).  No exception crosses the ABI.
+ *  - Sides: CAMX_SIDE_LEFT = frame sits left of the seam (band/correction at
+ *    its RIGHT edge), CAMX_SIDE_RIGHT = frame sits right of the seam
+ *    (exposure.py:41-45).
+ *  - Seams of an N-camera array: seam s joins camera s (LEFT side) and
+ *    camera s+1 (RIGHT side), s = 0..N-2; with `wrap` a 360-degree array
+ *    has an extra seam N-1 joining camera N-1 and camera 0.
+ *  - Maps: gain/offset are float64 [n_maps][K][3]; an array solve writes
+ *    map index ((b*S + s)*2 + side).
+ */
+#ifndef CAMX_H
+#define CAMX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CAMX_ABI_VERSION 1
+
+#define CAMX_OK 0
+#define CAMX_EINVAL (-1)      /* bad shape / size / config -> ValueError  */
+#define CAMX_EALIGN (-2)      /* pointer alignment not met                 */
+#define CAMX_ENOMEM (-3)      /* scratch allocation failed                 */
+
+#define CAMX_SIDE_LEFT 0
+#define CAMX_SIDE_RIGHT 1
+
+#define CAMX_MODE_STANDARD 0
+#define CAMX_MODE_OBJECT_REMOVAL 1
+#define CAMX_MODE_SMOOTHING 2
+
+/* Exact integer statistics of one (image, side, block) band segment.
+ * Replaces the float moments of BandStats (exposure.py:138-149): mean/std
+ * follow exactly from (valid, sum, sumsq).  `sum/sumsq` cover the pixels
+ * that survive the exclusion mask; `raw_*` cover all band pixels (the
+ * unmasked fit of OBJECT_REMOVAL, exposure.py:327).  112 bytes. */
+typedef struct camx_band_stat {
+  int64_t area;           /* band pixels in the block  (band_area)   */
+  int64_t valid;          /* pixels not excluded       (valid_count) */
+  uint64_t sum[3];
+  uint64_t sumsq[3];
+  uint64_t raw_sum[3];
+  uint64_t raw_sumsq[3];
+} camx_band_stat;
+
+/* ExposureConfig (exposure.py:54-63) fields the solve needs. */
+typedef struct camx_solve_config {
+  int32_t mode;                 /* CAMX_MODE_*                               */
+  int32_t blocks;               /* K                                         */
+  int64_t min_band_pixels;      /* strict: valid > min_band_pixels           */
+  double sigma_min;
+  double alpha;
+  double min_valid_fraction;
+  int32_t have_prev_maps;       /* prev_gain/prev_offset valid for frame 0   */
+  int32_t have_prev_frames;     /* OBJECT_REMOVAL: stats carry masked sums   */
+} camx_solve_config;
+
+/* ---- library ---------------------------------------------------------- */
+int camx_abi_version(void);
+const char *camx_status_string(int status);
+/* Number of SMs of the current device (grid sizing); host-synchronous. */
+int camx_device_sm_count(int32_t *sm_count_out);
+
+/* ---- stage 1: seam band statistics (K1) ---------------------------------
+ * Replaces band_stats (exposure.py:152-185) for BOTH sides of every image,
+ * plus the in-band part of mask_diff (core.py:191-196) when `prev_images`
+ * is given (OBJECT_REMOVAL, exposure.py:313-316): a band pixel is excluded
+ * iff max_c |cur - prev| > t_diff.  `excl_masks` (optional, (n,H,W) bytes,
+ * nonzero = excluded) is the explicit exclusion_mask argument; at most one
+ * of prev_images / excl_masks may be non-NULL.
+ * stats_out: [n_images][2 sides][blocks] records.
+ * hist_out (optional): uint32 [n_images][2][blocks][3][256] histograms of
+ * the non-excluded band pixels (builder-defined product; moments derive
+ * from it exactly).  Errors: band_width > W/2, blocks < 1, blocks > H. */
+int camx_band_stats(const uint8_t *images, const uint8_t *prev_images,
+                    const uint8_t *excl_masks, int64_t n_images,
+                    int32_t height, int32_t width, int32_t band_width,
+                    int32_t blocks, int32_t t_diff,
+                    camx_band_stat *stats_out, uint32_t *hist_out,
+                    void *stream);
+
+/* Float moments of records: mean/std (K,3) float64 per record as in
+ * BandStats (population std), valid/area int64.  use_raw selects raw_*.
+ * mean_out/std_out: [n_records][3]; valid_out/area_out: [n_records]. */
+int camx_band_moments(const camx_band_stat *stats, int64_t n_records,
+                      int32_t use_raw, double *mean_out, double *std_out,
+                      int64_t *valid_out, int64_t *area_out, void *stream);
+
+/* ---- stage 2: seam gain solve (K2) --------------------------------------
+ * Replaces update_exposure (exposure.py:245-344) = fit_affine :188-229 +
+ * resolve :275-293 + smooth_exposure :232-242 for every seam of a batch of
+ * n_batch consecutive array-frames.  Frame b uses frame b-1's output maps
+ * as prev_maps (frame 0 uses prev_gain/prev_offset when
+ * cfg->have_prev_maps), i.e. the batch is a tick loop.
+ * stats: [n_batch][n_cams][2][blocks] from camx_band_stats.
+ * prev_gain/prev_offset: [S][2][K][3]; gain_out/offset_out:
+ * [n_batch][S][2][K][3]; fit_ok_out (optional): [n_batch][S][K] bytes
+ * (the raw fit's fit_ok).  S = n_cams-1 (+1 with wrap). */
+int camx_seam_solve(const camx_band_stat *stats, int32_t n_batch,
+                    int32_t n_cams, int32_t wrap,
+                    const camx_solve_config *cfg, const double *prev_gain,
+                    const double *prev_offset, double *gain_out,
+                    double *offset_out, uint8_t *fit_ok_out, void *stream);
+
+/* fit_affine (exposure.py:188-229) on float moments (BandStats fields).
+ * l_mean/l_std/r_mean/r_std: [K][3]; l_valid/r_valid: [K].
+ * gain_out/offset_out: [2 sides][K][3]; fit_ok_out: [K] bytes. */
+int camx_fit_affine(const double *l_mean, const double *l_std,
+                    const int64_t *l_valid, const double *r_mean,
+                    const double *r_std, const int64_t *r_valid,
+                    int32_t blocks, double sigma_min,
+                    int64_t min_band_pixels, double *gain_out,
+                    double *offset_out, uint8_t *fit_ok_out, void *stream);
+
+/* smooth_exposure (exposure.py:232-242): out = (1-alpha)*prev + alpha*new,
+ * coefficient-wise over n doubles (gain and offset each). */
+int camx_smooth_maps(const double *prev_gain, const double *prev_offset,
+                     const double *new_gain, const double *new_offset,
+                     int64_t n, double alpha, double *gain_out,
+                     double *offset_out, void *stream);
+
+/* ---- stage 3: per-pixel correction apply (K3) ---------------------------
+ * Replaces _lambda_profile + _apply_arrays + apply_exposure
+ * (exposure.py:347-414): out = clip(rint(f32(p)*M + A), 0, 255) on the
+ * near half of each seam side, M = f32(1 + lam*(g-1)), A = f32(lam*b)
+ * evaluated in float64 per (block, column, channel) without materialising
+ * the (H, W/2, 3) tables; the far half is copied.  Bit-exact with numpy.
+ * Array form: images [n_batch][cam_count][H][W][3] are cameras
+ * cam_begin..cam_begin+cam_count-1 of an n_cams_total array; camera c uses
+ * the LEFT map of seam c and the RIGHT map of seam c-1 (wrap: seam N-1 for
+ * camera 0 / N-1).  maps: [n_batch][S][2][K][3].  `out` may equal
+ * `images` (apply_exposure_inplace, exposure.py:404-414). */
+int camx_apply_array(const uint8_t *images, uint8_t *out, int32_t n_batch,
+                     int32_t cam_begin, int32_t cam_count,
+                     int32_t n_cams_total, int32_t wrap, int32_t height,
+                     int32_t width, int32_t blocks, const double *gain,
+                     const double *offset, void *stream);
+
+/* One map on n_images images (apply_exposure / apply_exposure_inplace):
+ * gain/offset [K][3], side CAMX_SIDE_*. */
+int camx_apply_map(const uint8_t *images, uint8_t *out, int64_t n_images,
+                   int32_t height, int32_t width, int32_t side,
+                   int32_t blocks, const double *gain, const double *offset,
+                   void *stream);
+
+/* ---- stage 4a: motion mask + window counts (K4) -------------------------
+ * mask_diff (core.py:191-196): mask[i] = max_c |a - b| > t_diff over
+ * n_pixels RGB pixels; mask_out bytes 0/1. */
+int camx_mask_diff(const uint8_t *a, const uint8_t *b, int64_t n_pixels,
+                   int32_t t_diff, uint8_t *mask_out, void *stream);
+
+/* Per-window on-pixel counts of difference_plan (attention.py:96-100) on
+ * the mosaic of n_cams images (mosaic col x -> camera x / width), without
+ * materialising the mosaic.  Either `mask` ((n_cams,H,W) bytes, nonzero =
+ * on) or (`cur`, `prev`, t_diff) frames (fused mask_diff).  Windows are
+ * [n_windows][2] int32 (x, y) origins of size x size squares, device
+ * memory.  counts_out: int64 [n_windows]. */
+int camx_window_counts(const uint8_t *mask, const uint8_t *cur,
+                       const uint8_t *prev, int32_t t_diff, int32_t n_cams,
+                       int32_t height, int32_t width, const int32_t *windows,
+                       int32_t n_windows, int32_t size, int64_t *counts_out,
+                       void *stream);
+
+/* ---- stage 4b: attention tile crop / resize (K5) ------------------------
+ * Crop of ExternalDetector.detect (detect.py:297-300) of window (x, y, S)
+ * from the (virtual) mosaic of n_cams images, then bilinear resize to
+ * out_size x out_size (half-pixel centres, float32, round-half-even; the
+ * resize is builder-defined - the reference only crops).  out_size == S is
+ * the exact crop.  images: [n_batch][n_cams][H][W][3]; windows: device
+ * int32 [n_tiles][3] = (batch index, x, y); tiles_out: uint8
+ * [n_tiles][out_size][out_size][3]. */
+int camx_tiles(const uint8_t *images, int32_t n_cams, int32_t height,
+               int32_t width, const int32_t *windows, int32_t n_tiles,
+               int32_t size, int32_t out_size, uint8_t *tiles_out,
+               void *stream);
+
+/* Fused stage 3 + 4b (config 5): apply the array correction AND emit the
+ * tiles from the corrected pixels in one pass over the raw frames.
+ * Arguments as camx_apply_array (cam_begin = 0, cam_count = n_cams) and
+ * camx_tiles. */
+int camx_correct_and_tile(const uint8_t *images, uint8_t *out,
+                          int32_t n_batch, int32_t n_cams, int32_t wrap,
+                          int32_t height, int32_t width, int32_t blocks,
+                          const double *gain, const double *offset,
+                          const int32_t *windows, int32_t n_tiles,
+                          int32_t size, int32_t out_size, uint8_t *tiles_out,
+                          void *stream);
+
+/* ---- next: seam quality metric ------------------------------
+ * seam_cost (exposure.py:417-445) of n_pairs (left, right) image pairs of
+ * equal height: box-downsample by `factor`, per-row trend discrepancy,
+ * mean over rows.  left/right: [n_pairs][H][W][3] (widths may differ:
+ * left_width / right_width).  cost_out: float64 [n_pairs]. */
+int camx_seam_cost(const uint8_t *left, const uint8_t *right,
+                   int64_t n_pairs, int32_t height, int32_t left_width,
+                   int32_t right_width, int32_t factor, double *cost_out,
+                   void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CAMX_H */
