@@ -1,0 +1,264 @@
+"""Batched, device-resident array correction: the production path.
+
+`ArrayCorrector` runs the whole seam pipeline for a batch of array-frames
+(B array-frames x N cameras, uint8 (B, N, H, W, 3) in HBM) with three
+kernel launches and no host round trip:
+
+  K1 camx_band_stats  - both seam bands of every image, exact integer
+                         moments (+ optional histograms; + fused in-band
+                         mask_diff for OBJECT_REMOVAL)
+  K2 camx_seam_solve  - update_exposure for every seam, batch as a tick loop
+  K3 camx_apply_array - both seam corrections of every camera in one pass
+
+No reference driver exists for a whole array: the semantics are
+update_exposure per seam (exposure.py:245-344) followed by apply_exposure of
+the seam's LEFT map on camera s and RIGHT map on camera s+1
+(exposure.py:385-401).  Maps stay on the device; the previous batch's last
+maps (and, for OBJECT_REMOVAL, its last frame) seed the next batch.
+
+`correct_host` is the end-to-end entry point from pinned host memory: a
+3-slot device ring with H2D, compute and D2H on separate streams so the
+PCIe copies of chunk i+1 / i-1 overlap the kernels of chunk i.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev, _lib
+from .exposure import (ExposureConfig, ExposureMap, ExposureMode, SeamMaps, Side, _MODE_CODE,
+                       block_bounds)
+
+
+@dataclass
+class CorrectResult:
+    out: object            # uint8 (B, N, H, W, 3) CUDA tensor
+    gain: object           # float64 (B, S, 2, K, 3)
+    offset: object         # float64 (B, S, 2, K, 3)
+    fit_ok: object         # uint8 (B, S, K)
+    stats: object          # uint8 (B, N, 2, K, 112) camx_band_stat records
+    hist: object | None    # int32 (B, N, 2, K, 3, 256) (uint32 counts) or None
+
+
+class ArrayCorrector:
+    """Seam exposure correction of an N-camera array on one GPU."""
+
+    def __init__(self, n_cams: int, height: int, width: int,
+                 cfg: ExposureConfig = ExposureConfig(),
+                 mode: ExposureMode = ExposureMode.STANDARD, *, wrap: bool = False,
+                 histograms: bool = False, cam_begin: int = 0, cam_count: int | None = None,
+                 exchange=None):
+        """cam_begin/cam_count: the cameras this GPU owns (default all);
+        `exchange(stats_local) -> stats_full` assembles the (B, n_cams, 2, K)
+        stat records of every camera (an NCCL all-gather, see dist.py) when
+        the array is sharded across GPUs."""
+        if n_cams < 1:
+            raise ValueError("need at least one camera")
+        if wrap and n_cams < 2:
+            raise ValueError("a wrapped (360 degree) array needs two cameras")
+        if not isinstance(mode, ExposureMode):
+            raise ValueError(f"unknown exposure mode {mode!r}")
+        if cfg.band_width > width // 2:
+            raise ValueError(f"band width {cfg.band_width} exceeds half frame width {width // 2}")
+        block_bounds(height, cfg.blocks)
+        cam_count = n_cams - cam_begin if cam_count is None else cam_count
+        if cam_begin < 0 or cam_count < 1 or cam_begin + cam_count > n_cams:
+            raise ValueError("camera shard outside the array")
+        if cam_count != n_cams and exchange is None:
+            raise ValueError("a camera shard needs a stats exchange")
+        self.cam_begin, self.cam_count, self.exchange = cam_begin, cam_count, exchange
+        self.n_cams, self.height, self.width = n_cams, height, width
+        self.cfg, self.mode, self.wrap = cfg, mode, bool(wrap)
+        self.histograms = histograms
+        self.S = n_cams if wrap else n_cams - 1
+        self.K = cfg.blocks
+        self._bufs: dict = {}
+        self._prev_maps = None     # (gain, offset) device [S][2][K][3]
+        self._prev_frame = None    # device (N, H, W, 3), OBJECT_REMOVAL only
+        self._ring = None
+
+    # ------------------------------------------------------------ state
+    def reset(self) -> None:
+        """Forget previous maps / frames (next batch starts like tick 0)."""
+        self._prev_maps = None
+        self._prev_frame = None
+
+    def set_prev_maps(self, maps: list[SeamMaps]) -> None:
+        g = np.stack([[m.left.gain, m.right.gain] for m in maps])
+        o = np.stack([[m.left.offset, m.right.offset] for m in maps])
+        if g.shape != (self.S, 2, self.K, 3):
+            raise ValueError("exposure map geometry mismatch")
+        self._prev_maps = (_dev.to_device(g), _dev.to_device(o))
+
+    def _buffers(self, B: int):
+        buf = self._bufs.get(B)
+        if buf is None:
+            t = _dev.require_cuda()
+            N, K, S = self.cam_count, self.K, self.S
+            buf = dict(
+                stats=t.empty((B, N, 2, K, _lib.STAT_BYTES), dtype=t.uint8, device="cuda"),
+                gain=t.empty((B, max(S, 1), 2, K, 3), dtype=t.float64, device="cuda"),
+                offset=t.empty((B, max(S, 1), 2, K, 3), dtype=t.float64, device="cuda"),
+                fit_ok=t.empty((B, max(S, 1), K), dtype=t.uint8, device="cuda"),
+                hist=(t.empty((B, N, 2, K, 3, 256), dtype=t.int32, device="cuda")
+                      if self.histograms else None),
+                prev_g=t.ones((max(S, 1), 2, K, 3), dtype=t.float64, device="cuda"),
+                prev_o=t.zeros((max(S, 1), 2, K, 3), dtype=t.float64, device="cuda"),
+            )
+            self._bufs[B] = buf
+        return buf
+
+    # ------------------------------------------------------------ device path
+    def correct(self, frames, out=None, *, stream=None, prev_frames=None) -> CorrectResult:
+        """Correct a (B, cam_count, H, W, 3) uint8 CUDA tensor (this GPU's
+        cameras); returns device results.
+
+        `prev_frames` (N, H, W, 3) overrides the remembered previous frame
+        for OBJECT_REMOVAL's motion mask of array-frame 0."""
+        t = _dev.require_cuda()
+        if frames.dim() == 4:
+            frames = frames[None]
+        B, N, H, W, C = frames.shape
+        if (N, H, W, C) != (self.cam_count, self.height, self.width, 3) or frames.dtype != t.uint8:
+            raise ValueError(f"frames must be (B, {self.cam_count}, {self.height}, {self.width}, 3) "
+                             f"uint8, got {tuple(frames.shape)} {frames.dtype}")
+        if not frames.is_cuda or not frames.is_contiguous():
+            raise ValueError("frames must be a contiguous CUDA tensor")
+        if out is None:
+            out = t.empty_like(frames)
+        elif out.shape != frames.shape or not out.is_contiguous():
+            raise ValueError("out must match frames")
+        buf = self._buffers(B)
+        sh = _dev.stream_handle(stream)
+        cfg = self.cfg
+        per_img = H * W * 3
+        stats = buf["stats"]
+        hist = buf["hist"]
+        removal = self.mode is ExposureMode.OBJECT_REMOVAL
+        pf = prev_frames if prev_frames is not None else self._prev_frame
+        base = frames.data_ptr()
+        rec_bytes = N * 2 * self.K * _lib.STAT_BYTES
+        hist_bytes = N * 2 * self.K * 3 * 256 * 4
+        # K1: array-frame 0 (against the remembered previous frame), then
+        # frames 1.. against their predecessors (a contiguous view, no copy)
+        if removal and B > 1:
+            _lib.call("camx_band_stats", base + N * per_img, base, None, (B - 1) * N, H, W,
+                      cfg.band_width, self.K, cfg.t_diff, stats.data_ptr() + rec_bytes,
+                      None if hist is None else hist.data_ptr() + hist_bytes, sh)
+            n0 = N
+        else:
+            n0 = B * N
+        _lib.call("camx_band_stats", base, _dev.ptr(pf) if removal else None, None, n0, H, W,
+                  cfg.band_width, self.K, cfg.t_diff, stats.data_ptr(),
+                  _dev.ptr(hist), sh)
+        # seam statistics of every camera (all-gather when sharded)
+        full = stats if self.exchange is None else self.exchange(stats)
+        # K2
+        have_prev = self._prev_maps is not None
+        sc = _lib.SolveConfig(_MODE_CODE[self.mode], self.K, int(cfg.min_band_pixels),
+                              float(cfg.sigma_min), float(cfg.alpha),
+                              float(cfg.min_valid_fraction), int(have_prev),
+                              int(removal and pf is not None))
+        gain, off = buf["gain"], buf["offset"]
+        if self.S > 0:
+            pg, po = self._prev_maps if have_prev else (None, None)
+            _lib.call("camx_seam_solve", full.data_ptr(), B, self.n_cams, int(self.wrap),
+                      ctypes.byref(sc),
+                      _dev.ptr(pg), _dev.ptr(po), gain.data_ptr(), off.data_ptr(),
+                      buf["fit_ok"].data_ptr(), sh)
+        # K3
+        _lib.call("camx_apply_array", base, out.data_ptr(), B, self.cam_begin, N, self.n_cams,
+                  int(self.wrap), H, W, self.K, gain.data_ptr(), off.data_ptr(), sh)
+        # carry the tick-loop state to the next batch
+        if self.S > 0:
+            s = stream if stream is not None else t.cuda.current_stream()
+            with t.cuda.stream(s):
+                buf["prev_g"].copy_(gain[B - 1], non_blocking=True)
+                buf["prev_o"].copy_(off[B - 1], non_blocking=True)
+            self._prev_maps = (buf["prev_g"], buf["prev_o"])
+        if removal:
+            s = stream if stream is not None else t.cuda.current_stream()
+            if self._prev_frame is None:
+                self._prev_frame = t.empty_like(frames[0])
+            with t.cuda.stream(s):
+                self._prev_frame.copy_(frames[B - 1], non_blocking=True)
+        return CorrectResult(out, gain[:, : self.S], off[:, : self.S], buf["fit_ok"][:, : self.S],
+                             full, hist)
+
+    # ------------------------------------------------------------ results
+    def maps(self, result: CorrectResult, b: int = -1, camera_ids=None) -> list[SeamMaps]:
+        """Host SeamMaps of array-frame b (seam s = cameras (s, s+1 mod N))."""
+        ids = list(camera_ids) if camera_ids is not None else list(range(self.n_cams))
+        g = _dev.to_host(result.gain[b])
+        o = _dev.to_host(result.offset[b])
+        bw = self.cfg.band_width
+        maps = []
+        for s in range(self.S):
+            sid = (ids[s], ids[(s + 1) % self.n_cams])
+            maps.append(SeamMaps(ExposureMap(sid, Side.LEFT, bw, g[s, 0], o[s, 0]),
+                                 ExposureMap(sid, Side.RIGHT, bw, g[s, 1], o[s, 1])))
+        return maps
+
+    # ------------------------------------------------------------ host path
+    def correct_host(self, frames_host, out_host=None, *, chunk: int = 1):
+        """End-to-end correction of host frames (B, N, H, W, 3) uint8.
+
+        frames_host/out_host: pinned torch CPU tensors for full-speed async
+        copies (numpy arrays are accepted and wrapped, at pageable-copy
+        speed).  Returns out_host.  H2D, kernels and D2H of consecutive
+        chunks overlap on three streams."""
+        t = _dev.require_cuda()
+        src = frames_host if isinstance(frames_host, t.Tensor) else t.from_numpy(
+            np.ascontiguousarray(frames_host))
+        if src.dim() == 4:
+            src = src[None]
+        B = src.shape[0]
+        if out_host is None:
+            out_host = t.empty(src.shape, dtype=t.uint8, pin_memory=True)
+        dst = out_host if isinstance(out_host, t.Tensor) else t.from_numpy(out_host)
+        ring = self._host_ring(chunk)
+        n_chunks = (B + chunk - 1) // chunk
+        cur = t.cuda.current_stream()
+        for s in (ring["h2d"], ring["comp"], ring["d2h"]):
+            s.wait_stream(cur)
+        for i in range(n_chunks):
+            lo, hi = i * chunk, min(B, (i + 1) * chunk)
+            slot = i % ring["slots"]
+            dev_in = ring["in"][slot][: hi - lo]
+            dev_out = ring["out"][slot][: hi - lo]
+            with t.cuda.stream(ring["h2d"]):
+                ring["h2d"].wait_event(ring["in_free"][slot])
+                dev_in.copy_(src[lo:hi], non_blocking=True)
+                ring["h2d_done"][slot].record(ring["h2d"])
+            ring["comp"].wait_event(ring["h2d_done"][slot])
+            ring["comp"].wait_event(ring["out_free"][slot])
+            self.correct(dev_in, dev_out, stream=ring["comp"])
+            ring["in_free"][slot].record(ring["comp"])
+            ring["comp_done"][slot].record(ring["comp"])
+            with t.cuda.stream(ring["d2h"]):
+                ring["d2h"].wait_event(ring["comp_done"][slot])
+                dst[lo:hi].copy_(dev_out, non_blocking=True)
+                ring["out_free"][slot].record(ring["d2h"])
+        cur.wait_stream(ring["d2h"])
+        return out_host
+
+    def _host_ring(self, chunk: int):
+        ring = self._ring
+        if ring is not None and ring["chunk"] == chunk:
+            return ring
+        t = _dev.require_cuda()
+        slots = 3
+        shape = (chunk, self.cam_count, self.height, self.width, 3)
+        ring = dict(chunk=chunk, slots=slots,
+                    h2d=t.cuda.Stream(), comp=t.cuda.Stream(), d2h=t.cuda.Stream(),
+                    **{"in": [t.empty(shape, dtype=t.uint8, device="cuda") for _ in range(slots)]},
+                    out=[t.empty(shape, dtype=t.uint8, device="cuda") for _ in range(slots)],
+                    in_free=[t.cuda.Event() for _ in range(slots)],
+                    out_free=[t.cuda.Event() for _ in range(slots)],
+                    h2d_done=[t.cuda.Event() for _ in range(slots)],
+                    comp_done=[t.cuda.Event() for _ in range(slots)])
+        self._ring = ring
+        return ring

@@ -1,0 +1,172 @@
+// K4: motion mask (mask_diff) and per-window on-pixel counts (stage 4a).
+//
+// Reference: mask_diff (camarray core.py:191-196): on iff
+// max_c |p1 - p2| > t_diff (strict); difference_plan (attention.py:89-103)
+// counts on-pixels of each overlap-0 window of the mosaic (:96-100).  The
+// mosaic (core.py:102-119, a full np.concatenate copy) is never
+// materialised: mosaic column x maps to camera x / W, column x % W.
+#include "camx_common.cuh"
+
+namespace camx {
+
+// 16 pixels (48 bytes = 3 x uint4) per thread when aligned.
+__global__ void mask_diff_vec_kernel(const uint4 *a, const uint4 *b, int64_t n16, int t_diff,
+                                     uint4 *mask) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint4 va[3], vb[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      va[u] = ld_stream_v4(a + 3 * i + u);
+      vb[u] = ld_stream_v4(b + 3 * i + u);
+    }
+    const uint32_t *wa = reinterpret_cast<const uint32_t *>(va);
+    const uint32_t *wb = reinterpret_cast<const uint32_t *>(vb);
+    uint32_t dw[12];
+#pragma unroll
+    for (int u = 0; u < 12; ++u) dw[u] = __vabsdiffu4(wa[u], wb[u]);
+    const uint8_t *d = reinterpret_cast<const uint8_t *>(dw);
+    uint32_t out[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t w = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int px = q * 4 + e;
+        const int m = max(max(d[3 * px], d[3 * px + 1]), d[3 * px + 2]);
+        w |= (m > t_diff ? 1u : 0u) << (8 * e);
+      }
+      out[q] = w;
+    }
+    st_stream_v4(mask + i, make_uint4(out[0], out[1], out[2], out[3]));
+  }
+}
+
+__global__ void mask_diff_kernel(const uint8_t *a, const uint8_t *b, int64_t lo, int64_t n,
+                                 int t_diff, uint8_t *mask) {
+  for (int64_t i = lo + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int m = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) m = max(m, abs(static_cast<int>(a[3 * i + c]) - b[3 * i + c]));
+    mask[i] = m > t_diff ? 1 : 0;
+  }
+}
+
+// One CTA per (window, row slab).  Counts are exact int64 via one atomic
+// per CTA.
+struct CountParams {
+  const uint8_t *mask, *cur, *prev;
+  int32_t t_diff, n_cams, H, W, size, n_windows, slab;
+  const int32_t *windows;
+  int64_t *counts;
+};
+
+template <bool FUSED>
+__global__ void __launch_bounds__(256) window_count_kernel(const CountParams p) {
+  const int win = blockIdx.y;
+  const int x0 = p.windows[2 * win], y0 = p.windows[2 * win + 1];
+  const int ys = y0 + blockIdx.x * p.slab;
+  const int ye = min(min(y0 + p.size, ys + p.slab), p.H);
+  const int total_w = p.n_cams * p.W;
+  const int64_t img_px = static_cast<int64_t>(p.H) * p.W;
+  unsigned long long local = 0;
+  for (int y = ys; y < ye; ++y) {
+    for (int dx = threadIdx.x; dx < p.size; dx += blockDim.x) {
+      const int x = x0 + dx;
+      if (x < 0 || x >= total_w) continue;
+      const int cam = x / p.W;
+      const int col = x - cam * p.W;
+      const int64_t pix = cam * img_px + static_cast<int64_t>(y) * p.W + col;
+      bool on;
+      if (FUSED) {
+        int m = 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          m = max(m, abs(static_cast<int>(p.cur[3 * pix + c]) - p.prev[3 * pix + c]));
+        on = m > p.t_diff;
+      } else {
+        on = p.mask[pix] != 0;
+      }
+      local += on ? 1 : 0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  __shared__ unsigned long long part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += part[w];
+    atomicAdd(reinterpret_cast<unsigned long long *>(p.counts + win), t);
+  }
+}
+
+}  // namespace camx
+
+using namespace camx;
+
+extern "C" int camx_mask_diff(const uint8_t *a, const uint8_t *b, int64_t n_pixels, int32_t t_diff,
+                              uint8_t *mask_out, void *stream) {
+  if (n_pixels < 0 || !a || !b || !mask_out) return CAMX_EINVAL;
+  if (n_pixels == 0) return CAMX_OK;
+  cudaStream_t s = as_stream(stream);
+  int64_t done = 0;
+  const bool aligned = (reinterpret_cast<uintptr_t>(a) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(b) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(mask_out) % 16 == 0);
+  if (aligned && n_pixels >= 16) {
+    const int64_t n16 = n_pixels / 16;
+    int64_t blocks = (n16 + 255) / 256;
+    const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+    if (blocks > cap) blocks = cap;
+    mask_diff_vec_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        reinterpret_cast<const uint4 *>(a), reinterpret_cast<const uint4 *>(b), n16, t_diff,
+        reinterpret_cast<uint4 *>(mask_out));
+    done = n16 * 16;
+  }
+  if (done < n_pixels) {
+    const int64_t rest = n_pixels - done;
+    int64_t blocks = (rest + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    mask_diff_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, b, done, n_pixels, t_diff,
+                                                                    mask_out);
+  }
+  return launch_status();
+}
+
+extern "C" int camx_window_counts(const uint8_t *mask, const uint8_t *cur, const uint8_t *prev,
+                                  int32_t t_diff, int32_t n_cams, int32_t height, int32_t width,
+                                  const int32_t *windows, int32_t n_windows, int32_t size,
+                                  int64_t *counts_out, void *stream) {
+  if (n_cams < 1 || height < 1 || width < 1 || size < 1 || n_windows < 0 || !counts_out)
+    return CAMX_EINVAL;
+  if ((mask == nullptr) == (cur == nullptr || prev == nullptr)) return CAMX_EINVAL;
+  if (size > height || size > n_cams * width) return CAMX_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  if (n_windows == 0) return CAMX_OK;
+  if (!windows) return CAMX_EINVAL;
+  cudaError_t e = cudaMemsetAsync(counts_out, 0, sizeof(int64_t) * n_windows, s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  CountParams p{};
+  p.mask = mask;
+  p.cur = cur;
+  p.prev = prev;
+  p.t_diff = t_diff;
+  p.n_cams = n_cams;
+  p.H = height;
+  p.W = width;
+  p.size = size;
+  p.n_windows = n_windows;
+  p.windows = windows;
+  p.counts = counts_out;
+  p.slab = 32;
+  dim3 grid((size + p.slab - 1) / p.slab, n_windows);
+  if (mask) {
+    window_count_kernel<false><<<grid, 256, 0, s>>>(p);
+  } else {
+    window_count_kernel<true><<<grid, 256, 0, s>>>(p);
+  }
+  return launch_status();
+}

@@ -1,0 +1,81 @@
+"""CPU-side checks of the C ABI boundary: the library loads without a GPU
+and exports every function include/camx.h declares; struct layouts agree;
+host-side validation raises ValueError like the reference."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1910_03517_b200 import _lib
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = (ROOT / "include" / "camx.h").read_text()
+
+
+def declared_functions():
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(camx_\w+)\s*\(", HEADER, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not _lib.LIB_PATH.exists():
+        from paper_1910_03517_b200 import build
+        build.build()
+    return _lib.load()
+
+
+def test_header_declares_expected_api():
+    names = declared_functions()
+    assert "camx_apply_array" in names and "camx_band_stats" in names
+    assert set(names) == set(_lib.SIGNATURES), set(names) ^ set(_lib.SIGNATURES)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_abi_version_and_status_strings(lib):
+    assert lib.camx_abi_version() == 1
+    assert lib.camx_status_string(0) == b"ok"
+    assert lib.camx_status_string(-1) == b"invalid argument"
+
+
+def test_struct_layouts():
+    assert ctypes.sizeof(_lib.BandStatRecord) == 112
+    assert ctypes.sizeof(_lib.SolveConfig) == 48
+    m = re.search(r"typedef struct camx_band_stat \{(.*?)\}", HEADER, re.S).group(1)
+    assert "int64_t area" in m and "raw_sumsq[3]" in m
+
+
+def test_invalid_arguments_are_rejected_before_any_launch(lib):
+    # band wider than W/2, K > H, bad side: negative status, no CUDA needed
+    rec = np.zeros(8 * 112, np.uint8)
+    assert lib.camx_band_stats(rec.ctypes.data, None, None, 1, 16, 10, 6, 1, 20,
+                               rec.ctypes.data, None, None) == _lib.CAMX_EINVAL
+    assert lib.camx_band_stats(rec.ctypes.data, None, None, 1, 4, 10, 2, 5, 20,
+                               rec.ctypes.data, None, None) == _lib.CAMX_EINVAL
+    g = np.ones(3)
+    assert lib.camx_apply_map(rec.ctypes.data, rec.ctypes.data, 1, 4, 4, 7, 1, g.ctypes.data,
+                              g.ctypes.data, None) == _lib.CAMX_EINVAL
+    with pytest.raises(ValueError):
+        _lib.check(_lib.CAMX_EINVAL, "x")
+    with pytest.raises(RuntimeError):
+        _lib.check(100, "x")
+
+
+def test_product_fails_loudly_without_cuda():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1910_03517_b200 import exposure as xp
+    from paper_1910_03517_b200.core import Frame
+    f = Frame(0, 0, 0, np.zeros((8, 8, 3), np.uint8))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        xp.apply_exposure(f, xp.identity_map((0, 1), xp.Side.LEFT, 1, 4))
+    # host-side validation still raises ValueError first, like the reference
+    with pytest.raises(ValueError):
+        xp.band_stats(f, xp.Side.LEFT, band_width=6, blocks=1)

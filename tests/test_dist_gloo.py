@@ -1,0 +1,71 @@
+"""Multi-process (gloo, world_size 2, CPU) checks of the camera-sharding
+host logic: partition, the stat-record all-gather + re-assembly, and that
+the assembled records equal the 1-process records of the whole array."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1910_03517_b200.dist import camera_partition, make_stats_exchange
+
+
+def test_partition_contiguous_and_balanced():
+    for n in range(1, 17):
+        for w in range(1, n + 1):
+            parts = camera_partition(n, w)
+            assert sum(c for _, c in parts) == n
+            assert [b for b, _ in parts] == list(np.cumsum([0] + [c for _, c in parts])[:-1])
+            assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
+    with pytest.raises(ValueError):
+        camera_partition(2, 3)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def records(B, n_cams, K, seed=0):
+    """Deterministic fake stat records for the whole array (B, N, 2, K, 112)."""
+    g = torch.Generator().manual_seed(seed)
+    return torch.randint(0, 256, (B, n_cams, 2, K, 112), generator=g, dtype=torch.uint8)
+
+
+def _worker(rank, world, port, n_cams, B, K, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = records(B, n_cams, K)
+        begin, count = camera_partition(n_cams, world)[rank]
+        ex = make_stats_exchange(n_cams)
+        got = ex(full[:, begin:begin + count].contiguous())
+        q.put((rank, bool(torch.equal(got, full)), tuple(got.shape)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_cams", [8, 5, 2])
+def test_stats_allgather_reassembles_array(n_cams):
+    world, B, K = 2, 3, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_cams, B, K, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, same, shape in res:
+        assert same, f"rank {rank} re-assembled records differ"
+        assert shape == (B, n_cams, 2, K, 112)

@@ -1,0 +1,431 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden outputs and the pinned numpy oracle.
+
+Gates (BASELINE north_star): histograms and tile indices bit-exact; gains
+within 1e-5 relative (we hold 1e-12 / 1e-9 abs); corrected uint8 within
++-1 LSB (we hold bit-exact where the maps are given, and count LSB flips
+where maps are solved)."""
+
+import numpy as np
+import pytest
+
+from golden_io import load
+from oracle import camarray_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1910_03517_b200 import attention as at  # noqa: E402
+from paper_1910_03517_b200 import core, detect  # noqa: E402
+from paper_1910_03517_b200 import exposure as xp  # noqa: E402
+from paper_1910_03517_b200.array import ArrayCorrector  # noqa: E402
+
+SMALL = load("small")
+SCENE = load("scene")
+C1 = load("config1")
+GAIN_RTOL = 1e-12
+GAIN_ATOL = 1e-9
+
+
+def frame(px, cam=0, idx=0):
+    return core.Frame(cam, idx, 0, np.ascontiguousarray(px, dtype=np.uint8))
+
+
+def side_of(s):
+    return xp.Side.LEFT if str(s) == "left" else xp.Side.RIGHT
+
+
+# ------------------------------------------------------------ golden (reference)
+
+def test_band_stats_golden():
+    for c in SMALL["band_stats"]:
+        s = xp.band_stats(frame(c["px"]), side_of(c["side"]), int(c["bw"]), int(c["k"]), c["mask"])
+        np.testing.assert_array_equal(s.valid_count, c["valid"])
+        np.testing.assert_array_equal(s.band_area, c["area"])
+        np.testing.assert_allclose(s.mean, c["mean"], rtol=1e-14, atol=1e-12)
+        np.testing.assert_allclose(s.std, c["std"], rtol=1e-12, atol=1e-12)
+
+
+def test_fit_affine_golden():
+    for c in SMALL["fit_affine"]:
+        L = xp.BandStats(c["lmean"], c["lstd"], c["lvalid"], c["lvalid"])
+        R = xp.BandStats(c["rmean"], c["rstd"], c["rvalid"], c["rvalid"])
+        lm, rm, ok = xp.fit_affine(L, R)
+        np.testing.assert_array_equal(ok, c["ok"])
+        # identical float64 operation order -> bit-identical to numpy
+        np.testing.assert_array_equal(lm.gain, c["gl"])
+        np.testing.assert_array_equal(lm.offset, c["ol"])
+        np.testing.assert_array_equal(rm.gain, c["gr"])
+        np.testing.assert_array_equal(rm.offset, c["orr"])
+
+
+def test_apply_golden_bit_exact():
+    for c in SMALL["apply"]:
+        em = xp.ExposureMap((0, 1), side_of(c["side"]), 4, c["gain"], c["offset"])
+        out = xp.apply_exposure(frame(c["px"]), em).pixels
+        np.testing.assert_array_equal(out, c["out"])
+
+
+def test_mask_diff_golden():
+    for c in SMALL["mask_diff"]:
+        np.testing.assert_array_equal(core.mask_diff(c["a"], c["b"], int(c["t"])), c["out"])
+
+
+def test_difference_plan_golden():
+    for c in SMALL["difference"]:
+        plan = at.difference_plan(c["mask"], int(c["s"]), int(c["thr"]))
+        got = np.array([(r.window.x, r.window.y, r.priority) for r in plan],
+                       dtype=np.int64).reshape(-1, 3)
+        np.testing.assert_array_equal(got, c["plan"])
+        assert all(r.mechanism is at.Mechanism.DIFFERENCE for r in plan)
+
+
+def test_sliding_plan_golden():
+    for c in SMALL["sliding"]:
+        reqs = at.sliding_window_plan((int(c["w"]), int(c["h"])), int(c["s"]), float(c["ov"]))
+        xy = np.array([(r.window.x, r.window.y) for r in reqs], dtype=np.int64).reshape(-1, 2)
+        np.testing.assert_array_equal(xy, c["xy"])
+
+
+def test_seam_cost_golden():
+    for c in SMALL["seam_cost"]:
+        assert xp.seam_cost(c["a"], c["b"], int(c["f"])) == pytest.approx(float(c["cost"]),
+                                                                          rel=1e-12)
+
+
+MODES = [("standard", xp.ExposureMode.STANDARD, O.STANDARD),
+         ("object_removal", xp.ExposureMode.OBJECT_REMOVAL, O.OBJECT_REMOVAL),
+         ("smoothing", xp.ExposureMode.SMOOTHING, O.SMOOTHING)]
+
+
+@pytest.mark.parametrize("name,mode,_om", MODES)
+@pytest.mark.parametrize("arr", ["n2", "n3"])
+def test_update_exposure_tick_loop_golden(arr, name, mode, _om):
+    """Per-seam drop-in update_exposure + apply_exposure over the reference
+    scene's tick loop, against the reference's own outputs."""
+    sc = SCENE[arr]
+    frames = sc["frames"]
+    T, N = frames.shape[:2]
+    cfg = xp.ExposureConfig(band_width=int(sc["band_width"]), blocks=int(sc["blocks"]))
+    prev_maps = [None] * (N - 1)
+    prev_tick = None
+    for t_ in range(T):
+        tick = [frame(frames[t_, c], cam=c, idx=t_) for c in range(N)]
+        maps = []
+        for s in range(N - 1):
+            pf = None if prev_tick is None else (prev_tick[s], prev_tick[s + 1])
+            m = xp.update_exposure((tick[s], tick[s + 1]), prev_maps[s], mode, cfg, pf)
+            np.testing.assert_allclose(m.left.gain, sc[f"{name}_gain"][t_, s, 0],
+                                       rtol=GAIN_RTOL, atol=GAIN_ATOL)
+            np.testing.assert_allclose(m.right.gain, sc[f"{name}_gain"][t_, s, 1],
+                                       rtol=GAIN_RTOL, atol=GAIN_ATOL)
+            np.testing.assert_allclose(m.left.offset, sc[f"{name}_offset"][t_, s, 0],
+                                       rtol=GAIN_RTOL, atol=GAIN_ATOL)
+            np.testing.assert_allclose(m.right.offset, sc[f"{name}_offset"][t_, s, 1],
+                                       rtol=GAIN_RTOL, atol=GAIN_ATOL)
+            maps.append(m)
+        for c in range(N):
+            f = tick[c]
+            if c < N - 1:
+                f = xp.apply_exposure(f, maps[c].left)
+            if c >= 1:
+                f = xp.apply_exposure(f, maps[c - 1].right)
+            diff = np.abs(f.pixels.astype(int) - sc[f"{name}_out"][t_, c].astype(int))
+            assert diff.max() <= 1
+        prev_maps, prev_tick = maps, tick
+
+
+@pytest.mark.parametrize("name,mode,om", MODES)
+@pytest.mark.parametrize("arr", ["n2", "n3"])
+def test_array_corrector_tick_loop_golden(arr, name, mode, om):
+    """The batched device path over the whole tick loop in ONE call."""
+    sc = SCENE[arr]
+    frames = sc["frames"]
+    T, N, H, W = frames.shape[:4]
+    cfg = xp.ExposureConfig(band_width=int(sc["band_width"]), blocks=int(sc["blocks"]))
+    ac = ArrayCorrector(N, H, W, cfg, mode)
+    res = ac.correct(torch.from_numpy(frames).cuda())
+    g = res.gain.cpu().numpy()
+    o = res.offset.cpu().numpy()
+    np.testing.assert_allclose(g, sc[f"{name}_gain"], rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    np.testing.assert_allclose(o, sc[f"{name}_offset"], rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    out = res.out.cpu().numpy()
+    diff = np.abs(out.astype(int) - sc[f"{name}_out"].astype(int))
+    assert diff.max() <= 1
+    assert (diff > 0).mean() < 1e-5
+
+
+def test_config1_golden():
+    frames = C1["frames"]
+    ac = ArrayCorrector(2, 480, 640)
+    res = ac.correct(torch.from_numpy(frames).cuda())
+    np.testing.assert_allclose(res.gain.cpu().numpy()[0, 0], C1["gain"], rtol=GAIN_RTOL)
+    np.testing.assert_allclose(res.offset.cpu().numpy()[0, 0], C1["offset"], rtol=GAIN_RTOL,
+                               atol=GAIN_ATOL)
+    out = res.out.cpu().numpy()[0]
+    assert np.abs(out.astype(int) - C1["out"].astype(int)).max() <= 1
+    after = xp.seam_cost(out[0], out[1])
+    assert after == pytest.approx(float(C1["cost_after"]), rel=1e-6, abs=1e-9)
+
+
+# ------------------------------------------------ reference test-suite cases
+# Restatements of the reference's known-answer tests (test_exposure.py,
+# test_core.py, test_attention.py) run against the GPU drop-in.
+
+def gray(w, h, v, cam=0):
+    return frame(np.full((h, w, 3), v, np.uint8), cam)
+
+
+class TestReferenceKAT:
+    def test_uniform_band(self):          # test_exposure.py:36-41
+        s = xp.band_stats(gray(64, 32, 100), xp.Side.LEFT, band_width=8, blocks=4)
+        assert np.allclose(s.mean, 100.0) and np.allclose(s.std, 0.0)
+        assert (s.valid_count == 64).all()
+
+    def test_two_point(self):              # :43-51
+        px = np.full((8, 16, 3), 80, np.uint8)
+        px[4:] = 120
+        s = xp.band_stats(frame(px), xp.Side.LEFT, band_width=8, blocks=1)
+        assert np.allclose(s.mean, 100.0) and np.allclose(s.std, 20.0)
+
+    def test_full_exclusion(self):         # :53-57
+        s = xp.band_stats(gray(64, 32, 100), xp.Side.LEFT, 8, 4,
+                          exclusion_mask=np.ones((32, 64), bool))
+        assert (s.valid_count == 0).all()
+        assert (s.mean == 0).all() and (s.std == 0).all()
+
+    def test_band_side(self):              # :59-66
+        px = np.zeros((4, 10, 3), np.uint8)
+        px[:, -2:] = 200
+        assert np.allclose(xp.band_stats(frame(px), xp.Side.LEFT, 2, 1).mean, 200.0)
+        assert np.allclose(xp.band_stats(frame(px), xp.Side.RIGHT, 2, 1).mean, 0.0)
+
+    def test_band_too_wide(self):          # :68-70
+        with pytest.raises(ValueError):
+            xp.band_stats(gray(10, 4, 0), xp.Side.LEFT, band_width=6, blocks=1)
+
+    def test_moment_matching(self):        # :74-81
+        def st(mu, sd, n=10000):
+            return xp.BandStats(np.full((1, 3), float(mu)), np.full((1, 3), float(sd)),
+                                np.full(1, n, np.int64), np.full(1, n, np.int64))
+        lm, rm, ok = xp.fit_affine(st(100, 10), st(120, 20))
+        assert ok.all()
+        assert np.allclose(lm.gain, 1.5) and np.allclose(lm.offset, -40.0)
+        assert np.allclose(rm.gain, 0.75) and np.allclose(rm.offset, 20.0)
+        lm, rm, ok = xp.fit_affine(st(90, 0), st(110, 0))      # degenerate sigma
+        assert np.allclose(lm.gain, 1.0) and np.allclose(lm.offset, 10.0)
+        assert np.allclose(rm.offset, -10.0)
+        lm, _, ok = xp.fit_affine(st(100, 10, 10), st(120, 20))  # too few pixels
+        assert not ok.any() and np.allclose(lm.gain, 1.0) and np.allclose(lm.offset, 0.0)
+
+    def test_smooth(self):                 # :124-162
+        prev = xp.identity_map((0, 1), xp.Side.LEFT, 1, 32)
+        new = xp.ExposureMap((0, 1), xp.Side.LEFT, 32, np.ones((1, 3)), np.full((1, 3), 10.0))
+        out = xp.smooth_exposure(prev, new, alpha=0.05)
+        assert np.allclose(out.gain, 1.0) and np.allclose(out.offset, 0.5)
+        with pytest.raises(ValueError):
+            xp.smooth_exposure(xp.identity_map((0, 1), xp.Side.LEFT, 2, 32),
+                               xp.identity_map((0, 1), xp.Side.LEFT, 3, 32))
+        target = xp.ExposureMap((0, 1), xp.Side.LEFT, 32, np.ones((1, 3)), np.full((1, 3), 25.0))
+        cur = xp.identity_map((0, 1), xp.Side.LEFT, 1, 32)
+        for n in range(1, 41):
+            cur = xp.smooth_exposure(cur, target, 0.05)
+            assert abs(cur.offset[0, 0] - 25.0) == pytest.approx(0.95 ** n * 25.0, rel=1e-10)
+
+    def test_apply_cases(self):            # :249-304
+        f = gray(8, 4, 100)
+        em = xp.ExposureMap((0, 1), xp.Side.LEFT, 4, np.full((1, 3), 1.5), np.full((1, 3), -40.0))
+        assert (xp.apply_exposure(f, em).pixels[:, -1] == 110).all()
+        f = gray(9, 4, 100)
+        em = xp.ExposureMap((0, 1), xp.Side.LEFT, 4, np.full((1, 3), 1.9), np.full((1, 3), 30.0))
+        out = xp.apply_exposure(f, em).pixels
+        assert (out[:, :5] == 100).all() and (out[:, -1] != 100).all()
+        f = gray(9, 4, 100, cam=1)
+        em = xp.ExposureMap((0, 1), xp.Side.RIGHT, 4, np.ones((1, 3)), np.full((1, 3), 40.0))
+        out = xp.apply_exposure(f, em).pixels
+        assert (out[:, 0] == 140).all() and (out[:, 4:] == 100).all() and (out[:, 2] == 120).all()
+        f = gray(8, 6, 100)
+        em = xp.ExposureMap((0, 1), xp.Side.LEFT, 4, np.ones((2, 3)),
+                            np.stack([np.full(3, 20.0), np.full(3, -20.0)]))
+        out = xp.apply_exposure(f, em).pixels
+        assert (out[:3, -1] == 120).all() and (out[3:, -1] == 80).all()
+        em = xp.ExposureMap((0, 1), xp.Side.LEFT, 4, np.full((1, 3), 2.0), np.zeros((1, 3)))
+        assert xp.apply_exposure(gray(8, 4, 250), em).pixels.max() == 255
+        rng = np.random.default_rng(1234)
+        px = rng.integers(0, 256, (16, 9, 3), dtype=np.uint8)
+        assert np.array_equal(
+            xp.apply_exposure(frame(px), xp.identity_map((0, 1), xp.Side.LEFT, 2, 4)).pixels, px)
+
+    def test_apply_inplace(self):
+        rng = np.random.default_rng(5)
+        px = rng.integers(0, 256, (12, 16, 3), dtype=np.uint8)
+        em = xp.ExposureMap((0, 1), xp.Side.RIGHT, 4, rng.uniform(0.3, 2.5, (3, 3)),
+                            rng.uniform(-30, 30, (3, 3)))
+        want = O.apply_exposure(px, em.gain, em.offset, O.RIGHT)
+        xp.apply_exposure_inplace(px, em)
+        np.testing.assert_array_equal(px, want)
+
+    def test_mask_kat(self):               # test_core.py:51-80
+        f1 = gray(8, 6, 100)
+        px = f1.pixels.copy()
+        px[3, 5, 1] = 121
+        m = core.abs_diff_threshold(f1, frame(px), 20)
+        assert m.sum() == 1 and m[3, 5]
+        assert not core.abs_diff_threshold(gray(8, 6, 100), gray(8, 6, 120), 20).any()
+        with pytest.raises(ValueError):
+            core.abs_diff_threshold(gray(8, 6, 0), gray(6, 8, 0))
+
+    def test_difference_plan_kat(self):    # test_attention.py:54-78
+        mask = np.zeros((256, 256), bool)
+        mask[0, :50] = True
+        assert at.difference_plan(mask, 256, 50) == []
+        mask[0, 50] = True
+        assert len(at.difference_plan(mask, 256, 50)) == 1
+        mask = np.zeros((128, 256), bool)
+        mask[10:20, 138:188] = True
+        mask[10:12, 10:40] = True
+        plan = at.difference_plan(mask, 128, 50)
+        assert [p.window.x for p in plan] == [128, 0]
+
+    def test_seam_cost_kat(self):          # test_exposure.py:308-343
+        left = np.zeros((4, 2, 3), np.uint8)
+        left[:, 0], left[:, 1] = 100, 110
+        right = np.zeros((4, 2, 3), np.uint8)
+        right[:, 0], right[:, 1] = 130, 140
+        assert xp.seam_cost(left, right, 1) == pytest.approx(10.0 * np.sqrt(3.0))
+        with pytest.raises(ValueError):
+            xp.seam_cost(np.zeros((16, 8, 3), np.uint8), np.zeros((16, 8, 3), np.uint8), 8)
+
+    def test_update_errors(self):
+        with pytest.raises(ValueError):
+            xp.update_exposure((gray(64, 32, 1), gray(64, 16, 1, 1)), None)
+        with pytest.raises(ValueError):
+            xp.update_exposure((gray(64, 32, 1), gray(64, 32, 1, 1)), None, "bogus")
+
+
+def test_maps_table_round_trip_exact():
+    text = open(__import__("golden_io").GOLDEN / "maps_table.txt").read()
+    maps = xp.read_maps_table(text)
+    assert xp.write_maps_table(maps) == text
+    with pytest.raises(ValueError):
+        xp.read_maps_table("0-1 left 0 r 1.0 0.0\n")
+
+
+# ------------------------------------------------------ oracle (builder-defined)
+
+def test_histograms_bit_exact():
+    rng = np.random.default_rng(3)
+    for (n, h, w, bw, k) in [(3, 96, 128, 32, 16), (2, 37, 40, 9, 5), (1, 300, 64, 32, 1)]:
+        px = rng.integers(0, 256, (n, h, w, 3), dtype=np.uint8)
+        px[0, :, :, 1] = 200          # flat channel: all increments on one bin
+        hist = xp.band_histograms(px, bw, k)
+        for i in range(n):
+            for s, side in ((0, O.LEFT), (1, O.RIGHT)):
+                np.testing.assert_array_equal(hist[i, s], O.band_histograms(px[i], side, bw, k))
+        masks = rng.random((n, h, w)) < 0.3
+        hist = xp.band_histograms(px, bw, k, masks)
+        for i in range(n):
+            np.testing.assert_array_equal(hist[i, 0], O.band_histograms(px[i], O.LEFT, bw, k,
+                                                                         masks[i]))
+
+
+def test_long_band_counter_flush():
+    # > 255 pixels per lane forces several counter flush rounds
+    rng = np.random.default_rng(4)
+    px = rng.integers(0, 4, (1, 2160, 64, 3), dtype=np.uint8)
+    hist = xp.band_histograms(px, 32, 1)
+    np.testing.assert_array_equal(hist[0, 0], O.band_histograms(px[0], O.LEFT, 32, 1))
+    s = xp.band_stats(frame(px[0]), xp.Side.RIGHT, 32, 1)
+    m, sd, v, a = O.band_stats(px[0], O.RIGHT, 32, 1)
+    np.testing.assert_allclose(s.mean, m, rtol=1e-14)
+    np.testing.assert_allclose(s.std, sd, rtol=1e-12)
+
+
+@pytest.mark.parametrize("mode,om", [(xp.ExposureMode.STANDARD, O.STANDARD),
+                                     (xp.ExposureMode.OBJECT_REMOVAL, O.OBJECT_REMOVAL),
+                                     (xp.ExposureMode.SMOOTHING, O.SMOOTHING)])
+@pytest.mark.parametrize("wrap", [False, True])
+def test_array_vs_oracle_synthetic(mode, om, wrap):
+    N, H, W, B = 4, 120, 160, 5
+    frames = np.stack([O.synthetic_array(N, H, W, seed=11, objects=3, frame_index=t)
+                       for t in range(B)])
+    cfg = xp.ExposureConfig(band_width=16, blocks=6, min_band_pixels=64)
+    ocfg = O.Cfg(band_width=16, blocks=6, min_band_pixels=64)
+    ac = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap, histograms=True)
+    # two calls (3 + 2 frames) exercise the carried tick-loop state
+    r1 = ac.correct(torch.from_numpy(frames[:3]).cuda())
+    out1, g1 = r1.out.cpu().numpy(), r1.gain.cpu().numpy()
+    r2 = ac.correct(torch.from_numpy(frames[3:]).cuda())
+    out = np.concatenate([out1, r2.out.cpu().numpy()])
+    g = np.concatenate([g1, r2.gain.cpu().numpy()])
+    want_out, want_g, _, _ = O.correct_sequence(frames, None, om, ocfg, None, wrap)
+    np.testing.assert_allclose(g, want_g, rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    d = np.abs(out.astype(int) - want_out.astype(int))
+    assert d.max() <= 1 and (d > 0).mean() < 1e-5
+
+
+def test_apply_array_bit_exact_given_maps():
+    """K3 alone, maps given: bit-exact at several geometries incl. 2048 wide."""
+    rng = np.random.default_rng(9)
+    from paper_1910_03517_b200 import _lib
+    for (N, H, W, K, wrap) in [(3, 64, 2048 // 4, 4, False), (2, 96, 640, 16, True),
+                               (3, 31, 27, 4, False), (2, 50, 100, 7, False)]:
+        S = N if wrap else N - 1
+        frames = rng.integers(0, 256, (2, N, H, W, 3), dtype=np.uint8)
+        gain = rng.uniform(0.2, 3.0, (2, S, 2, K, 3))
+        off = rng.uniform(-80, 80, (2, S, 2, K, 3))
+        d_in = torch.from_numpy(frames).cuda()
+        d_out = torch.empty_like(d_in)
+        g = torch.from_numpy(gain).cuda()
+        o = torch.from_numpy(off).cuda()
+        _lib.call("camx_apply_array", d_in.data_ptr(), d_out.data_ptr(), 2, 0, N, N, int(wrap),
+                  H, W, K, g.data_ptr(), o.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        got = d_out.cpu().numpy()
+        for b in range(2):
+            want = O.apply_array(frames[b], gain[b], off[b], wrap)
+            np.testing.assert_array_equal(got[b], want)
+
+
+def test_correct_host_matches_device():
+    N, H, W, B = 3, 96, 128, 4
+    frames = np.stack([O.synthetic_array(N, H, W, seed=2, frame_index=t) for t in range(B)])
+    dev = ArrayCorrector(N, H, W).correct(torch.from_numpy(frames).cuda()).out.cpu().numpy()
+    host_in = torch.from_numpy(frames).pin_memory()
+    got = ArrayCorrector(N, H, W).correct_host(host_in).numpy()
+    np.testing.assert_array_equal(got, dev)
+
+
+def test_tiles_crop_and_resize_vs_oracle():
+    rng = np.random.default_rng(12)
+    N, H, W = 3, 200, 180
+    arr = rng.integers(0, 256, (2, N, H, W, 3), dtype=np.uint8)
+    mosaic = [np.concatenate(list(arr[b]), axis=1) for b in range(2)]
+    wins = [(0, 0, 0), (1, 150, 20), (0, N * W - 128, H - 128), (1, 170, 72)]
+    d = torch.from_numpy(arr).cuda()
+    crops = detect.tiles(d, wins, 128, 128).cpu().numpy()
+    res = detect.tiles(d, wins, 128, 52).cpu().numpy()
+    up = detect.tiles(d, wins, 128, 200).cpu().numpy()
+    for i, (b, x, y) in enumerate(wins):
+        c = O.crop(mosaic[b], x, y, 128)
+        np.testing.assert_array_equal(crops[i], c)
+        np.testing.assert_array_equal(res[i], O.resize_bilinear(c, 52))
+        np.testing.assert_array_equal(up[i], O.resize_bilinear(c, 200))
+    with pytest.raises(ValueError):
+        detect.tiles(d, [(0, N * W - 100, 0)], 128, 64)
+
+
+def test_window_counts_vs_oracle():
+    rng = np.random.default_rng(13)
+    N, H, W = 4, 300, 250
+    cur = rng.integers(0, 256, (N, H, W, 3), dtype=np.uint8)
+    prev = cur.copy()
+    prev[rng.random((N, H, W)) < 0.05] += 60
+    mosaic_mask = np.concatenate([O.mask_diff(cur[c], prev[c], 20) for c in range(N)], axis=1)
+    wins, want = O.window_counts(mosaic_mask, 128)
+    got = at.window_counts(wins, 128, cur=cur, prev=prev, t_diff=20, n_cams=N)
+    np.testing.assert_array_equal(got, want)
+    got2 = at.window_counts(wins, 128, mask=np.stack(np.split(mosaic_mask, N, axis=1)), n_cams=N)
+    np.testing.assert_array_equal(got2, want)
