@@ -61,6 +61,10 @@ SIGNATURES = {
     "camx_band_stats": [P, P, P, I64, I32, I32, I32, I32, I32, P, P, P],
     "camx_band_moments": [P, I64, I32, P, P, P, P, P],
     "camx_seam_solve": [P, I32, I32, I32, P, P, P, P, P, P, P],
+    "camx_band_stats_solve": [P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P,
+                              P, P, P, P, P],
+    "camx_correct_batch": [P, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P,
+                           P],
     "camx_fit_affine": [P, P, P, P, P, P, I32, F64, I64, P, P, P, P],
     "camx_smooth_maps": [P, P, P, P, I64, F64, P, P, P],
     "camx_apply_array": [P, P, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P],

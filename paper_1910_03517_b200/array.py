@@ -24,6 +24,7 @@ PCIe copies of chunk i+1 / i-1 overlap the kernels of chunk i.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -132,61 +133,165 @@ class ArrayCorrector:
         elif out.shape != frames.shape or not out.is_contiguous():
             raise ValueError("out must match frames")
         buf = self._buffers(B)
-        sh = _dev.stream_handle(stream)
-        cfg = self.cfg
-        per_img = H * W * 3
-        stats = buf["stats"]
-        hist = buf["hist"]
+        main = stream if stream is not None else t.cuda.current_stream()
         removal = self.mode is ExposureMode.OBJECT_REMOVAL
         pf = prev_frames if prev_frames is not None else self._prev_frame
-        base = frames.data_ptr()
-        rec_bytes = N * 2 * self.K * _lib.STAT_BYTES
-        hist_bytes = N * 2 * self.K * 3 * 256 * 4
-        # K1: array-frame 0 (against the remembered previous frame), then
-        # frames 1.. against their predecessors (a contiguous view, no copy)
-        if removal and B > 1:
-            _lib.call("camx_band_stats", base + N * per_img, base, None, (B - 1) * N, H, W,
-                      cfg.band_width, self.K, cfg.t_diff, stats.data_ptr() + rec_bytes,
-                      None if hist is None else hist.data_ptr() + hist_bytes, sh)
-            n0 = N
-        else:
-            n0 = B * N
-        _lib.call("camx_band_stats", base, _dev.ptr(pf) if removal else None, None, n0, H, W,
-                  cfg.band_width, self.K, cfg.t_diff, stats.data_ptr(),
-                  _dev.ptr(hist), sh)
-        # seam statistics of every camera (all-gather when sharded)
-        full = stats if self.exchange is None else self.exchange(stats)
-        # K2
+        if self.exchange is None and self.S > 0 and self.pipeline_chunks <= 1 and self.fused:
+            self._correct_fused(frames, out, buf, _dev.stream_handle(main), pf)
+            return self._finish(frames, out, buf, main, removal)
+        # Chunked pipeline: K1+K2 of chunk i+1 run on a side stream while K3
+        # of chunk i streams on `main`; the tick-loop state flows between
+        # chunks through device pointers (no copies).
+        n_chunks = max(1, min(self.pipeline_chunks, B))
+        bounds = [(B * i) // n_chunks for i in range(n_chunks + 1)]
+        side = self._side_stream() if n_chunks > 1 else main
+        if side is not main:
+            side.wait_stream(main)
+        prev_maps = self._prev_maps
+        prev_frame_ptr = _dev.ptr(pf)
+        ready = []
+        for i in range(n_chunks):
+            lo, hi = bounds[i], bounds[i + 1]
+            if hi <= lo:
+                continue
+            self._stats_solve(frames, buf, lo, hi, _dev.stream_handle(side), prev_maps,
+                              prev_frame_ptr if removal else None)
+            ev = t.cuda.Event()
+            ev.record(side)
+            ready.append((lo, hi, ev))
+            if self.S > 0:
+                prev_maps = (buf["gain"][hi - 1], buf["offset"][hi - 1])
+            prev_frame_ptr = frames[hi - 1].data_ptr()
+        for lo, hi, ev in ready:
+            main.wait_event(ev)
+            self._apply(frames, out, buf, lo, hi, _dev.stream_handle(main))
+        if side is not main:
+            main.wait_stream(side)
+        return self._finish(frames, out, buf, main, removal)
+
+    def _finish(self, frames, out, buf, main, removal) -> CorrectResult:
+        t = _dev.torch()
+        B = frames.shape[0]
+        gain, off = buf["gain"], buf["offset"]
+        # carry the tick-loop state to the next batch
+        with t.cuda.stream(main):
+            if self.S > 0:
+                buf["prev_g"].copy_(gain[B - 1], non_blocking=True)
+                buf["prev_o"].copy_(off[B - 1], non_blocking=True)
+                self._prev_maps = (buf["prev_g"], buf["prev_o"])
+            if removal:
+                if self._prev_frame is None:
+                    self._prev_frame = t.empty_like(frames[0])
+                self._prev_frame.copy_(frames[B - 1], non_blocking=True)
+        full = buf["stats"] if self.exchange is None else buf["full"]
+        return CorrectResult(out, gain[:, : self.S], off[:, : self.S], buf["fit_ok"][:, : self.S],
+                             full, buf["hist"])
+
+    # >1: K1+K2 of chunk i+1 on a side stream under K3 of chunk i.  Measured
+    # slower than the fused single-chunk path on B200 (smaller K3 launches,
+    # SM contention), so only the sharded path uses chunks.
+    pipeline_chunks = 1
+    # fused K1+K2 (+PDL K3) single call; CAMX_FUSED=0 selects K1, K2, K3 launches
+    fused = os.environ.get("CAMX_FUSED", "1") != "0"
+    # camx_band_stats_solve (K1+K2 in one kernel, last-arriver solve) instead
+    # of K1 -> K2 (PDL); measured slower on B200 (96 regs, serial tail)
+    fused_stats_solve = os.environ.get("CAMX_FUSED_K12", "0") == "1"
+
+    def _correct_fused(self, frames, out, buf, sh, pf):
+        """camx_correct_batch: fused K1+K2 (last-arriver solve) + K3 (PDL)."""
+        cfg = self.cfg
+        B = frames.shape[0]
+        removal = self.mode is ExposureMode.OBJECT_REMOVAL
         have_prev = self._prev_maps is not None
         sc = _lib.SolveConfig(_MODE_CODE[self.mode], self.K, int(cfg.min_band_pixels),
                               float(cfg.sigma_min), float(cfg.alpha),
                               float(cfg.min_valid_fraction), int(have_prev),
                               int(removal and pf is not None))
-        gain, off = buf["gain"], buf["offset"]
-        if self.S > 0:
-            pg, po = self._prev_maps if have_prev else (None, None)
-            _lib.call("camx_seam_solve", full.data_ptr(), B, self.n_cams, int(self.wrap),
-                      ctypes.byref(sc),
-                      _dev.ptr(pg), _dev.ptr(po), gain.data_ptr(), off.data_ptr(),
-                      buf["fit_ok"].data_ptr(), sh)
-        # K3
-        _lib.call("camx_apply_array", base, out.data_ptr(), B, self.cam_begin, N, self.n_cams,
-                  int(self.wrap), H, W, self.K, gain.data_ptr(), off.data_ptr(), sh)
-        # carry the tick-loop state to the next batch
-        if self.S > 0:
-            s = stream if stream is not None else t.cuda.current_stream()
-            with t.cuda.stream(s):
-                buf["prev_g"].copy_(gain[B - 1], non_blocking=True)
-                buf["prev_o"].copy_(off[B - 1], non_blocking=True)
-            self._prev_maps = (buf["prev_g"], buf["prev_o"])
-        if removal:
-            s = stream if stream is not None else t.cuda.current_stream()
-            if self._prev_frame is None:
-                self._prev_frame = t.empty_like(frames[0])
-            with t.cuda.stream(s):
-                self._prev_frame.copy_(frames[B - 1], non_blocking=True)
-        return CorrectResult(out, gain[:, : self.S], off[:, : self.S], buf["fit_ok"][:, : self.S],
-                             full, hist)
+        pg, po = self._prev_maps if have_prev else (None, None)
+        if "counters" not in buf:
+            buf["counters"] = _dev.torch().zeros((self.S * self.K,), dtype=_dev.torch().int32,
+                                                 device="cuda")
+        if self.fused_stats_solve:
+            N, H, W = self.n_cams, self.height, self.width
+            fb = N * H * W * 3
+            base = frames.data_ptr()
+            common = (H, W, cfg.band_width, cfg.t_diff, int(self.wrap), ctypes.byref(sc),
+                      _dev.ptr(pg), _dev.ptr(po), buf["stats"].data_ptr(), _dev.ptr(buf["hist"]),
+                      buf["gain"].data_ptr(), buf["offset"].data_ptr(), buf["fit_ok"].data_ptr(),
+                      buf["counters"].data_ptr(), sh)
+            if removal and B > 1:
+                _lib.call("camx_band_stats_solve", base + fb, base, B, N, 1, B - 1, *common)
+                _lib.call("camx_band_stats_solve", base, _dev.ptr(pf), B, N, 0, 1, *common)
+            else:
+                _lib.call("camx_band_stats_solve", base, _dev.ptr(pf) if removal else None, B, N,
+                          0, B, *common)
+            self._apply(frames, out, buf, 0, B, sh)
+            return
+        _lib.call("camx_correct_batch", frames.data_ptr(), out.data_ptr(),
+                  _dev.ptr(pf) if removal else None, B, self.n_cams, int(self.wrap),
+                  self.height, self.width, cfg.band_width, cfg.t_diff, ctypes.byref(sc),
+                  _dev.ptr(pg), _dev.ptr(po), buf["stats"].data_ptr(), _dev.ptr(buf["hist"]),
+                  buf["gain"].data_ptr(), buf["offset"].data_ptr(), buf["fit_ok"].data_ptr(),
+                  buf["counters"].data_ptr(), sh)
+
+    def _side_stream(self):
+        if getattr(self, "_side", None) is None:
+            self._side = _dev.torch().cuda.Stream()
+        return self._side
+
+    def _stats_solve(self, frames, buf, lo, hi, sh, prev_maps, prev_frame_ptr):
+        """K1 + (exchange) + K2 for array-frames [lo, hi) on stream `sh`."""
+        cfg = self.cfg
+        N, H, W = self.cam_count, self.height, self.width
+        per_img = H * W * 3
+        n = hi - lo
+        stats, hist = buf["stats"], buf["hist"]
+        rec_bytes = N * 2 * self.K * _lib.STAT_BYTES
+        hist_bytes = N * 2 * self.K * 3 * 256 * 4
+        base = frames.data_ptr() + lo * N * per_img
+        st_ptr = stats.data_ptr() + lo * rec_bytes
+        h_ptr = None if hist is None else hist.data_ptr() + lo * hist_bytes
+        removal = self.mode is ExposureMode.OBJECT_REMOVAL
+        # frames lo+1.. against their predecessors (a contiguous view, no
+        # copy), frame lo against the previous chunk's / batch's last frame
+        if removal and n > 1:
+            _lib.call("camx_band_stats", base + N * per_img, base, None, (n - 1) * N, H, W,
+                      cfg.band_width, self.K, cfg.t_diff, st_ptr + rec_bytes,
+                      None if h_ptr is None else h_ptr + hist_bytes, sh)
+            n0 = N
+        else:
+            n0 = n * N
+        _lib.call("camx_band_stats", base, prev_frame_ptr if removal else None, None, n0, H, W,
+                  cfg.band_width, self.K, cfg.t_diff, st_ptr, h_ptr, sh)
+        if self.S == 0:
+            return
+        full_ptr = stats.data_ptr() + lo * rec_bytes
+        if self.exchange is not None:
+            t = _dev.torch()
+            with t.cuda.stream(t.cuda.ExternalStream(sh)):
+                full = self.exchange(stats[lo:hi])
+                if "full" not in buf:
+                    buf["full"] = t.empty((buf["stats"].shape[0], self.n_cams, *full.shape[2:]),
+                                          dtype=full.dtype, device=full.device)
+                buf["full"][lo:hi].copy_(full)
+            full_ptr = buf["full"][lo].data_ptr()
+        have_prev = prev_maps is not None
+        sc = _lib.SolveConfig(_MODE_CODE[self.mode], self.K, int(cfg.min_band_pixels),
+                              float(cfg.sigma_min), float(cfg.alpha),
+                              float(cfg.min_valid_fraction), int(have_prev),
+                              int(removal and prev_frame_ptr is not None))
+        pg, po = prev_maps if have_prev else (None, None)
+        _lib.call("camx_seam_solve", full_ptr, n, self.n_cams, int(self.wrap), ctypes.byref(sc),
+                  _dev.ptr(pg), _dev.ptr(po), buf["gain"][lo].data_ptr(),
+                  buf["offset"][lo].data_ptr(), buf["fit_ok"][lo].data_ptr(), sh)
+
+    def _apply(self, frames, out, buf, lo, hi, sh):
+        N, H, W = self.cam_count, self.height, self.width
+        per_img = H * W * 3
+        off = lo * N * per_img
+        _lib.call("camx_apply_array", frames.data_ptr() + off, out.data_ptr() + off, hi - lo,
+                  self.cam_begin, N, self.n_cams, int(self.wrap), H, W, self.K,
+                  buf["gain"][lo].data_ptr(), buf["offset"][lo].data_ptr(), sh)
 
     # ------------------------------------------------------------ results
     def maps(self, result: CorrectResult, b: int = -1, camera_ids=None) -> list[SeamMaps]:

@@ -20,6 +20,8 @@
 //   fma(., 256, 2^23)      = 2^23 + rint_half_even(clip(y, 0, 256))
 //   min(., 255) on the 16-bit lanes (VIMNMX.U16x2), then byte pack.
 // Since clamp bounds are integers, clip(rint(y)) == rint(clip(y)).
+#include <cstdlib>
+
 #include "camx_common.cuh"
 
 namespace camx {
@@ -38,6 +40,7 @@ struct ApplyParams {
   const double *offset;
   // fast kernel decomposition
   int32_t chunks_per_row, col_groups, row_splits, rows_per_split;
+  int32_t pdl;  // launched as a programmatic dependent of the stats/solve kernel
 };
 
 // Map pointers (LEFT role = seam at the right edge, RIGHT role = seam at the
@@ -217,6 +220,137 @@ __global__ void __launch_bounds__(kApplyThreads, 4) apply_fast_kernel(const Appl
   }
 }
 
+// ------------------------------------------------- TMA bulk-copy pipeline
+// Same work decomposition as apply_fast_kernel, but the rows stream through
+// a kStages-deep shared-memory ring filled by 1-D bulk async copies
+// (cp.async.bulk, the TMA engine) completing on mbarriers, so the bytes in
+// flight per SM no longer depend on registers x occupancy (the LDG version
+// is long-scoreboard bound at 16 warps/SM).  Thread 0 issues; every thread
+// consumes its 16-byte column chunk of each row from shared memory.
+constexpr int kTmaStages = 6;
+constexpr int kTmaRows = 2;  // rows per stage
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kApplyThreads, 4) apply_tma_kernel(const ApplyParams p) {
+  extern __shared__ __align__(128) uint4 ring[];  // [kTmaStages][kTmaRows][kApplyThreads]
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  int64_t item = blockIdx.x;
+  const int cg = static_cast<int>(item % p.col_groups);
+  item /= p.col_groups;
+  const int rs = static_cast<int>(item % p.row_splits);
+  item /= p.row_splits;
+  const int k = static_cast<int>(item % p.K);
+  const int64_t img = item / p.K;
+
+  const int blk_r0 = k * p.bh;
+  const int blk_r1 = (k == p.K - 1) ? p.H : blk_r0 + p.bh;
+  const int r0 = blk_r0 + rs * p.rows_per_split;
+  const int r1 = min(blk_r1, r0 + p.rows_per_split);
+  if (r0 >= r1) return;  // CTA-uniform
+  const int chunks = min(kApplyThreads, p.chunks_per_row - cg * kApplyThreads);
+  const uint32_t seg = static_cast<uint32_t>(chunks) * 16u;
+  const int j = cg * kApplyThreads + threadIdx.x;
+  const int64_t rb = p.row_bytes;
+  const uint8_t *src0 = p.src + img * p.img_bytes + static_cast<int64_t>(r0) * rb +
+                        static_cast<int64_t>(cg) * kApplyThreads * 16;
+  const int nrows = r1 - r0;
+  const int nst = (nrows + kTmaRows - 1) / kTmaRows;
+
+  auto issue = [&](int st) {
+    const int slot = st % kTmaStages;
+    const int rr = min(kTmaRows, nrows - st * kTmaRows);
+    mbar_expect_tx(&full[slot], seg * rr);
+    for (int i = 0; i < rr; ++i)
+      bulk_g2s(ring + (slot * kTmaRows + i) * kApplyThreads,
+               src0 + static_cast<int64_t>(st * kTmaRows + i) * rb, seg, &full[slot]);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaStages; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int st = 0; st < min(kTmaStages, nst); ++st) issue(st);
+  }
+  __syncthreads();
+  // maps come from the preceding stats/solve grid (programmatic dependent
+  // launch): only the raw-pixel prefetch above may run before it completes
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  const bool active = threadIdx.x < chunks;
+  const double *gl, *bl, *gr, *br;
+  map_ptrs(p, img, gl, bl, gr, br);
+  Coef16 cf;
+  if (active) {
+    const int q0 = j * 16;
+    int col = q0 / 3;
+    int ch = q0 - col * 3;
+    float m[16], a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      coef_f32(col, ch, k, p.W, gl, bl, gr, br, m[i], a[i]);
+      if (++ch == 3) {
+        ch = 0;
+        ++col;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      cf.m[i >> 1] = pack2(m[i] * 0.00390625f, m[i + 1] * 0.00390625f);
+      cf.c[i >> 1] = pack2(m[i] * -32768.0f, m[i + 1] * -32768.0f);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      cf.a[i] = fabsf(a[i]) < 7.7037197787136e-34f ? 0.0f : a[i] * 0.00390625f;
+  }
+
+  uint8_t *dst = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
+  for (int st = 0; st < nst; ++st) {
+    const int slot = st % kTmaStages;
+    mbar_wait(&full[slot], (st / kTmaStages) & 1);
+    const int rr = min(kTmaRows, nrows - st * kTmaRows);
+    if (active) {
+      uint4 v[kTmaRows];
+#pragma unroll
+      for (int i = 0; i < kTmaRows; ++i)
+        if (i < rr) v[i] = ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x];
+#pragma unroll
+      for (int i = 0; i < kTmaRows; ++i)
+        if (i < rr) st_stream_v4(dst + static_cast<int64_t>(st * kTmaRows + i) * rb, correct16(v[i], cf));
+    }
+    __syncthreads();  // slot fully consumed
+    if (threadIdx.x == 0 && st + kTmaStages < nst) issue(st + kTmaStages);
+  }
+}
+
 // ------------------------------------------------------------- generic path
 // Any width / alignment: one thread per pixel, coefficients per pixel.
 __global__ void apply_generic_kernel(const ApplyParams p) {
@@ -260,7 +394,36 @@ static int launch_apply(ApplyParams &p, cudaStream_t stream) {
     p.row_splits = splits;
     p.rows_per_split = (max_rows + splits - 1) / splits;
     const int64_t grid = base * splits;
-    apply_fast_kernel<<<static_cast<unsigned>(grid), kApplyThreads, 0, stream>>>(p);
+    static const int use_ldg = [] {
+      const char *e = getenv("CAMX_APPLY_KERNEL");
+      return (e != nullptr && e[0] == 'l') ? 1 : 0;
+    }();
+    if (use_ldg) {
+      apply_fast_kernel<<<static_cast<unsigned>(grid), kApplyThreads, 0, stream>>>(p);
+    } else {
+      const int smem = kTmaStages * kTmaRows * kApplyThreads * 16;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+      }
+      if (p.pdl) {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(static_cast<unsigned>(grid));
+        lc.blockDim = dim3(kApplyThreads);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&lc, apply_tma_kernel, p);
+        if (e != cudaSuccess) return static_cast<int>(e);
+      } else {
+        apply_tma_kernel<<<static_cast<unsigned>(grid), kApplyThreads, smem, stream>>>(p);
+      }
+    }
   } else {
     const int64_t npx = static_cast<int64_t>(p.n_img) * p.H * p.W;
     int64_t blocks = (npx + 255) / 256;
@@ -274,6 +437,13 @@ static int launch_apply(ApplyParams &p, cudaStream_t stream) {
 }  // namespace camx
 
 using namespace camx;
+
+namespace camx {
+int launch_seam_solve(const camx_band_stat *stats, int32_t n_batch, int32_t n_cams, int32_t wrap,
+                      const camx_solve_config *cfg, const double *prev_gain,
+                      const double *prev_offset, double *gain_out, double *offset_out,
+                      uint8_t *fit_ok_out, cudaStream_t stream, bool pdl);
+}
 
 extern "C" int camx_apply_array(const uint8_t *images, uint8_t *out, int32_t n_batch,
                                 int32_t cam_begin, int32_t cam_count, int32_t n_cams_total,
@@ -330,5 +500,63 @@ extern "C" int camx_apply_map(const uint8_t *images, uint8_t *out, int64_t n_ima
   p.n_cams = 1;
   p.gain = gain;
   p.offset = offset;
+  return launch_apply(p, as_stream(stream));
+}
+
+extern "C" int camx_correct_batch(const uint8_t *images, uint8_t *out, const uint8_t *prev_frame,
+                                  int32_t n_batch, int32_t n_cams, int32_t wrap, int32_t height,
+                                  int32_t width, int32_t band_width, int32_t t_diff,
+                                  const camx_solve_config *cfg, const double *prev_gain,
+                                  const double *prev_offset, camx_band_stat *stats,
+                                  uint32_t *hist, double *gain_out, double *offset_out,
+                                  uint8_t *fit_ok_out, int32_t *counters, void *stream) {
+  if (cfg == nullptr || images == nullptr || out == nullptr || stats == nullptr) return CAMX_EINVAL;
+  if (gain_out == nullptr || offset_out == nullptr) return CAMX_EINVAL;
+  if (n_batch < 1 || n_cams < 2 || cfg->blocks < 1 || cfg->blocks > height) return CAMX_EINVAL;
+  if (cfg->mode < CAMX_MODE_STANDARD || cfg->mode > CAMX_MODE_SMOOTHING) return CAMX_EINVAL;
+  if (cfg->have_prev_maps && (prev_gain == nullptr || prev_offset == nullptr)) return CAMX_EINVAL;
+  (void)counters;  // used by the fused variant (camx_band_stats_solve)
+  const int64_t img_bytes = static_cast<int64_t>(height) * width * 3;
+  const int64_t frame_bytes = img_bytes * n_cams;
+  const int64_t rec_frame = static_cast<int64_t>(n_cams) * 2 * cfg->blocks;
+  const bool removal = cfg->mode == CAMX_MODE_OBJECT_REMOVAL;
+  int st;
+  // K1: band statistics (frames 1.. against their predecessors, frame 0
+  // against prev_frame, for OBJECT_REMOVAL)
+  if (removal && n_batch > 1) {
+    st = camx_band_stats(images + frame_bytes, images, nullptr, (n_batch - 1) * int64_t(n_cams),
+                         height, width, band_width, cfg->blocks, t_diff, stats + rec_frame,
+                         hist == nullptr ? nullptr : hist + rec_frame * 768, stream);
+    if (st != CAMX_OK) return st;
+    st = camx_band_stats(images, prev_frame, nullptr, n_cams, height, width, band_width,
+                         cfg->blocks, t_diff, stats, hist, stream);
+  } else {
+    st = camx_band_stats(images, removal ? prev_frame : nullptr, nullptr,
+                         int64_t(n_batch) * n_cams, height, width, band_width, cfg->blocks,
+                         t_diff, stats, hist, stream);
+  }
+  if (st != CAMX_OK) return st;
+  // K2 as a programmatic dependent of K1, K3 as one of K2
+  st = launch_seam_solve(stats, n_batch, n_cams, wrap, cfg, prev_gain, prev_offset, gain_out,
+                         offset_out, fit_ok_out, as_stream(stream), true);
+  if (st != CAMX_OK) return st;
+  ApplyParams p{};
+  p.src = images;
+  p.dst = out;
+  p.H = height;
+  p.W = width;
+  p.K = cfg->blocks;
+  p.bh = height / cfg->blocks;
+  p.row_bytes = width * 3;
+  p.img_bytes = img_bytes;
+  p.n_img = n_batch * n_cams;
+  p.cam_begin = 0;
+  p.cam_count = n_cams;
+  p.n_cams = n_cams;
+  p.wrap = wrap;
+  p.S = wrap ? n_cams : n_cams - 1;
+  p.gain = gain_out;
+  p.offset = offset_out;
+  p.pdl = 1;
   return launch_apply(p, as_stream(stream));
 }

@@ -12,13 +12,17 @@
 // channel) from which mean / population std follow; the optional 256-bin
 // histograms are an exact sufficient statistic of the same pixel sets.
 //
-// Decomposition: one CTA of 3 warps per (image, side, block); warp w owns
-// colour channel w, so every lane counts only one channel.  Histograms use
-// per-lane private 8-bit counters in shared memory (4 bins per 32-bit word,
-// word (bin/4, lane) at bank `lane`, so increments never conflict and need
-// no atomics), flushed every 255 pixels per lane into per-lane registers
-// by a SWAR (2 x 16-bit lanes) column sum.
-#include "camx_common.cuh"
+// Decomposition: one CTA of 4 warps per (image, side, block) unit, warps
+// interleaved over the band's pixel quads.  When the band is
+// 4-pixel aligned (W % 4 == 0, bw % 4 == 0) a lane reads pixel quads as
+// three 32-bit words (12 bytes = r g b r g b r g b r g b, so the channel of
+// every byte is fixed), U quads per batch so U*3 loads are in flight per
+// lane; otherwise it falls back to per-pixel byte loads.  Histograms use
+// per-lane private 8-bit counters in shared memory (4 bins per 32-bit
+// word; word (channel, bin/4, lane) sits in bank `lane`, so increments
+// never conflict and need no atomics), flushed every <= 255 pixels per lane
+// into per-lane registers by a SWAR (2 x 16-bit) column sum.
+#include "camx_solve.cuh"
 
 namespace camx {
 
@@ -28,13 +32,50 @@ struct StatsParams {
   const uint8_t *mask;   // mode 1
   int64_t img_bytes;
   int64_t mask_bytes;    // H * W
+  int64_t n_units;       // n_images * 2 * K
   int32_t H, W, bw, K, bh, t_diff;
   camx_band_stat *out;
   uint32_t *hist;        // optional
+  // fused stats + solve (camx_band_stats_solve)
+  int64_t img_begin;     // absolute image index of this launch's image 0
+  int32_t n_cams, wrap;
+  int32_t *counters;     // [S*K] arrivals, zero between launches
+  SolveParams solve;
 };
 
-constexpr int kStatsWarps = 3;
-constexpr int kCounterWords = 64 * 32;  // per warp: 64 bin-quads x 32 lanes
+// Last-arriver solve: every K1 CTA whose band feeds seam (s, k) bumps
+// counters[s*K+k] after publishing its record; the CTA that completes the
+// 2*B records of that seam block runs the K2 solve for it (whole batch) and
+// re-arms the counter.  Removes the separate K2 launch and its record
+// round trip.
+__device__ __noinline__ void fused_solve_tail(const StatsParams &p, int64_t unit_abs) {
+  __shared__ Cand cand[kSolveFrames][3];
+  __shared__ int last;
+  const int K = p.K;
+  const int k = static_cast<int>(unit_abs % K);
+  const int side = static_cast<int>((unit_abs / K) % 2);
+  const int cam = static_cast<int>((unit_abs / (2 * K)) % p.n_cams);
+  int s = -1;
+  if (side == CAMX_SIDE_LEFT)
+    s = (cam < p.n_cams - 1 || p.wrap) ? cam : -1;
+  else
+    s = cam >= 1 ? cam - 1 : (p.wrap ? p.n_cams - 1 : -1);
+  if (s < 0) return;  // edge band of a non-wrapped array: no seam
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int old = atomicAdd(&p.counters[s * K + k], 1);
+    last = (old == 2 * p.solve.B - 1);
+    if (last) p.counters[s * K + k] = 0;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  solve_seam_block(p.solve, s, k, cand);
+}
+
+constexpr int kStatsWarps = 4;  // warps per (image, side, block) unit = per CTA
+constexpr int kCounterWords = 3 * 64 * 32;  // per warp: 3 ch x 64 bin-quads x 32 lanes
+constexpr int kQuadBatch = 4;
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
@@ -42,13 +83,99 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
   return v;
 }
 
-template <bool HIST, int MASKMODE>
-__global__ void __launch_bounds__(96) band_stats_kernel(const StatsParams p) {
+struct Acc {
+  uint64_t raw_s[3], raw_q[3], val_s[3], val_q[3];
+  uint32_t nvalid;
+};
+
+template <bool HIST>
+__device__ __forceinline__ void add_pixel(Acc &a, uint32_t *cnt, int lane, uint32_t r, uint32_t g,
+                                          uint32_t b, bool excluded) {
+  const uint32_t v[3] = {r, g, b};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    a.raw_s[c] += v[c];
+    a.raw_q[c] += v[c] * v[c];
+  }
+  if (!excluded) {
+    a.nvalid += 1;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (HIST) {
+        uint32_t *wp = cnt + ((c * 64 + (v[c] >> 2)) << 5) + lane;
+        *wp += 1u << ((v[c] & 3u) << 3);
+      } else {
+        a.val_s[c] += v[c];
+        a.val_q[c] += v[c] * v[c];
+      }
+    }
+  }
+}
+
+// Column sums of the lane counters into this lane's 24 bins (3 channels x
+// bin-quads lane and lane+32), then clear the counters.
+__device__ __forceinline__ void flush_counters(uint32_t *cnt, int lane, uint32_t bins[3][8]) {
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int w = c * 64 + lane + 32 * h;
+      uint32_t lo = 0, hi = 0;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) {
+        const uint32_t x = cnt[(w << 5) + ((l + lane) & 31)];
+        lo += x & 0x00FF00FFu;
+        hi += (x >> 8) & 0x00FF00FFu;
+      }
+      bins[c][4 * h + 0] += lo & 0xFFFFu;
+      bins[c][4 * h + 1] += hi & 0xFFFFu;
+      bins[c][4 * h + 2] += lo >> 16;
+      bins[c][4 * h + 3] += hi >> 16;
+    }
+  }
+  __syncwarp();
+  for (int w = 0; w < 3 * 64; ++w) cnt[(w << 5) + lane] = 0u;
+  __syncwarp();
+}
+
+// Excluded-pixel flags of a quad (bit e set = pixel e excluded).
+template <int MASKMODE>
+__device__ __forceinline__ uint32_t quad_exclusion(const StatsParams &p, const uint32_t w[3],
+                                                   const uint32_t pw[3], uint32_t mword) {
+  if (MASKMODE == 1) {
+    // mask bytes nonzero = excluded
+    const uint32_t g = __vcmpne4(mword, 0u);  // 0xFF where excluded
+    return (g & 0x1u) | ((g >> 7) & 0x2u) | ((g >> 14) & 0x4u) | ((g >> 21) & 0x8u);
+  } else if (MASKMODE == 2) {
+    const uint32_t d0 = __vabsdiffu4(w[0], pw[0]);
+    const uint32_t d1 = __vabsdiffu4(w[1], pw[1]);
+    const uint32_t d2 = __vabsdiffu4(w[2], pw[2]);
+    // per pixel the three channel diffs: p0 = d0.b0 d0.b1 d0.b2, p1 = d0.b3 d1.b0 d1.b1,
+    // p2 = d1.b2 d1.b3 d2.b0, p3 = d2.b1 d2.b2 d2.b3
+    const uint32_t x = __byte_perm(__byte_perm(d0, d1, 0x0630u), d2, 0x5210u);  // c0 of p0..p3
+    const uint32_t y = __byte_perm(__byte_perm(d0, d1, 0x0741u), d2, 0x6210u);  // c1
+    const uint32_t z = __byte_perm(__byte_perm(d0, d1, 0x0052u), d2, 0x7410u);  // c2
+    const uint32_t m = __vmaxu4(__vmaxu4(x, y), z);
+    if (p.t_diff < 0) return 0xFu;            // every |d| >= 0 > t_diff
+    const uint32_t t = static_cast<uint32_t>(min(p.t_diff, 255));
+    const uint32_t gt = __vcmpgtu4(m, t * 0x01010101u);  // 0xFF where max > t_diff
+    return (gt & 0x1u) | ((gt >> 7) & 0x2u) | ((gt >> 14) & 0x4u) | ((gt >> 21) & 0x8u);
+  }
+  return 0u;
+}
+
+template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
+__global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const StatsParams p) {
   extern __shared__ uint32_t smem[];
+  __shared__ uint64_t part[kStatsWarps][13];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int ch = warp;
   const int64_t unit = blockIdx.x;
+  constexpr int kStride = 32 * kStatsWarps;  // quads (pixels) per CTA-wide step
+  // let a programmatically dependent K3 launch early: it only prefetches
+  // raw pixels (which this kernel does not write) before griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int k = static_cast<int>(unit % p.K);
   const int side = static_cast<int>((unit / p.K) % 2);
   const int64_t img = unit / (2 * p.K);
@@ -56,133 +183,196 @@ __global__ void __launch_bounds__(96) band_stats_kernel(const StatsParams p) {
   const int r0 = k * p.bh;
   const int r1 = (k == p.K - 1) ? p.H : r0 + p.bh;
   const int col0 = (side == CAMX_SIDE_LEFT) ? p.W - p.bw : 0;
-  const int64_t npix = static_cast<int64_t>(r1 - r0) * p.bw;
   const int64_t row_bytes = static_cast<int64_t>(p.W) * 3;
   const uint8_t *base = p.img + img * p.img_bytes;
   const uint8_t *pbase = (MASKMODE == 2) ? p.prev + img * p.img_bytes : nullptr;
   const uint8_t *mbase = (MASKMODE == 1) ? p.mask + img * p.mask_bytes : nullptr;
 
-  uint32_t *cnt = smem + warp * kCounterWords;
+  uint32_t *cnt = HIST ? smem + warp * kCounterWords : nullptr;
   if (HIST) {
-    for (int w = 0; w < 64; ++w) cnt[w * 32 + lane] = 0u;
+    for (int w = 0; w < 3 * 64; ++w) cnt[(w << 5) + lane] = 0u;
     __syncwarp();
   }
-  uint32_t bins[8];  // this lane's bins 4*lane..4*lane+3 and 128+4*lane..+3
+  uint32_t bins[3][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) bins[i] = 0u;
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bins[c][i] = 0u;
+  Acc a;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) a.raw_s[c] = a.raw_q[c] = a.val_s[c] = a.val_q[c] = 0;
+  a.nvalid = 0;
 
-  uint64_t raw_s = 0, raw_q = 0, val_s = 0, val_q = 0, nvalid = 0;
-  // (row, col) of pixel index p = lane + 32 t, stepped incrementally
-  int rr = r0 + lane / p.bw;
-  int cc = lane % p.bw;
-  int64_t pidx = lane;
-  int round_left = 255;
-  const int64_t iters = (npix + 31) / 32;
-  for (int64_t t = 0; t < iters; ++t) {
-    if (pidx < npix) {
-      const int64_t off = static_cast<int64_t>(rr) * row_bytes + static_cast<int64_t>(col0 + cc) * 3;
-      const uint32_t v = base[off + ch];
-      bool excluded = false;
-      if (MASKMODE == 1) {
-        excluded = mbase[static_cast<int64_t>(rr) * p.W + col0 + cc] != 0;
-      } else if (MASKMODE == 2) {
+  const int rows = r1 - r0;
+  int since_flush = 0;  // pixels added per lane since the last counter flush
+  if (QUAD) {
+    const int qpr = p.bw >> 2;
+    const int nq = rows * qpr;
+    for (int i0 = warp * 32; i0 < nq; i0 += kStride * kQuadBatch) {
+      uint32_t w[kQuadBatch][3], pw[kQuadBatch][3], mw[kQuadBatch];
+      bool live[kQuadBatch];
+#pragma unroll
+      for (int u = 0; u < kQuadBatch; ++u) {
+        const int i = i0 + u * kStride + lane;
+        live[u] = i < nq;
+        const int ii = live[u] ? i : 0;
+        const int row = r0 + ii / qpr;
+        const int col = col0 + (ii - (ii / qpr) * qpr) * 4;
+        const int64_t off = row * row_bytes + static_cast<int64_t>(col) * 3;
+        const uint32_t *wp = reinterpret_cast<const uint32_t *>(base + off);
+        w[u][0] = __ldg(wp);
+        w[u][1] = __ldg(wp + 1);
+        w[u][2] = __ldg(wp + 2);
+        if (MASKMODE == 2) {
+          const uint32_t *pp = reinterpret_cast<const uint32_t *>(pbase + off);
+          pw[u][0] = __ldg(pp);
+          pw[u][1] = __ldg(pp + 1);
+          pw[u][2] = __ldg(pp + 2);
+        }
+        if (MASKMODE == 1)
+          mw[u] = __ldg(reinterpret_cast<const uint32_t *>(mbase + static_cast<int64_t>(row) * p.W + col));
+      }
+#pragma unroll
+      for (int u = 0; u < kQuadBatch; ++u) {
+        if (!live[u]) continue;
+        const uint32_t ex = quad_exclusion<MASKMODE>(p, w[u], pw[u], mw[u]);
+        const uint32_t *q = w[u];
+        add_pixel<HIST>(a, cnt, lane, q[0] & 0xFF, (q[0] >> 8) & 0xFF, (q[0] >> 16) & 0xFF, ex & 1);
+        add_pixel<HIST>(a, cnt, lane, q[0] >> 24, q[1] & 0xFF, (q[1] >> 8) & 0xFF, ex & 2);
+        add_pixel<HIST>(a, cnt, lane, (q[1] >> 16) & 0xFF, q[1] >> 24, q[2] & 0xFF, ex & 4);
+        add_pixel<HIST>(a, cnt, lane, (q[2] >> 8) & 0xFF, (q[2] >> 16) & 0xFF, q[2] >> 24, ex & 8);
+      }
+      if (HIST) {
+        since_flush += 4 * kQuadBatch;
+        if (since_flush > 255 - 4 * kQuadBatch) {  // warp-uniform
+          flush_counters(cnt, lane, bins);
+          since_flush = 0;
+        }
+      }
+    }
+  } else {
+    const int npix = rows * p.bw;
+    for (int i0 = warp * 32; i0 < npix; i0 += kStride * kQuadBatch) {
+      uint32_t v[kQuadBatch][3];
+      bool ex[kQuadBatch], live[kQuadBatch];
+#pragma unroll
+      for (int u = 0; u < kQuadBatch; ++u) {
+        const int i = i0 + u * kStride + lane;
+        live[u] = i < npix;
+        const int ii = live[u] ? i : 0;
+        const int row = r0 + ii / p.bw;
+        const int col = col0 + (ii - (ii / p.bw) * p.bw);
+        const int64_t off = row * row_bytes + static_cast<int64_t>(col) * 3;
         int d = 0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const int a = base[off + c], b = pbase[off + c];
-          d = max(d, abs(a - b));
+          v[u][c] = __ldg(base + off + c);
+          if (MASKMODE == 2) d = max(d, abs(static_cast<int>(v[u][c]) - __ldg(pbase + off + c)));
         }
-        excluded = d > p.t_diff;
+        ex[u] = (MASKMODE == 2) ? (d > p.t_diff)
+                : (MASKMODE == 1) ? (__ldg(mbase + static_cast<int64_t>(row) * p.W + col) != 0)
+                                  : false;
       }
-      raw_s += v;
-      raw_q += v * v;
-      if (!excluded) {
-        nvalid += 1;
-        if (HIST) {
-          uint32_t *wp = cnt + (v >> 2) * 32 + lane;
-          *wp += 1u << ((v & 3u) * 8u);
-        } else {
-          val_s += v;
-          val_q += v * v;
-        }
-      }
-    }
-    pidx += 32;
-    cc += 32;
-    while (cc >= p.bw) {
-      cc -= p.bw;
-      ++rr;
-    }
-    if (HIST && (--round_left == 0 || t == iters - 1)) {
-      round_left = 255;
-      __syncwarp();
-      // lane owns bin-quads w = lane and lane + 32; sum them over 32 lanes
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int w = lane + 32 * h;
-        uint32_t lo = 0, hi = 0;
-#pragma unroll 8
-        for (int l = 0; l < 32; ++l) {
-          const uint32_t x = cnt[w * 32 + ((l + lane) & 31)];
-          lo += x & 0x00FF00FFu;
-          hi += (x >> 8) & 0x00FF00FFu;
+      for (int u = 0; u < kQuadBatch; ++u)
+        if (live[u]) add_pixel<HIST>(a, cnt, lane, v[u][0], v[u][1], v[u][2], ex[u]);
+      if (HIST) {
+        since_flush += kQuadBatch;
+        if (since_flush > 255 - kQuadBatch) {
+          flush_counters(cnt, lane, bins);
+          since_flush = 0;
         }
-        bins[4 * h + 0] += lo & 0xFFFFu;
-        bins[4 * h + 1] += hi & 0xFFFFu;
-        bins[4 * h + 2] += lo >> 16;
-        bins[4 * h + 3] += hi >> 16;
       }
-      __syncwarp();
-      for (int w = 0; w < 64; ++w) cnt[w * 32 + lane] = 0u;
-      __syncwarp();
     }
   }
 
   if (HIST) {
-    val_s = 0;
-    val_q = 0;
+    if (since_flush > 0) flush_counters(cnt, lane, bins);
+    // combine the 4 warps' bins: stage them in (now unused) counter memory
+    __syncthreads();
+    uint32_t *stage = smem;  // [warp][3][256]
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint64_t bin = 4 * (lane + 32 * h) + i;
-        val_s += bin * bins[4 * h + i];
-        val_q += bin * bin * bins[4 * h + i];
-      }
+    for (int c = 0; c < 3; ++c) {
+      reinterpret_cast<uint4 *>(stage + (warp * 3 + c) * 256)[lane] =
+          make_uint4(bins[c][0], bins[c][1], bins[c][2], bins[c][3]);
+      reinterpret_cast<uint4 *>(stage + (warp * 3 + c) * 256 + 128)[lane] =
+          make_uint4(bins[c][4], bins[c][5], bins[c][6], bins[c][7]);
     }
-    if (p.hist != nullptr) {
-      uint32_t *hp = p.hist + ((img * 2 + side) * p.K + k) * 768 + ch * 256;
-      reinterpret_cast<uint4 *>(hp)[lane] = make_uint4(bins[0], bins[1], bins[2], bins[3]);
-      reinterpret_cast<uint4 *>(hp + 128)[lane] = make_uint4(bins[4], bins[5], bins[6], bins[7]);
+    __syncthreads();
+    // thread t owns bins t, t+128, ... of the 768 (channel, bin) pairs
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a.val_s[c] = a.val_q[c] = 0;
+    for (int e = threadIdx.x; e < 768; e += kStatsWarps * 32) {
+      uint32_t tot = 0;
+#pragma unroll
+      for (int w2 = 0; w2 < kStatsWarps; ++w2) tot += stage[w2 * 768 + e];
+      const int c = e >> 8;
+      const uint64_t bin = e & 255;
+      if (p.hist != nullptr) p.hist[unit * 768 + e] = tot;
+      // c is warp-uniform for e in steps of 128 within one channel
+      const uint64_t s1 = bin * tot, s2 = bin * bin * tot;
+      if (c == 0) { a.val_s[0] += s1; a.val_q[0] += s2; }
+      if (c == 1) { a.val_s[1] += s1; a.val_q[1] += s2; }
+      if (c == 2) { a.val_s[2] += s1; a.val_q[2] += s2; }
+    }
+  } else if (MASKMODE == 0) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      a.val_s[c] = a.raw_s[c];
+      a.val_q[c] = a.raw_q[c];
     }
   }
-  raw_s = warp_sum_u64(raw_s);
-  raw_q = warp_sum_u64(raw_q);
-  val_s = warp_sum_u64(val_s);
-  val_q = warp_sum_u64(val_q);
-  nvalid = warp_sum_u64(nvalid);
+  uint64_t r[13];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    r[c] = warp_sum_u64(a.val_s[c]);
+    r[3 + c] = warp_sum_u64(a.val_q[c]);
+    r[6 + c] = warp_sum_u64(a.raw_s[c]);
+    r[9 + c] = warp_sum_u64(a.raw_q[c]);
+  }
+  r[12] = warp_sum_u64(a.nvalid);
   if (lane == 0) {
-    camx_band_stat *o = p.out + (img * 2 + side) * p.K + k;
-    o->sum[ch] = val_s;
-    o->sumsq[ch] = val_q;
-    o->raw_sum[ch] = raw_s;
-    o->raw_sumsq[ch] = raw_q;
-    if (ch == 0) {
-      o->area = npix;
-      o->valid = static_cast<int64_t>(nvalid);
-    }
+#pragma unroll
+    for (int i = 0; i < 13; ++i) part[warp][i] = r[i];
   }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < 13; ++i)
+      for (int w2 = 1; w2 < kStatsWarps; ++w2) r[i] += part[w2][i];
+    camx_band_stat o;
+    o.area = static_cast<int64_t>(rows) * p.bw;
+    o.valid = static_cast<int64_t>(r[12]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      o.sum[c] = r[c];
+      o.sumsq[c] = r[3 + c];
+      o.raw_sum[c] = r[6 + c];
+      o.raw_sumsq[c] = r[9 + c];
+    }
+    p.out[unit] = o;
+  }
+  if (FUSE) fused_solve_tail(p, p.img_begin * 2 * p.K + unit);
 }
 
-template <bool HIST, int MASKMODE>
-static void launch_stats(const StatsParams &p, int64_t n_units, cudaStream_t s) {
-  const size_t smem = HIST ? kStatsWarps * kCounterWords * sizeof(uint32_t) : 0;
+template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
+static void launch_stats(const StatsParams &p, cudaStream_t s) {
+  const int warps = kStatsWarps;
+  const size_t smem = HIST ? static_cast<size_t>(warps) * kCounterWords * sizeof(uint32_t) : 0;
   if (HIST) {
-    cudaFuncSetAttribute(band_stats_kernel<HIST, MASKMODE>,
+    cudaFuncSetAttribute(band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   }
-  band_stats_kernel<HIST, MASKMODE>
-      <<<static_cast<unsigned>(n_units), kStatsWarps * 32, smem, s>>>(p);
+  band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>
+      <<<static_cast<unsigned>(p.n_units), warps * 32, smem, s>>>(p);
+}
+
+template <bool HIST, int MASKMODE, bool FUSE = false>
+static void launch_stats_q(const StatsParams &p, bool quad, cudaStream_t s) {
+  if (quad)
+    launch_stats<HIST, MASKMODE, true, FUSE>(p, s);
+  else
+    launch_stats<HIST, MASKMODE, false, FUSE>(p, s);
 }
 
 // ---- moments --------------------------------------------------------------
@@ -250,20 +440,22 @@ extern "C" int camx_band_stats(const uint8_t *images, const uint8_t *prev_images
   p.t_diff = t_diff;
   p.img_bytes = static_cast<int64_t>(height) * width * 3;
   p.mask_bytes = static_cast<int64_t>(height) * width;
+  p.n_units = n_images * 2 * blocks;
   p.out = stats_out;
   p.hist = hist_out;
-  const int64_t units = n_images * 2 * blocks;
   cudaStream_t s = as_stream(stream);
   const int mm = prev_images ? 2 : (excl_masks ? 1 : 0);
-  const bool h = hist_out != nullptr;
-  if (h) {
-    if (mm == 0) launch_stats<true, 0>(p, units, s);
-    if (mm == 1) launch_stats<true, 1>(p, units, s);
-    if (mm == 2) launch_stats<true, 2>(p, units, s);
+  auto al4 = [](const void *x) { return reinterpret_cast<uintptr_t>(x) % 4 == 0; };
+  const bool quad = (width % 4 == 0) && (band_width % 4 == 0) && al4(images) &&
+                    (mm != 2 || al4(prev_images)) && (mm != 1 || al4(excl_masks));
+  if (hist_out != nullptr) {
+    if (mm == 0) launch_stats_q<true, 0>(p, quad, s);
+    if (mm == 1) launch_stats_q<true, 1>(p, quad, s);
+    if (mm == 2) launch_stats_q<true, 2>(p, quad, s);
   } else {
-    if (mm == 0) launch_stats<false, 0>(p, units, s);
-    if (mm == 1) launch_stats<false, 1>(p, units, s);
-    if (mm == 2) launch_stats<false, 2>(p, units, s);
+    if (mm == 0) launch_stats_q<false, 0>(p, quad, s);
+    if (mm == 1) launch_stats_q<false, 1>(p, quad, s);
+    if (mm == 2) launch_stats_q<false, 2>(p, quad, s);
   }
   return launch_status();
 }
@@ -277,5 +469,72 @@ extern "C" int camx_band_moments(const camx_band_stat *stats, int64_t n_records,
   band_moments_kernel<<<static_cast<unsigned>(blocks > 4096 ? 4096 : blocks), 128, 0,
                         as_stream(stream)>>>(stats, n_records, use_raw, mean_out, std_out,
                                              valid_out, area_out);
+  return launch_status();
+}
+
+extern "C" int camx_band_stats_solve(const uint8_t *images, const uint8_t *prev_images,
+                                     int32_t n_batch, int32_t n_cams, int32_t frame_begin,
+                                     int32_t frame_count, int32_t height, int32_t width,
+                                     int32_t band_width, int32_t t_diff, int32_t wrap,
+                                     const camx_solve_config *cfg, const double *prev_gain,
+                                     const double *prev_offset, camx_band_stat *stats,
+                                     uint32_t *hist, double *gain_out, double *offset_out,
+                                     uint8_t *fit_ok_out, int32_t *counters, void *stream) {
+  if (cfg == nullptr || images == nullptr || stats == nullptr || counters == nullptr ||
+      gain_out == nullptr || offset_out == nullptr)
+    return CAMX_EINVAL;
+  const int32_t blocks = cfg->blocks;
+  if (n_batch < 1 || n_cams < 2 || frame_begin < 0 || frame_count < 0 ||
+      frame_begin + frame_count > n_batch)
+    return CAMX_EINVAL;
+  if (height < 1 || width < 1 || band_width < 1 || band_width > width / 2) return CAMX_EINVAL;
+  if (blocks < 1 || blocks > height) return CAMX_EINVAL;
+  if (cfg->mode < CAMX_MODE_STANDARD || cfg->mode > CAMX_MODE_SMOOTHING) return CAMX_EINVAL;
+  if (cfg->have_prev_maps && (prev_gain == nullptr || prev_offset == nullptr)) return CAMX_EINVAL;
+  if (hist != nullptr && (reinterpret_cast<uintptr_t>(hist) % 16) != 0) return CAMX_EALIGN;
+  if (frame_count == 0) return CAMX_OK;
+  StatsParams p{};
+  p.img = images;
+  p.prev = prev_images;
+  p.H = height;
+  p.W = width;
+  p.bw = band_width;
+  p.K = blocks;
+  p.bh = height / blocks;
+  p.img_bytes = static_cast<int64_t>(height) * width * 3;
+  p.mask_bytes = static_cast<int64_t>(height) * width;
+  const int64_t first = static_cast<int64_t>(frame_begin) * n_cams;
+  p.n_units = static_cast<int64_t>(frame_count) * n_cams * 2 * blocks;
+  p.out = stats + first * 2 * blocks;
+  p.hist = hist == nullptr ? nullptr : hist + first * 2 * blocks * 768;
+  p.img_begin = first;
+  p.n_cams = n_cams;
+  p.wrap = wrap;
+  p.counters = counters;
+  p.solve.stats = stats;
+  p.solve.B = n_batch;
+  p.solve.N = n_cams;
+  p.solve.S = wrap ? n_cams : n_cams - 1;
+  p.solve.K = blocks;
+  p.solve.wrap = wrap;
+  p.solve.cfg = *cfg;
+  p.solve.prev_gain = prev_gain;
+  p.solve.prev_offset = prev_offset;
+  p.solve.gain = gain_out;
+  p.solve.offset = offset_out;
+  p.solve.fit_ok = fit_ok_out;
+  p.t_diff = t_diff;
+  cudaStream_t s = as_stream(stream);
+  auto al4 = [](const void *x) { return reinterpret_cast<uintptr_t>(x) % 4 == 0; };
+  const bool mm2 = prev_images != nullptr;
+  const bool quad = (width % 4 == 0) && (band_width % 4 == 0) && al4(images) &&
+                    (!mm2 || al4(prev_images));
+  if (hist != nullptr) {
+    if (mm2) launch_stats_q<true, 2, true>(p, quad, s);
+    else launch_stats_q<true, 0, true>(p, quad, s);
+  } else {
+    if (mm2) launch_stats_q<false, 2, true>(p, quad, s);
+    else launch_stats_q<false, 0, true>(p, quad, s);
+  }
   return launch_status();
 }

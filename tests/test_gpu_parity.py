@@ -344,17 +344,24 @@ def test_long_band_counter_flush():
     np.testing.assert_allclose(s.std, sd, rtol=1e-12)
 
 
+PATHS = {"pdl": dict(), "fused_k12": dict(fused_stats_solve=True),
+         "separate": dict(fused=False), "chunked": dict(fused=False, pipeline_chunks=2)}
+
+
 @pytest.mark.parametrize("mode,om", [(xp.ExposureMode.STANDARD, O.STANDARD),
                                      (xp.ExposureMode.OBJECT_REMOVAL, O.OBJECT_REMOVAL),
                                      (xp.ExposureMode.SMOOTHING, O.SMOOTHING)])
 @pytest.mark.parametrize("wrap", [False, True])
-def test_array_vs_oracle_synthetic(mode, om, wrap):
+@pytest.mark.parametrize("path", sorted(PATHS))
+def test_array_vs_oracle_synthetic(mode, om, wrap, path):
     N, H, W, B = 4, 120, 160, 5
     frames = np.stack([O.synthetic_array(N, H, W, seed=11, objects=3, frame_index=t)
                        for t in range(B)])
     cfg = xp.ExposureConfig(band_width=16, blocks=6, min_band_pixels=64)
     ocfg = O.Cfg(band_width=16, blocks=6, min_band_pixels=64)
     ac = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap, histograms=True)
+    for k, v in PATHS[path].items():
+        setattr(ac, k, v)
     # two calls (3 + 2 frames) exercise the carried tick-loop state
     r1 = ac.correct(torch.from_numpy(frames[:3]).cuda())
     out1, g1 = r1.out.cpu().numpy(), r1.gain.cpu().numpy()
