@@ -32,6 +32,7 @@ WORKLOADS = {
     "config2": (8, 1536, 2048, 30, "8 cameras x 2048x1536 (25.17 MP array), 30-frame batch"),
     "config3": (8, 1536, 2048, 30, "8-camera 25 MP array sharded one camera group per GPU"),
     "config4": (14, 2160, 3840, 16, "14-camera 360-degree 4K array (wrap seam)"),
+    "config5": (8, 1536, 2048, 30, "config 2 + 36 attention tiles/array-frame, 960 -> 416x416"),
 }
 FALLBACK_HBM_GBS = 6650.0
 
@@ -224,9 +225,20 @@ def run_camx(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    tiles_mode = name == "config5"
+    tiles_buf = None
+    if tiles_mode:
+        n_tiles = len(ac.tile_windows(960)) * B
+        tiles_buf = torch.empty((n_tiles, 416, 416, 3), dtype=torch.uint8, device="cuda")
+
+    def step():
+        if tiles_mode:
+            return ac.correct_and_tile(frames, out=out, tiles=tiles_buf, stream=stream)[0]
+        return ac.correct(frames, out, stream=stream)
+
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            ac.correct(frames, out, stream=stream)
+            step()
     barrier()
 
     # timed region: K steps, events on the launching stream, every camx
@@ -236,9 +248,10 @@ def run_camx(args):
     orig_call = _lib.call
 
     def traced_call(fn, *a):
-        if fn == "camx_correct_batch":
-            # fused K1+K2 (x2 launches for OBJECT_REMOVAL with B > 1) + K3
+        if fn in ("camx_correct_batch", "camx_correct_batch_tiles"):
+            # K1 (x2 for OBJECT_REMOVAL with B > 1) + K2 + K3 (+ tile fix-up)
             n_launch[0] += 3 if (mode is ExposureMode.OBJECT_REMOVAL and a[3] > 1) else 2
+            n_launch[0] += 1 if fn == "camx_correct_batch" else 2
         elif fn.startswith("camx_"):
             n_launch[0] += 1
         orig_call(fn, *a)
@@ -252,7 +265,7 @@ def run_camx(args):
             start.record(stream)
             with torch.cuda.stream(stream):
                 for _ in range(args.steps):
-                    res = ac.correct(frames, out, stream=stream)
+                    res = step()
             stop.record(stream)
             stop.synchronize()
             barrier()
@@ -302,7 +315,7 @@ def run_camx(args):
 
     # e2e through the public host API (pinned host in -> pinned host out)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not tiles_mode:
         Be = min(args.e2e_batch, B)
         host_in = frames[:Be].cpu().pin_memory()
         host_out = torch.empty_like(host_in).pin_memory()
@@ -359,6 +372,7 @@ def run_camx(args):
             "data": "synthetic (on-device panorama + per-camera affine distortion + moving objects)",
             "array_frames_per_sec": round(afps, 2),
             "config": {"workload": f"{name}: {desc}", "batch": B, "mode": mode.value,
+                       "tiles_per_step": (tiles_buf.shape[0] if tiles_mode else 0),
                        "cameras_per_gpu": count, "frame": f"{W}x{H}",
                        "step": "K1 band stats + K2 seam solve + K3 apply per array-frame",
                        "l2": "inputs larger than L2 (batch >> 126 MB)",

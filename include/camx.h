@@ -233,17 +233,37 @@ int camx_tiles(const uint8_t *images, int32_t n_cams, int32_t height,
                int32_t size, int32_t out_size, uint8_t *tiles_out,
                void *stream);
 
-/* Fused stage 3 + 4b (config 5): apply the array correction AND emit the
- * tiles from the corrected pixels in one pass over the raw frames.
- * Arguments as camx_apply_array (cam_begin = 0, cam_count = n_cams) and
- * camx_tiles. */
+/* Stage 3 + 4b (config 5): apply the array correction AND cut the tiles
+ * from the corrected pixels.  When the geometry allows (aligned rows, at
+ * most 64 windows per array-frame, out_size <= 3*size) this is ONE pass
+ * over the raw frames: the apply kernel resamples every tile row whose
+ * source rows it holds in shared memory, and a small fix-up kernel
+ * completes the outputs whose taps straddle two CTAs from the corrected
+ * frame.  Otherwise apply, then camx_tiles on `out`.  windows: device int32
+ * [n_tiles][3] (batch index, x, y) GROUPED BY batch index; frame_off:
+ * device int32 [n_batch+1] first tile of each array-frame (NULL disables
+ * fusion); max_tiles_per_frame: the largest group.  Maps as
+ * camx_apply_array (cam_begin = 0, cam_count = n_cams). */
 int camx_correct_and_tile(const uint8_t *images, uint8_t *out,
                           int32_t n_batch, int32_t n_cams, int32_t wrap,
                           int32_t height, int32_t width, int32_t blocks,
                           const double *gain, const double *offset,
-                          const int32_t *windows, int32_t n_tiles,
+                          const int32_t *windows, const int32_t *frame_off,
+                          int32_t n_tiles, int32_t max_tiles_per_frame,
                           int32_t size, int32_t out_size, uint8_t *tiles_out,
                           void *stream);
+
+/* camx_correct_batch + tiles: K1, K2 (PDL), fused apply+tiles (PDL). */
+int camx_correct_batch_tiles(
+    const uint8_t *images, uint8_t *out, const uint8_t *prev_frame,
+    int32_t n_batch, int32_t n_cams, int32_t wrap, int32_t height,
+    int32_t width, int32_t band_width, int32_t t_diff,
+    const camx_solve_config *cfg, const double *prev_gain,
+    const double *prev_offset, camx_band_stat *stats, uint32_t *hist,
+    double *gain_out, double *offset_out, uint8_t *fit_ok_out,
+    const int32_t *windows, const int32_t *frame_off, int32_t n_tiles,
+    int32_t max_tiles_per_frame, int32_t size, int32_t out_size,
+    uint8_t *tiles_out, void *stream);
 
 /* ---- next: seam quality metric ------------------------------
  * seam_cost (exposure.py:417-445) of n_pairs (left, right) image pairs of

@@ -72,7 +72,10 @@ SIGNATURES = {
     "camx_mask_diff": [P, P, I64, I32, P, P],
     "camx_window_counts": [P, P, P, I32, I32, I32, I32, P, I32, I32, P, P],
     "camx_tiles": [P, I32, I32, I32, P, I32, I32, I32, P, P],
-    "camx_correct_and_tile": [P, P, I32, I32, I32, I32, I32, I32, P, P, P, I32, I32, I32, P, P],
+    "camx_correct_and_tile": [P, P, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, I32, I32, I32,
+                              P, P],
+    "camx_correct_batch_tiles": [P, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P, P,
+                                 P, P, P, I32, I32, I32, I32, P, P],
     "camx_seam_cost": [P, P, I64, I32, I32, I32, I32, P, P],
 }
 

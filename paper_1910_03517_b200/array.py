@@ -113,7 +113,8 @@ class ArrayCorrector:
         return buf
 
     # ------------------------------------------------------------ device path
-    def correct(self, frames, out=None, *, stream=None, prev_frames=None) -> CorrectResult:
+    def correct(self, frames, out=None, *, stream=None, prev_frames=None,
+                _tile_args=None) -> CorrectResult:
         """Correct a (B, cam_count, H, W, 3) uint8 CUDA tensor (this GPU's
         cameras); returns device results.
 
@@ -137,7 +138,7 @@ class ArrayCorrector:
         removal = self.mode is ExposureMode.OBJECT_REMOVAL
         pf = prev_frames if prev_frames is not None else self._prev_frame
         if self.exchange is None and self.S > 0 and self.pipeline_chunks <= 1 and self.fused:
-            self._correct_fused(frames, out, buf, _dev.stream_handle(main), pf)
+            self._correct_fused(frames, out, buf, _dev.stream_handle(main), pf, _tile_args)
             return self._finish(frames, out, buf, main, removal)
         # Chunked pipeline: K1+K2 of chunk i+1 run on a side stream while K3
         # of chunk i streams on `main`; the tick-loop state flows between
@@ -197,7 +198,7 @@ class ArrayCorrector:
     # of K1 -> K2 (PDL); measured slower on B200 (96 regs, serial tail)
     fused_stats_solve = os.environ.get("CAMX_FUSED_K12", "0") == "1"
 
-    def _correct_fused(self, frames, out, buf, sh, pf):
+    def _correct_fused(self, frames, out, buf, sh, pf, tile_args=None):
         """camx_correct_batch: fused K1+K2 (last-arriver solve) + K3 (PDL)."""
         cfg = self.cfg
         B = frames.shape[0]
@@ -227,12 +228,15 @@ class ArrayCorrector:
                           0, B, *common)
             self._apply(frames, out, buf, 0, B, sh)
             return
-        _lib.call("camx_correct_batch", frames.data_ptr(), out.data_ptr(),
-                  _dev.ptr(pf) if removal else None, B, self.n_cams, int(self.wrap),
-                  self.height, self.width, cfg.band_width, cfg.t_diff, ctypes.byref(sc),
-                  _dev.ptr(pg), _dev.ptr(po), buf["stats"].data_ptr(), _dev.ptr(buf["hist"]),
-                  buf["gain"].data_ptr(), buf["offset"].data_ptr(), buf["fit_ok"].data_ptr(),
-                  buf["counters"].data_ptr(), sh)
+        common = (frames.data_ptr(), out.data_ptr(), _dev.ptr(pf) if removal else None, B,
+                  self.n_cams, int(self.wrap), self.height, self.width, cfg.band_width,
+                  cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),
+                  buf["stats"].data_ptr(), _dev.ptr(buf["hist"]), buf["gain"].data_ptr(),
+                  buf["offset"].data_ptr(), buf["fit_ok"].data_ptr())
+        if tile_args is not None:
+            _lib.call("camx_correct_batch_tiles", *common, *tile_args, sh)
+        else:
+            _lib.call("camx_correct_batch", *common, buf["counters"].data_ptr(), sh)
 
     def _side_stream(self):
         if getattr(self, "_side", None) is None:
@@ -292,6 +296,59 @@ class ArrayCorrector:
         _lib.call("camx_apply_array", frames.data_ptr() + off, out.data_ptr() + off, hi - lo,
                   self.cam_begin, N, self.n_cams, int(self.wrap), H, W, self.K,
                   buf["gain"][lo].data_ptr(), buf["offset"][lo].data_ptr(), sh)
+
+    # ------------------------------------------------------------ tiles
+    def tile_windows(self, size: int, overlap: float = 0.0):
+        """Sliding-window origins over one array-frame's mosaic
+        (attention.sliding_window_plan, attention.py:66-86)."""
+        from .attention import window_origins
+        return window_origins((self.n_cams * self.width, self.height), size, overlap)
+
+    def correct_and_tile(self, frames, windows=None, *, size: int = 960, out_size: int = 416,
+                         out=None, tiles=None, stream=None):
+        """Correct a batch and cut detector tiles from the corrected mosaic of
+        every array-frame (config 5).  windows: (x, y) origins applied to every
+        frame (default: the sliding plan) or (b, x, y) triples.  Returns
+        (CorrectResult, tiles uint8 (T, out_size, out_size, 3))."""
+        t = _dev.require_cuda()
+        if self.cam_count != self.n_cams:
+            raise ValueError("tiles need the whole array on one GPU")
+        B = frames.shape[0] if frames.dim() == 5 else 1
+        wins = self.tile_windows(size) if windows is None else list(windows)
+        if wins and len(wins[0]) == 2:
+            wins = [(b, x, y) for b in range(B) for (x, y) in wins]
+        for (b, x, y) in wins:
+            if not (0 <= b < B and 0 <= x and 0 <= y and x + size <= self.n_cams * self.width
+                    and y + size <= self.height):
+                raise ValueError(f"window ({b}, {x}, {y}, {size}) outside the array")
+        # grouped by array-frame (the fused kernel's contract), order kept within a frame
+        wins = sorted(wins, key=lambda w: w[0])
+        key = ("tiles", B, tuple(wins))
+        wd = self._bufs.get(key)
+        if wd is None:
+            counts = np.bincount(np.asarray([w[0] for w in wins], dtype=np.int64), minlength=B)
+            off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+            wd = (_dev.to_device(np.asarray(wins, dtype=np.int32).reshape(-1, 3)),
+                  _dev.to_device(off), int(counts.max()) if len(wins) else 0)
+            self._bufs[key] = wd
+        T = len(wins)
+        if tiles is None:
+            tiles = t.empty((T, out_size, out_size, 3), dtype=t.uint8, device="cuda")
+        tile_args = (wd[0].data_ptr(), wd[1].data_ptr(), T, wd[2], int(size), int(out_size),
+                     tiles.data_ptr())
+        if self.exchange is None and self.S > 0 and self.fused and not self.fused_stats_solve:
+            if frames.dim() == 4:
+                frames = frames[None]
+            if out is None:
+                out = t.empty_like(frames)
+            res = self.correct(frames, out, stream=stream, _tile_args=tile_args)
+        else:
+            res = self.correct(frames, out, stream=stream)
+            if T:
+                _lib.call("camx_tiles", res.out.data_ptr(), self.n_cams, self.height, self.width,
+                          wd[0].data_ptr(), T, int(size), int(out_size), tiles.data_ptr(),
+                          _dev.stream_handle(stream))
+        return res, tiles
 
     # ------------------------------------------------------------ results
     def maps(self, result: CorrectResult, b: int = -1, camera_ids=None) -> list[SeamMaps]:

@@ -22,7 +22,7 @@
 // Since clamp bounds are integers, clip(rint(y)) == rint(clip(y)).
 #include <cstdlib>
 
-#include "camx_common.cuh"
+#include "camx_resize.cuh"
 
 namespace camx {
 
@@ -76,36 +76,49 @@ __device__ __forceinline__ void map_ptrs(const ApplyParams &p, int64_t img, cons
   }
 }
 
-// Exact float32 (M, A) of one (column, channel, block); identity outside
-// the lam > 0 half of each present map.
-__device__ __forceinline__ void coef_f32(int col, int ch, int k, int W, const double *gl,
-                                         const double *bl, const double *gr, const double *br,
-                                         float &m32, float &a32) {
+// lam of one column (exposure.py:347-355) and which map it uses: 0 = LEFT
+// role (seam at the right edge), 1 = RIGHT role, -1 = identity (outside the
+// lam > 0 half of every present map).
+__device__ __forceinline__ double col_lambda(int col, int W, bool have_l, bool have_r, int &role) {
   const double c0 = (W - 1) * 0.5;
   const double colf = static_cast<double>(col);
-  double lam = 0.0, g = 1.0, b = 0.0;
-  bool have = false;
-  if (gl != nullptr && 2 * col > W - 1) {
+  double lam = 0.0;
+  role = -1;
+  if (have_l && 2 * col > W - 1) {
     lam = __ddiv_rn(__dsub_rn(colf, c0), __dsub_rn(static_cast<double>(W - 1), c0));
-    g = gl[k * 3 + ch];
-    b = bl[k * 3 + ch];
-    have = true;
-  } else if (gr != nullptr && 2 * col < W - 1) {
+    role = 0;
+  } else if (have_r && 2 * col < W - 1) {
     lam = __ddiv_rn(__dsub_rn(c0, colf), c0);
-    g = gr[k * 3 + ch];
-    b = br[k * 3 + ch];
-    have = true;
+    role = 1;
   }
-  if (!have || !(lam > 0.0)) {
+  if (!(lam > 0.0)) role = -1;
+  return fmin(lam, 1.0);
+}
+
+// Exact float32 (M, A) of one (column, channel, block) given its lam/role.
+__device__ __forceinline__ void coef_from_lam(double lam, int role, int k, int ch,
+                                              const double *gl, const double *bl,
+                                              const double *gr, const double *br, float &m32,
+                                              float &a32) {
+  if (role < 0) {
     m32 = 1.0f;
     a32 = 0.0f;
     return;
   }
-  lam = fmin(lam, 1.0);
+  const double g = role == 0 ? gl[k * 3 + ch] : gr[k * 3 + ch];
+  const double b = role == 0 ? bl[k * 3 + ch] : br[k * 3 + ch];
   const double M = __dadd_rn(1.0, __dmul_rn(lam, __dsub_rn(g, 1.0)));
   const double A = __dmul_rn(lam, b);
   m32 = __double2float_rn(M);
   a32 = __double2float_rn(A);
+}
+
+__device__ __forceinline__ void coef_f32(int col, int ch, int k, int W, const double *gl,
+                                         const double *bl, const double *gr, const double *br,
+                                         float &m32, float &a32) {
+  int role;
+  const double lam = col_lambda(col, W, gl != nullptr, gr != nullptr, role);
+  coef_from_lam(lam, role, k, ch, gl, bl, gr, br, m32, a32);
 }
 
 // ---------------------------------------------------------------- fast path
@@ -261,7 +274,127 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
-__global__ void __launch_bounds__(kApplyThreads, 4) apply_tma_kernel(const ApplyParams p) {
+// Tile fusion (config 5): the corrected rows of every stage are written back
+// into their ring slot; each output row of each attention tile whose two
+// source rows the CTA holds (the previous stage's last row stays resident:
+// a slot is refilled one stage late) is resampled from shared memory for
+// the output columns whose two column taps are whole pixels of the CTA's
+// byte range.  Outputs whose taps straddle CTAs are produced afterwards by
+// tile_fixup_kernel from the corrected frame.
+struct TileFuse {
+  const int32_t *wins;       // [T][3] (batch, x, y), grouped by batch
+  const int32_t *frame_off;  // [B+1] first tile of each array-frame
+  uint8_t *tiles;            // [T][out][out][3]
+  int32_t size, out;
+  float scale;
+};
+constexpr int kFuseMaxWin = 64;  // windows per array-frame the fused path accepts
+// downscale/crop only (out <= size): a source row is the second tap of at
+// most one output row per window, so a 2-row stage has <= 2 hits per window
+constexpr int kFuseMaxHits = 2 * kFuseMaxWin;
+
+struct FuseSmem {  // carved from dynamic shared memory after the ring
+  int16_t *i0, *i1;
+  uint32_t *wpk;           // (256 - w1) | w1 << 16: dp2a operand
+  int32_t *rstart, *rlen;  // output rows whose second source row is r
+  int4 *win;               // intersecting windows: (tile, x0, y0, lo | hi << 16)
+  int4 *hit;               // 2 buffers x kFuseMaxHits x 2 int4 (see build_hits)
+  int32_t *counts;         // [0] n_win, [1]/[2] hits, [3]/[4] items of buffer 0 / 1
+};
+
+// Resample one hit (an output row segment [lo, hi) of one tile) from the
+// corrected source rows ra (first tap row) and rb (second tap row) in shared
+// memory; threads t, t + nt, ... of the group, kWsUnroll independent pixels
+// per iteration (all shared loads hoisted for ILP).  Per pixel: the 6 bytes
+// of the two column taps (adjacent pixels) of each row via 3 aligned words
+// + funnel shift, channel pairs by PRMT, horizontal blend by dp2a, vertical
+// by IMAD, round half up (camx_resize.cuh: bilerp_fx).  kWsUnroll > 1 is
+// for the warp-specialised kernel (latency-bound resampler warps).
+template <int kWsUnroll>
+__device__ __forceinline__ void resample_hit(const uint8_t *ra, const uint8_t *rb, uint32_t wyp,
+                                             int xc3, uint8_t *trow, int lo, int hi, int t,
+                                             int nt, const FuseSmem &fs) {
+  const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
+  for (int ox0 = lo + t; ox0 < hi; ox0 += nt * kWsUnroll) {
+    uint32_t wa[kWsUnroll][3], wb[kWsUnroll][3], wx[kWsUnroll], shv[kWsUnroll];
+#pragma unroll
+    for (int u = 0; u < kWsUnroll; ++u) {
+      const int ox = min(ox0 + u * nt, hi - 1);
+      wx[u] = fs.wpk[ox];
+      const int la = xc3 + 3 * fs.i0[ox];
+      shv[u] = (la & 3) * 8;
+      const uint32_t *pa = reinterpret_cast<const uint32_t *>(ra + (la & ~3));
+      const uint32_t *pb = reinterpret_cast<const uint32_t *>(rb + (la & ~3));
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        wa[u][i] = pa[i];
+        wb[u][i] = pb[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kWsUnroll; ++u) {
+      const int ox = ox0 + u * nt;
+      if (ox >= hi) break;
+      const uint32_t alo = __funnelshift_r(wa[u][0], wa[u][1], shv[u]);
+      const uint32_t ahi = __funnelshift_r(wa[u][1], wa[u][2], shv[u]);
+      const uint32_t blo = __funnelshift_r(wb[u][0], wb[u][1], shv[u]);
+      const uint32_t bhi = __funnelshift_r(wb[u][1], wb[u][2], shv[u]);
+      uint8_t *o = trow + 3 * ox;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
+        const uint32_t v0 = __dp2a_lo(wx[u], __byte_perm(alo, ahi, sel), 0u);
+        const uint32_t v1 = __dp2a_lo(wx[u], __byte_perm(blo, bhi, sel), 0u);
+        o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+      }
+    }
+  }
+}
+
+// Warp 0: records of the output rows whose second source row lies in stage
+// `st` (rows r0 + 2st, r0 + 2st + 1) and whose first source row is in this
+// CTA: smem offsets of both (corrected) source rows, packed vertical
+// weights, window origin in segment bytes, the tile row pointer and the
+// output column range [lo, hi) whose taps are whole pixels of this CTA.
+__device__ __forceinline__ void build_hits(const FuseSmem &fs, const TileFuse &q,
+                                           const ApplyParams &p, int st, int r0, int nrows,
+                                           int cam, int cb0) {
+  const int lane = threadIdx.x & 31;
+  const int rr = min(kTmaRows, nrows - st * kTmaRows);
+  const int rs0 = r0 + st * kTmaRows;
+  int4 *hits = fs.hit + (st & 1) * kFuseMaxHits * 2;
+  int *cnt = &fs.counts[1 + (st & 1)];
+  if (lane == 0) *cnt = 0;
+  __syncwarp();
+  const int nwin = fs.counts[0];
+  for (int e = lane; e < nwin * rr; e += 32) {
+    const int4 w = fs.win[e / rr];
+    const int R = rs0 + e % rr;
+    const int lr = R - w.z;
+    if (lr < 0 || lr >= q.size) continue;
+    const int o0 = fs.rstart[lr], n = fs.rlen[lr];
+    for (int oy = o0; oy < o0 + n; ++oy) {
+      const int Ra = w.z + fs.i0[oy];
+      if (Ra < r0) continue;  // first tap row belongs to the previous CTA
+      const int h = atomicAdd(cnt, 1);
+      auto off = [&](int Rw) {
+        const int sidx = (Rw - r0) / kTmaRows, ri = (Rw - r0) % kTmaRows;
+        return ((sidx % kTmaStages) * kTmaRows + ri) * kApplyThreads * 16;
+      };
+      const uint64_t trow = reinterpret_cast<uint64_t>(
+          q.tiles + (static_cast<int64_t>(w.x) * q.out + oy) * q.out * 3);
+      hits[2 * h] = make_int4(off(Ra), off(R), static_cast<int>(fs.wpk[oy]),
+                              3 * (w.y - cam * p.W) - cb0);
+      hits[2 * h + 1] = make_int4(static_cast<int>(trow & 0xFFFFFFFFu), static_cast<int>(trow >> 32),
+                                  w.w, 0);
+    }
+  }
+  __syncwarp();
+}
+
+template <bool TILES>
+__global__ void __launch_bounds__(kApplyThreads, 4)
+    apply_tma_kernel(const ApplyParams p, const TileFuse q) {
   extern __shared__ __align__(128) uint4 ring[];  // [kTmaStages][kTmaRows][kApplyThreads]
   __shared__ __align__(8) uint64_t full[kTmaStages];
   int64_t item = blockIdx.x;
@@ -300,6 +433,71 @@ __global__ void __launch_bounds__(kApplyThreads, 4) apply_tma_kernel(const Apply
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int st = 0; st < min(kTmaStages, nst); ++st) issue(st);
   }
+
+  // ---- tile fusion prologue (independent of the maps: overlaps the PDL wait)
+  FuseSmem fs{};
+  int cam = 0, cb0 = 0, px_lo = 0, px_hi = 0;
+  int64_t bfr = 0;
+  if (TILES) {
+    uint8_t *base = reinterpret_cast<uint8_t *>(ring + kTmaStages * kTmaRows * kApplyThreads);
+    fs.i0 = reinterpret_cast<int16_t *>(base);
+    fs.i1 = fs.i0 + q.out;
+    fs.wpk = reinterpret_cast<uint32_t *>(base + ((4 * q.out + 15) & ~15));
+    fs.rstart = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(fs.wpk) + ((4 * q.out + 15) & ~15));
+    fs.rlen = fs.rstart + q.size;
+    fs.win = reinterpret_cast<int4 *>(reinterpret_cast<uint8_t *>(fs.rlen) + ((4 * q.size + 15) & ~15));
+    fs.hit = fs.win + kFuseMaxWin;
+    fs.counts = reinterpret_cast<int32_t *>(fs.hit + 2 * kFuseMaxHits * 2);
+    bfr = img / p.cam_count;
+    cam = p.cam_begin + static_cast<int>(img % p.cam_count);
+    cb0 = cg * kApplyThreads * 16;
+    px_lo = (cb0 + 2) / 3;                       // first whole pixel of the byte range
+    px_hi = (cb0 + static_cast<int>(seg)) / 3;   // one past the last whole pixel
+    for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
+      int a, b, w1;
+      src_coord_w(i, q.scale, q.size, a, b, w1);
+      fs.i0[i] = static_cast<int16_t>(a);
+      fs.i1[i] = static_cast<int16_t>(b);
+      fs.wpk[i] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
+    }
+    for (int r = threadIdx.x; r < q.size; r += blockDim.x) {
+      fs.rstart[r] = 0x7FFFFFFF;
+      fs.rlen[r] = 0;
+    }
+    if (threadIdx.x == 0) fs.counts[0] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
+      const int r = fs.i1[i];
+      atomicMin(&fs.rstart[r], i);
+      atomicAdd(&fs.rlen[r], 1);
+    }
+    __syncthreads();
+    // windows of this array-frame that overlap the CTA region (mosaic coords),
+    // with the contiguous range [lo, hi) of output columns whose two column
+    // taps are whole pixels of this CTA (i0, i1 are nondecreasing in ox)
+    const int w_lo = q.frame_off[bfr], w_hi = q.frame_off[bfr + 1];
+    const int mx0 = cam * p.W + px_lo, mx1 = cam * p.W + px_hi;
+    for (int t = w_lo + threadIdx.x; t < w_hi; t += blockDim.x) {
+      const int x0 = q.wins[3 * t + 1], y0 = q.wins[3 * t + 2];
+      if (x0 < mx1 && x0 + q.size > mx0 && y0 < r1 && y0 + q.size > r0) {
+        const int xc = x0 - cam * p.W;
+        int lo = 0, hi = q.out;  // first ox with xc + i0 >= px_lo
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (xc + fs.i0[mid] >= px_lo) hi = mid; else lo = mid + 1;
+        }
+        int lo2 = lo, hi2 = q.out;  // first ox with xc + i1 >= px_hi
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          if (xc + fs.i1[mid] >= px_hi) hi2 = mid; else lo2 = mid + 1;
+        }
+        if (lo2 > lo) {
+          const int slot = atomicAdd(&fs.counts[0], 1);
+          fs.win[slot] = make_int4(t, x0, y0, lo | (lo2 << 16));
+        }
+      }
+    }
+  }
   __syncthreads();
   // maps come from the preceding stats/solve grid (programmatic dependent
   // launch): only the raw-pixel prefetch above may run before it completes
@@ -310,10 +508,12 @@ __global__ void __launch_bounds__(kApplyThreads, 4) apply_tma_kernel(const Apply
   map_ptrs(p, img, gl, bl, gr, br);
   Coef16 cf;
   if (active) {
+    // per sub-pixel (a per-column lambda cache measured ~6% slower end to
+    // end on B200: tools/ab_k3.py)
+    float m[16], a[16];
     const int q0 = j * 16;
     int col = q0 / 3;
     int ch = q0 - col * 3;
-    float m[16], a[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       coef_f32(col, ch, k, p.W, gl, bl, gr, br, m[i], a[i]);
@@ -344,10 +544,333 @@ __global__ void __launch_bounds__(kApplyThreads, 4) apply_tma_kernel(const Apply
         if (i < rr) v[i] = ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x];
 #pragma unroll
       for (int i = 0; i < kTmaRows; ++i)
-        if (i < rr) st_stream_v4(dst + static_cast<int64_t>(st * kTmaRows + i) * rb, correct16(v[i], cf));
+        if (i < rr) {
+          const uint4 o = correct16(v[i], cf);
+          st_stream_v4(dst + static_cast<int64_t>(st * kTmaRows + i) * rb, o);
+          if (TILES) ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x] = o;
+        }
     }
-    __syncthreads();  // slot fully consumed
-    if (threadIdx.x == 0 && st + kTmaStages < nst) issue(st + kTmaStages);
+    __syncthreads();  // slot consumed (and, with TILES, corrected rows visible)
+    if (TILES) {
+      // every thread has finished the previous stage's resample (it came
+      // before this barrier): the slot of stage st-2 is free
+      if (threadIdx.x == 0 && st >= 2 && st - 2 + kTmaStages < nst) issue(st - 2 + kTmaStages);
+      // warp 0 builds this stage's hit records, then everyone resamples
+      if (threadIdx.x < 32) build_hits(fs, q, p, st, r0, nrows, cam, cb0);
+      __syncthreads();
+      const int4 *hits = fs.hit + (st & 1) * kFuseMaxHits * 2;
+      const int nhit = fs.counts[1 + (st & 1)];
+      const uint8_t *ringb = reinterpret_cast<const uint8_t *>(ring);
+      for (int hh = 0; hh < nhit; ++hh) {
+        const int4 h0 = hits[2 * hh], h1 = hits[2 * hh + 1];
+        resample_hit<1>(ringb + h0.x, ringb + h0.y, static_cast<uint32_t>(h0.z), h0.w,
+                        reinterpret_cast<uint8_t *>(
+                            (static_cast<uint64_t>(static_cast<uint32_t>(h1.y)) << 32) |
+                            static_cast<uint32_t>(h1.x)),
+                        h1.z & 0xFFFF, h1.z >> 16, threadIdx.x, kApplyThreads, fs);
+      }
+    } else {
+      if (threadIdx.x == 0 && st + kTmaStages < nst) issue(st + kTmaStages);
+    }
+  }
+}
+
+// ---------------------------------------------- warp-specialised fusion
+// CTA = 224 threads.  Warps 0-3 (correctors) run exactly the plain K3 loop
+// over the TMA ring and additionally write each corrected stage back into
+// its ring slot, then arrive on corr[slot].  Warps 4-6 (resamplers) trail:
+// they wait corr[slot], build the stage's hit records (warp 4), resample
+// them (named barrier 1 among the resamplers only) and, once stage st
+// is done, refill the slot of stage st-1 (its last row was stage st's
+// "previous row").  No CTA-wide barrier inside the loop: correctors only
+// ever wait for TMA data.
+constexpr int kWsStages = 8;
+constexpr int kWsResamplers = 96;  // 3 warps (4 + 3 warps x 92 regs: 3 CTAs per SM)
+constexpr int kWsThreads = kApplyThreads + kWsResamplers;
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void build_hits_ws(const FuseSmem &fs, const TileFuse &q,
+                                              const ApplyParams &p, int st, int r0, int nrows,
+                                              int cam, int cb0) {
+  const int lane = threadIdx.x & 31;
+  const int rr = min(kTmaRows, nrows - st * kTmaRows);
+  const int rs0 = r0 + st * kTmaRows;
+  int4 *hits = fs.hit;
+  int *cnt = &fs.counts[1];
+  if (lane == 0) *cnt = 0;
+  __syncwarp();
+  const int nwin = fs.counts[0];
+  for (int e = lane; e < nwin * rr; e += 32) {
+    const int4 w = fs.win[e / rr];
+    const int R = rs0 + e % rr;
+    const int lr = R - w.z;
+    if (lr < 0 || lr >= q.size) continue;
+    const int o0 = fs.rstart[lr], n = fs.rlen[lr];
+    for (int oy = o0; oy < o0 + n; ++oy) {
+      const int Ra = w.z + fs.i0[oy];
+      if (Ra < r0) continue;  // first tap row belongs to the previous CTA
+      const int h = atomicAdd(cnt, 1);
+      auto off = [&](int Rw) {
+        const int sidx = (Rw - r0) / kTmaRows, ri = (Rw - r0) % kTmaRows;
+        return ((sidx % kWsStages) * kTmaRows + ri) * kApplyThreads * 16;
+      };
+      const uint64_t trow = reinterpret_cast<uint64_t>(
+          q.tiles + (static_cast<int64_t>(w.x) * q.out + oy) * q.out * 3);
+      hits[2 * h] = make_int4(off(Ra), off(R), static_cast<int>(fs.wpk[oy]),
+                              3 * (w.y - cam * p.W) - cb0);
+      hits[2 * h + 1] = make_int4(static_cast<int>(trow & 0xFFFFFFFFu), static_cast<int>(trow >> 32),
+                                  w.w, 0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWsThreads, 3)
+    apply_tile_ws_kernel(const ApplyParams p, const TileFuse q) {
+  extern __shared__ __align__(128) uint4 ring[];  // [kWsStages][kTmaRows][kApplyThreads]
+  __shared__ __align__(8) uint64_t full[kWsStages];
+  __shared__ __align__(8) uint64_t corr[kWsStages];
+  int64_t item = blockIdx.x;
+  const int cg = static_cast<int>(item % p.col_groups);
+  item /= p.col_groups;
+  const int rs = static_cast<int>(item % p.row_splits);
+  item /= p.row_splits;
+  const int k = static_cast<int>(item % p.K);
+  const int64_t img = item / p.K;
+
+  const int blk_r0 = k * p.bh;
+  const int blk_r1 = (k == p.K - 1) ? p.H : blk_r0 + p.bh;
+  const int r0 = blk_r0 + rs * p.rows_per_split;
+  const int r1 = min(blk_r1, r0 + p.rows_per_split);
+  if (r0 >= r1) return;  // CTA-uniform
+  const int chunks = min(kApplyThreads, p.chunks_per_row - cg * kApplyThreads);
+  const uint32_t seg = static_cast<uint32_t>(chunks) * 16u;
+  const int64_t rb = p.row_bytes;
+  const uint8_t *src0 = p.src + img * p.img_bytes + static_cast<int64_t>(r0) * rb +
+                        static_cast<int64_t>(cg) * kApplyThreads * 16;
+  const int nrows = r1 - r0;
+  const int nst = (nrows + kTmaRows - 1) / kTmaRows;
+  const bool corrector = threadIdx.x < kApplyThreads;
+
+  auto issue = [&](int st) {
+    const int slot = st % kWsStages;
+    const int rr = min(kTmaRows, nrows - st * kTmaRows);
+    mbar_expect_tx(&full[slot], seg * rr);
+    for (int i = 0; i < rr; ++i)
+      bulk_g2s(ring + (slot * kTmaRows + i) * kApplyThreads,
+               src0 + static_cast<int64_t>(st * kTmaRows + i) * rb, seg, &full[slot]);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kWsStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&corr[i], kApplyThreads / 32);  // one arrival per corrector warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int st = 0; st < min(kWsStages, nst); ++st) issue(st);
+  }
+
+  // tables and the intersecting-window list (geometry only)
+  FuseSmem fs{};
+  uint8_t *base = reinterpret_cast<uint8_t *>(ring + kWsStages * kTmaRows * kApplyThreads);
+  fs.i0 = reinterpret_cast<int16_t *>(base);
+  fs.i1 = fs.i0 + q.out;
+  fs.wpk = reinterpret_cast<uint32_t *>(base + ((4 * q.out + 15) & ~15));
+  fs.rstart = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(fs.wpk) + ((4 * q.out + 15) & ~15));
+  fs.rlen = fs.rstart + q.size;
+  fs.win = reinterpret_cast<int4 *>(reinterpret_cast<uint8_t *>(fs.rlen) + ((4 * q.size + 15) & ~15));
+  fs.hit = fs.win + kFuseMaxWin;
+  fs.counts = reinterpret_cast<int32_t *>(fs.hit + 2 * kFuseMaxHits * 2);
+  const int64_t bfr = img / p.cam_count;
+  const int cam = p.cam_begin + static_cast<int>(img % p.cam_count);
+  const int cb0 = cg * kApplyThreads * 16;
+  const int px_lo = (cb0 + 2) / 3;
+  const int px_hi = (cb0 + static_cast<int>(seg)) / 3;
+  for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
+    int a, b, w1;
+    src_coord_w(i, q.scale, q.size, a, b, w1);
+    fs.i0[i] = static_cast<int16_t>(a);
+    fs.i1[i] = static_cast<int16_t>(b);
+    fs.wpk[i] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
+  }
+  for (int r = threadIdx.x; r < q.size; r += blockDim.x) {
+    fs.rstart[r] = 0x7FFFFFFF;
+    fs.rlen[r] = 0;
+  }
+  if (threadIdx.x == 0) fs.counts[0] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
+    const int r = fs.i1[i];
+    atomicMin(&fs.rstart[r], i);
+    atomicAdd(&fs.rlen[r], 1);
+  }
+  {
+    const int w_lo = q.frame_off[bfr], w_hi = q.frame_off[bfr + 1];
+    const int mx0 = cam * p.W + px_lo, mx1 = cam * p.W + px_hi;
+    for (int t = w_lo + threadIdx.x; t < w_hi; t += blockDim.x) {
+      const int x0 = q.wins[3 * t + 1], y0 = q.wins[3 * t + 2];
+      if (x0 < mx1 && x0 + q.size > mx0 && y0 < r1 && y0 + q.size > r0) {
+        const int xc = x0 - cam * p.W;
+        int lo = 0, hi = q.out;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (xc + fs.i0[mid] >= px_lo) hi = mid; else lo = mid + 1;
+        }
+        int lo2 = lo, hi2 = q.out;
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          if (xc + fs.i1[mid] >= px_hi) hi2 = mid; else lo2 = mid + 1;
+        }
+        if (lo2 > lo) {
+          const int slot = atomicAdd(&fs.counts[0], 1);
+          fs.win[slot] = make_int4(t, x0, y0, lo | (lo2 << 16));
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  if (corrector) {
+    // ---------------------------------------------------------- correctors
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int j = cg * kApplyThreads + threadIdx.x;
+    const bool active = threadIdx.x < chunks;
+    const double *gl, *bl, *gr, *br;
+    map_ptrs(p, img, gl, bl, gr, br);
+    Coef16 cf;
+    if (active) {
+      float m[16], a[16];
+      const int q0 = j * 16;
+      int col = q0 / 3;
+      int ch = q0 - col * 3;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        coef_f32(col, ch, k, p.W, gl, bl, gr, br, m[i], a[i]);
+        if (++ch == 3) {
+          ch = 0;
+          ++col;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        cf.m[i >> 1] = pack2(m[i] * 0.00390625f, m[i + 1] * 0.00390625f);
+        cf.c[i >> 1] = pack2(m[i] * -32768.0f, m[i + 1] * -32768.0f);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        cf.a[i] = fabsf(a[i]) < 7.7037197787136e-34f ? 0.0f : a[i] * 0.00390625f;
+    }
+    uint8_t *dst = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
+    for (int st = 0; st < nst; ++st) {
+      const int slot = st % kWsStages;
+      mbar_wait(&full[slot], (st / kWsStages) & 1);
+      const int rr = min(kTmaRows, nrows - st * kTmaRows);
+      if (active) {
+        uint4 v[kTmaRows];
+#pragma unroll
+        for (int i = 0; i < kTmaRows; ++i)
+          if (i < rr) v[i] = ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x];
+#pragma unroll
+        for (int i = 0; i < kTmaRows; ++i)
+          if (i < rr) {
+            const uint4 o = correct16(v[i], cf);
+            st_stream_v4(dst + static_cast<int64_t>(st * kTmaRows + i) * rb, o);
+            ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x] = o;
+          }
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&corr[slot]);
+    }
+  } else {
+    // ---------------------------------------------------------- resamplers
+    const int rt = threadIdx.x - kApplyThreads;  // 0..kWsResamplers-1
+    const uint8_t *ringb = reinterpret_cast<const uint8_t *>(ring);
+    for (int st = 0; st < nst; ++st) {
+      const int slot = st % kWsStages;
+      mbar_wait(&corr[slot], (st / kWsStages) & 1);
+      if (rt < 32) build_hits_ws(fs, q, p, st, r0, nrows, cam, cb0);
+      named_bar(1, kWsResamplers);
+      const int nhit = fs.counts[1];
+      for (int hh = 0; hh < nhit; ++hh) {
+        const int4 h0 = fs.hit[2 * hh], h1 = fs.hit[2 * hh + 1];
+        resample_hit<4>(ringb + h0.x, ringb + h0.y, static_cast<uint32_t>(h0.z), h0.w,
+                        reinterpret_cast<uint8_t *>(
+                            (static_cast<uint64_t>(static_cast<uint32_t>(h1.y)) << 32) |
+                            static_cast<uint32_t>(h1.x)),
+                        h1.z & 0xFFFF, h1.z >> 16, rt, kWsResamplers, fs);
+      }
+      named_bar(1, kWsResamplers);  // stage st resampled: hits reusable, slot st-1 free
+      if (rt == 0 && st >= 1 && st - 1 + kWsStages < nst) issue(st - 1 + kWsStages);
+    }
+  }
+}
+
+// Tile outputs the fused kernel could not produce (taps straddling CTA rows
+// or column groups), resampled from the corrected frame.  One CTA per tile.
+__device__ __forceinline__ int row_cta(const ApplyParams &p, int r) {
+  const int k = min(r / p.bh, p.K - 1);
+  return k * p.row_splits + (r - k * p.bh) / p.rows_per_split;
+}
+__device__ __forceinline__ int col_cta(const ApplyParams &p, int mx) {
+  // whole-pixel column group of mosaic column mx, or -1 if the pixel's bytes
+  // straddle two groups
+  const int camc = mx / p.W, px = mx - camc * p.W;
+  const int g0 = (3 * px) / (kApplyThreads * 16), g1 = (3 * px + 2) / (kApplyThreads * 16);
+  return g0 == g1 ? camc * p.col_groups + g0 : -1 - camc;
+}
+
+__global__ void __launch_bounds__(256) tile_fixup_kernel(const ApplyParams p, const TileFuse q) {
+  extern __shared__ int32_t fx_smem[];
+  int32_t *colbad = fx_smem;          // [out] ox whose column taps are not one CTA's
+  int32_t *rowbad = fx_smem + q.out;  // [out] oy whose row taps are not one CTA's
+  __shared__ int ncol, nrow;
+  const int t = blockIdx.x;
+  const int64_t b = q.wins[3 * t];
+  const int x0 = q.wins[3 * t + 1], y0 = q.wins[3 * t + 2];
+  if (threadIdx.x == 0) ncol = nrow = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
+    int a, c;
+    float f;
+    src_coord(i, q.scale, q.size, a, c, f);
+    const int ga = col_cta(p, x0 + a), gb = col_cta(p, x0 + c);
+    if (ga < 0 || ga != gb) colbad[atomicAdd(&ncol, 1)] = i;
+    if (row_cta(p, y0 + a) != row_cta(p, y0 + c)) rowbad[atomicAdd(&nrow, 1)] = i;
+  }
+  __syncthreads();
+  const int nc = ncol, nr = nrow;
+  // work items: every ox of a bad row, then the bad columns of every row
+  // (bad rows included twice would only rewrite identical bytes; skip them)
+  const int64_t n_items = static_cast<int64_t>(nr) * q.out + static_cast<int64_t>(q.out) * nc;
+  const uint8_t *frame = p.dst + b * p.cam_count * p.img_bytes;
+  auto px = [&](int row, int mx) -> const uint8_t * {
+    const int camc = mx / p.W;
+    return frame + camc * p.img_bytes + static_cast<int64_t>(row) * p.row_bytes +
+           (mx - camc * p.W) * 3;
+  };
+  for (int64_t it = threadIdx.x; it < n_items; it += blockDim.x) {
+    int oy, ox;
+    if (it < static_cast<int64_t>(nr) * q.out) {
+      oy = rowbad[it / q.out];
+      ox = static_cast<int>(it % q.out);
+    } else {
+      const int64_t u = it - static_cast<int64_t>(nr) * q.out;
+      oy = static_cast<int>(u / nc);
+      ox = colbad[u % nc];
+    }
+    int ya, yb, xa, xb, wy, wx;
+    src_coord_w(oy, q.scale, q.size, ya, yb, wy);
+    src_coord_w(ox, q.scale, q.size, xa, xb, wx);
+    const uint8_t *A = px(y0 + ya, x0 + xa), *Bp = px(y0 + ya, x0 + xb);
+    const uint8_t *C = px(y0 + yb, x0 + xa), *D = px(y0 + yb, x0 + xb);
+    uint8_t *o = q.tiles + ((static_cast<int64_t>(t) * q.out + oy) * q.out + ox) * 3;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) o[ch] = static_cast<uint8_t>(bilerp_fx(A[ch], Bp[ch], C[ch], D[ch], wx, wy));
   }
 }
 
@@ -377,60 +900,122 @@ __global__ void apply_generic_kernel(const ApplyParams p) {
   }
 }
 
-static int launch_apply(ApplyParams &p, cudaStream_t stream) {
-  if (p.n_img <= 0 || p.H <= 0 || p.W <= 0) return CAMX_OK;
+static size_t fuse_smem_bytes(const TileFuse &q) {
+  size_t b = 2 * ((4 * static_cast<size_t>(q.out) + 15) & ~static_cast<size_t>(15));
+  b += (4 * static_cast<size_t>(q.size) + 15) & ~static_cast<size_t>(15);
+  b += 4 * static_cast<size_t>(q.size);
+  b = (b + 15) & ~static_cast<size_t>(15);
+  b += sizeof(int4) * (kFuseMaxWin + 2 * kFuseMaxHits * 2) + 32;
+  return b;
+}
+
+// Decomposition of the fast path (shared by K3 and the tile fix-up).
+static bool plan_fast(ApplyParams &p) {
   const bool aligned = (p.row_bytes % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(p.src) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(p.dst) % 16 == 0);
-  if (aligned) {
-    p.chunks_per_row = p.row_bytes / 16;
-    p.col_groups = (p.chunks_per_row + kApplyThreads - 1) / kApplyThreads;
-    // Whole block rows per CTA unless the grid would under-fill the GPU.
-    const int max_rows = p.H - (p.K - 1) * p.bh;  // last block is the tallest
-    int64_t base = static_cast<int64_t>(p.n_img) * p.K * p.col_groups;
-    int splits = 1;
-    const int64_t target = static_cast<int64_t>(sm_count()) * 8;
-    while (base * splits < target && (max_rows + splits) / (splits + 1) >= 16) ++splits;
-    p.row_splits = splits;
-    p.rows_per_split = (max_rows + splits - 1) / splits;
-    const int64_t grid = base * splits;
+  if (!aligned) return false;
+  p.chunks_per_row = p.row_bytes / 16;
+  p.col_groups = (p.chunks_per_row + kApplyThreads - 1) / kApplyThreads;
+  // Whole block rows per CTA unless the grid would under-fill the GPU.
+  const int max_rows = p.H - (p.K - 1) * p.bh;  // last block is the tallest
+  const int64_t base = static_cast<int64_t>(p.n_img) * p.K * p.col_groups;
+  int splits = 1;
+  const int64_t target = static_cast<int64_t>(sm_count()) * 8;
+  while (base * splits < target && (max_rows + splits) / (splits + 1) >= 16) ++splits;
+  p.row_splits = splits;
+  p.rows_per_split = (max_rows + splits - 1) / splits;
+  return true;
+}
+
+template <bool TILES>
+static int launch_tma(const ApplyParams &p, const TileFuse &q, cudaStream_t stream) {
+  const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
+  const size_t smem = kTmaStages * kTmaRows * kApplyThreads * 16 + (TILES ? fuse_smem_bytes(q) : 0);
+  cudaError_t e = cudaFuncSetAttribute(apply_tma_kernel<TILES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return static_cast<int>(e);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(static_cast<unsigned>(grid));
+  lc.blockDim = dim3(kApplyThreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = p.pdl ? 1 : 0;
+  e = cudaLaunchKernelEx(&lc, apply_tma_kernel<TILES>, p, q);
+  return e == cudaSuccess ? launch_status() : static_cast<int>(e);
+}
+
+static int launch_apply(ApplyParams &p, cudaStream_t stream) {
+  if (p.n_img <= 0 || p.H <= 0 || p.W <= 0) return CAMX_OK;
+  if (plan_fast(p)) {
     static const int use_ldg = [] {
       const char *e = getenv("CAMX_APPLY_KERNEL");
       return (e != nullptr && e[0] == 'l') ? 1 : 0;
     }();
     if (use_ldg) {
+      const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
       apply_fast_kernel<<<static_cast<unsigned>(grid), kApplyThreads, 0, stream>>>(p);
-    } else {
-      const int smem = kTmaStages * kTmaRows * kApplyThreads * 16;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-      }
-      if (p.pdl) {
-        cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3(static_cast<unsigned>(grid));
-        lc.blockDim = dim3(kApplyThreads);
-        lc.dynamicSmemBytes = smem;
-        lc.stream = stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        lc.attrs = at;
-        lc.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&lc, apply_tma_kernel, p);
-        if (e != cudaSuccess) return static_cast<int>(e);
-      } else {
-        apply_tma_kernel<<<static_cast<unsigned>(grid), kApplyThreads, smem, stream>>>(p);
-      }
+      return launch_status();
     }
-  } else {
-    const int64_t npx = static_cast<int64_t>(p.n_img) * p.H * p.W;
-    int64_t blocks = (npx + 255) / 256;
-    const int64_t cap = static_cast<int64_t>(sm_count()) * 16;
-    if (blocks > cap) blocks = cap;
-    apply_generic_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(p);
+    return launch_tma<false>(p, TileFuse{}, stream);
   }
+  const int64_t npx = static_cast<int64_t>(p.n_img) * p.H * p.W;
+  int64_t blocks = (npx + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 16;
+  if (blocks > cap) blocks = cap;
+  apply_generic_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(p);
+  return launch_status();
+}
+
+// Fused K3 + K5 (+ fix-up).  Returns CAMX_EINVAL if the geometry is not
+// fusable (caller falls back to apply + tiles).
+static int launch_apply_tiles(ApplyParams &p, TileFuse &q, int32_t n_tiles,
+                              int32_t max_tiles_per_frame, cudaStream_t stream) {
+  if (!plan_fast(p)) return CAMX_EINVAL;
+  // strict downscale: no clamped taps, each source row is the second tap of <= 1 output row
+  if (max_tiles_per_frame > kFuseMaxWin || q.out >= q.size || q.size > 4096) return CAMX_EINVAL;
+  if (fuse_smem_bytes(q) + kWsStages * kTmaRows * kApplyThreads * 16 > 110 * 1024) return CAMX_EINVAL;
+  static const bool use_ws = [] {
+    const char *e = getenv("CAMX_TILE_WS");
+    return e != nullptr && e[0] == '1';
+  }();
+  int st;
+  if (!use_ws) {
+    st = launch_tma<true>(p, q, stream);
+  } else {
+    const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
+    const size_t smem = kWsStages * kTmaRows * kApplyThreads * 16 + fuse_smem_bytes(q);
+    cudaError_t e = cudaFuncSetAttribute(apply_tile_ws_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(static_cast<unsigned>(grid));
+    lc.blockDim = dim3(kWsThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = p.pdl ? 1 : 0;
+    e = cudaLaunchKernelEx(&lc, apply_tile_ws_kernel, p, q);
+    st = e == cudaSuccess ? launch_status() : static_cast<int>(e);
+  }
+  if (st != CAMX_OK || n_tiles == 0) return st;
+  const size_t smem = 2 * sizeof(int32_t) * q.out;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(tile_fixup_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  tile_fixup_kernel<<<n_tiles, 256, smem, stream>>>(p, q);
   return launch_status();
 }
 
@@ -503,26 +1088,25 @@ extern "C" int camx_apply_map(const uint8_t *images, uint8_t *out, int64_t n_ima
   return launch_apply(p, as_stream(stream));
 }
 
-extern "C" int camx_correct_batch(const uint8_t *images, uint8_t *out, const uint8_t *prev_frame,
-                                  int32_t n_batch, int32_t n_cams, int32_t wrap, int32_t height,
-                                  int32_t width, int32_t band_width, int32_t t_diff,
-                                  const camx_solve_config *cfg, const double *prev_gain,
-                                  const double *prev_offset, camx_band_stat *stats,
-                                  uint32_t *hist, double *gain_out, double *offset_out,
-                                  uint8_t *fit_ok_out, int32_t *counters, void *stream) {
-  if (cfg == nullptr || images == nullptr || out == nullptr || stats == nullptr) return CAMX_EINVAL;
+namespace camx {
+
+// K1 (+ K2 as a programmatic dependent) for a whole batch.
+static int stats_and_solve(const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch,
+                           int32_t n_cams, int32_t wrap, int32_t height, int32_t width,
+                           int32_t band_width, int32_t t_diff, const camx_solve_config *cfg,
+                           const double *prev_gain, const double *prev_offset,
+                           camx_band_stat *stats, uint32_t *hist, double *gain_out,
+                           double *offset_out, uint8_t *fit_ok_out, void *stream) {
+  if (cfg == nullptr || images == nullptr || stats == nullptr) return CAMX_EINVAL;
   if (gain_out == nullptr || offset_out == nullptr) return CAMX_EINVAL;
   if (n_batch < 1 || n_cams < 2 || cfg->blocks < 1 || cfg->blocks > height) return CAMX_EINVAL;
   if (cfg->mode < CAMX_MODE_STANDARD || cfg->mode > CAMX_MODE_SMOOTHING) return CAMX_EINVAL;
   if (cfg->have_prev_maps && (prev_gain == nullptr || prev_offset == nullptr)) return CAMX_EINVAL;
-  (void)counters;  // used by the fused variant (camx_band_stats_solve)
-  const int64_t img_bytes = static_cast<int64_t>(height) * width * 3;
-  const int64_t frame_bytes = img_bytes * n_cams;
+  const int64_t frame_bytes = static_cast<int64_t>(height) * width * 3 * n_cams;
   const int64_t rec_frame = static_cast<int64_t>(n_cams) * 2 * cfg->blocks;
   const bool removal = cfg->mode == CAMX_MODE_OBJECT_REMOVAL;
   int st;
-  // K1: band statistics (frames 1.. against their predecessors, frame 0
-  // against prev_frame, for OBJECT_REMOVAL)
+  // frames 1.. against their predecessors, frame 0 against prev_frame (OBJECT_REMOVAL)
   if (removal && n_batch > 1) {
     st = camx_band_stats(images + frame_bytes, images, nullptr, (n_batch - 1) * int64_t(n_cams),
                          height, width, band_width, cfg->blocks, t_diff, stats + rec_frame,
@@ -536,27 +1120,124 @@ extern "C" int camx_correct_batch(const uint8_t *images, uint8_t *out, const uin
                          t_diff, stats, hist, stream);
   }
   if (st != CAMX_OK) return st;
-  // K2 as a programmatic dependent of K1, K3 as one of K2
-  st = launch_seam_solve(stats, n_batch, n_cams, wrap, cfg, prev_gain, prev_offset, gain_out,
-                         offset_out, fit_ok_out, as_stream(stream), true);
-  if (st != CAMX_OK) return st;
+  return launch_seam_solve(stats, n_batch, n_cams, wrap, cfg, prev_gain, prev_offset, gain_out,
+                           offset_out, fit_ok_out, as_stream(stream), true);
+}
+
+static ApplyParams array_params(const uint8_t *images, uint8_t *out, int32_t n_batch,
+                                int32_t n_cams, int32_t wrap, int32_t height, int32_t width,
+                                int32_t blocks, const double *gain, const double *offset) {
   ApplyParams p{};
   p.src = images;
   p.dst = out;
   p.H = height;
   p.W = width;
-  p.K = cfg->blocks;
-  p.bh = height / cfg->blocks;
+  p.K = blocks;
+  p.bh = height / blocks;
   p.row_bytes = width * 3;
-  p.img_bytes = img_bytes;
+  p.img_bytes = static_cast<int64_t>(height) * width * 3;
   p.n_img = n_batch * n_cams;
   p.cam_begin = 0;
   p.cam_count = n_cams;
   p.n_cams = n_cams;
   p.wrap = wrap;
   p.S = wrap ? n_cams : n_cams - 1;
-  p.gain = gain_out;
-  p.offset = offset_out;
-  p.pdl = 1;
+  p.gain = gain;
+  p.offset = offset;
+  return p;
+}
+
+extern "C" int camx_tiles(const uint8_t *images, int32_t n_cams, int32_t height, int32_t width,
+                          const int32_t *windows, int32_t n_tiles, int32_t size, int32_t out_size,
+                          uint8_t *tiles_out, void *stream);
+
+// K3 + K5: fused when the geometry allows (one pass over the raw frames),
+// else apply followed by the row-staged tile kernel on the corrected frames.
+static int apply_and_tile(ApplyParams &p, const int32_t *windows, const int32_t *frame_off,
+                          int32_t n_tiles, int32_t max_tiles_per_frame, int32_t size,
+                          int32_t out_size, uint8_t *tiles_out, void *stream) {
+  if (n_tiles < 0 || size < 1 || out_size < 1 || size > p.H || size > p.n_cams * p.W)
+    return CAMX_EINVAL;
+  if (n_tiles > 0 && (windows == nullptr || tiles_out == nullptr)) return CAMX_EINVAL;
+  static const bool fuse_enabled = [] {
+    const char *e = getenv("CAMX_TILE_FUSE");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  if (fuse_enabled && n_tiles > 0 && frame_off != nullptr && max_tiles_per_frame > 0 &&
+      p.cam_count == p.n_cams) {
+    TileFuse q{};
+    q.wins = windows;
+    q.frame_off = frame_off;
+    q.tiles = tiles_out;
+    q.size = size;
+    q.out = out_size;
+    q.scale = static_cast<float>(size) / static_cast<float>(out_size);
+    ApplyParams pf = p;
+    const int st = launch_apply_tiles(pf, q, n_tiles, max_tiles_per_frame, as_stream(stream));
+    if (st != CAMX_EINVAL) return st;
+  }
+  int st = launch_apply(p, as_stream(stream));
+  if (st != CAMX_OK || n_tiles == 0) return st;
+  return camx_tiles(p.dst, p.n_cams, p.H, p.W, windows, n_tiles, size, out_size, tiles_out,
+                    stream);
+}
+
+}  // namespace camx
+using namespace camx;
+
+extern "C" int camx_correct_batch(const uint8_t *images, uint8_t *out, const uint8_t *prev_frame,
+                                  int32_t n_batch, int32_t n_cams, int32_t wrap, int32_t height,
+                                  int32_t width, int32_t band_width, int32_t t_diff,
+                                  const camx_solve_config *cfg, const double *prev_gain,
+                                  const double *prev_offset, camx_band_stat *stats,
+                                  uint32_t *hist, double *gain_out, double *offset_out,
+                                  uint8_t *fit_ok_out, int32_t *counters, void *stream) {
+  (void)counters;  // reserved for the fused camx_band_stats_solve variant
+  if (out == nullptr) return CAMX_EINVAL;
+  int st = stats_and_solve(images, prev_frame, n_batch, n_cams, wrap, height, width, band_width,
+                           t_diff, cfg, prev_gain, prev_offset, stats, hist, gain_out, offset_out,
+                           fit_ok_out, stream);
+  if (st != CAMX_OK) return st;
+  ApplyParams p = array_params(images, out, n_batch, n_cams, wrap, height, width, cfg->blocks,
+                               gain_out, offset_out);
+  p.pdl = 1;  // K3 is a programmatic dependent of K2
   return launch_apply(p, as_stream(stream));
+}
+
+extern "C" int camx_correct_batch_tiles(
+    const uint8_t *images, uint8_t *out, const uint8_t *prev_frame, int32_t n_batch,
+    int32_t n_cams, int32_t wrap, int32_t height, int32_t width, int32_t band_width,
+    int32_t t_diff, const camx_solve_config *cfg, const double *prev_gain,
+    const double *prev_offset, camx_band_stat *stats, uint32_t *hist, double *gain_out,
+    double *offset_out, uint8_t *fit_ok_out, const int32_t *windows, const int32_t *frame_off,
+    int32_t n_tiles, int32_t max_tiles_per_frame, int32_t size, int32_t out_size,
+    uint8_t *tiles_out, void *stream) {
+  if (out == nullptr) return CAMX_EINVAL;
+  int st = stats_and_solve(images, prev_frame, n_batch, n_cams, wrap, height, width, band_width,
+                           t_diff, cfg, prev_gain, prev_offset, stats, hist, gain_out, offset_out,
+                           fit_ok_out, stream);
+  if (st != CAMX_OK) return st;
+  ApplyParams p = array_params(images, out, n_batch, n_cams, wrap, height, width, cfg->blocks,
+                               gain_out, offset_out);
+  p.pdl = 1;
+  return apply_and_tile(p, windows, frame_off, n_tiles, max_tiles_per_frame, size, out_size,
+                        tiles_out, stream);
+}
+
+extern "C" int camx_correct_and_tile(const uint8_t *images, uint8_t *out, int32_t n_batch,
+                                     int32_t n_cams, int32_t wrap, int32_t height, int32_t width,
+                                     int32_t blocks, const double *gain, const double *offset,
+                                     const int32_t *windows, const int32_t *frame_off,
+                                     int32_t n_tiles, int32_t max_tiles_per_frame, int32_t size,
+                                     int32_t out_size, uint8_t *tiles_out, void *stream) {
+  if (images == nullptr || out == nullptr || n_batch < 0 || n_cams < 1) return CAMX_EINVAL;
+  if (height < 1 || width < 1 || blocks < 1 || blocks > height) return CAMX_EINVAL;
+  if (wrap && n_cams < 2) return CAMX_EINVAL;
+  const int S = wrap ? n_cams : n_cams - 1;
+  if (S > 0 && (gain == nullptr || offset == nullptr)) return CAMX_EINVAL;
+  if (n_batch == 0) return CAMX_OK;
+  ApplyParams p = array_params(images, out, n_batch, n_cams, wrap, height, width, blocks, gain,
+                               offset);
+  return apply_and_tile(p, windows, frame_off, n_tiles, max_tiles_per_frame, size, out_size,
+                        tiles_out, stream);
 }

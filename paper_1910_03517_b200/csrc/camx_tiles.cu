@@ -8,7 +8,7 @@
 // order, round-half-even (oracle/camarray_oracle.py: resize_bilinear).
 //
 // seam_cost: exposure.py:417-445 (box downsample, Eq. 1 of the paper).
-#include "camx_common.cuh"
+#include "camx_resize.cuh"
 
 namespace camx {
 
@@ -19,14 +19,6 @@ struct TileParams {
   uint8_t *tiles;
   float scale;
 };
-
-__device__ __forceinline__ void src_coord(int i, float scale, int S, int &i0, int &i1, float &f) {
-  float s = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(i), 0.5f), scale), 0.5f);
-  s = fminf(fmaxf(s, 0.0f), static_cast<float>(S - 1));
-  i0 = static_cast<int>(floorf(s));
-  i1 = min(i0 + 1, S - 1);
-  f = __fsub_rn(s, static_cast<float>(i0));
-}
 
 __device__ __forceinline__ const uint8_t *mosaic_px(const TileParams &p, int64_t b, int row,
                                                      int mx) {
@@ -52,25 +44,94 @@ __global__ void tiles_kernel(const TileParams p) {
       dst[3 * q + 2] = s[2];
       continue;
     }
-    int y_0, y_1, x_0, x_1;
-    float fy, fx;
-    src_coord(oy, p.scale, p.size, y_0, y_1, fy);
-    src_coord(ox, p.scale, p.size, x_0, x_1, fx);
+    int y_0, y_1, x_0, x_1, wy, wx;
+    src_coord_w(oy, p.scale, p.size, y_0, y_1, wy);
+    src_coord_w(ox, p.scale, p.size, x_0, x_1, wx);
     const uint8_t *a = mosaic_px(p, b, y0 + y_0, x0 + x_0);
     const uint8_t *bb = mosaic_px(p, b, y0 + y_0, x0 + x_1);
     const uint8_t *c = mosaic_px(p, b, y0 + y_1, x0 + x_0);
     const uint8_t *d = mosaic_px(p, b, y0 + y_1, x0 + x_1);
-    const float gx = __fsub_rn(1.0f, fx), gy = __fsub_rn(1.0f, fy);
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      const float top = __fadd_rn(__fmul_rn(static_cast<float>(a[ch]), gx),
-                                  __fmul_rn(static_cast<float>(bb[ch]), fx));
-      const float bot = __fadd_rn(__fmul_rn(static_cast<float>(c[ch]), gx),
-                                  __fmul_rn(static_cast<float>(d[ch]), fx));
-      float v = __fadd_rn(__fmul_rn(top, gy), __fmul_rn(bot, fy));
-      v = fminf(fmaxf(rintf(v), 0.0f), 255.0f);
-      dst[3 * q + ch] = static_cast<uint8_t>(v);
+    for (int ch = 0; ch < 3; ++ch)
+      dst[3 * q + ch] = static_cast<uint8_t>(bilerp_fx(a[ch], bb[ch], c[ch], d[ch], wx, wy));
+  }
+}
+
+// Row-staged version: CTA = (tile, band of kTileRowsPerCta output rows).  For
+// each output row the two source rows' window segments (S*3 bytes, split
+// at camera boundaries) are staged in shared memory with 16-byte loads of
+// the aligned superset, the row is resampled from shared memory into a
+// shared output row, then stored with 16-byte stores.  Same arithmetic as
+// tiles_kernel (camx_resize.cuh).
+constexpr int kTileThreads = 256;
+constexpr int kTileRowsPerCta = 4;
+
+__device__ __forceinline__ void stage_row(const TileParams &p, int64_t b, int row, int x0,
+                                          uint8_t *dst) {
+  // dst[j] = byte j of the window row (j < S*3); copies per camera segment
+  int x = x0;
+  const int xe = x0 + p.size;
+  int dofs = 0;
+  while (x < xe) {  // CTA-uniform loop over camera segments
+    const int cam = x / p.W;
+    const int seg_end = min(xe, (cam + 1) * p.W);
+    const int nbytes = (seg_end - x) * 3;
+    const uint8_t *src = p.img + (((b * p.n_cams + cam) * p.H + row) * static_cast<int64_t>(p.W) +
+                                  (x - cam * p.W)) * 3;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t base = a0 & ~static_cast<uintptr_t>(15);
+    const int head = static_cast<int>(a0 - base);
+    const int nvec = (head + nbytes + 15) >> 4;
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4 *>(base) + v);
+      const uint8_t *qb = reinterpret_cast<const uint8_t *>(&q);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int j = v * 16 + e - head;
+        if (j >= 0 && j < nbytes) dst[dofs + j] = qb[e];
+      }
     }
+    dofs += nbytes;
+    x = seg_end;
+  }
+}
+
+__global__ void __launch_bounds__(kTileThreads) tiles_rows_kernel(const TileParams p) {
+  extern __shared__ __align__(16) uint8_t tsm[];
+  const int S3 = p.size * 3;
+  uint8_t *rowA = tsm;
+  uint8_t *rowB = tsm + ((S3 + 15) & ~15);
+  uint8_t *orow = rowB + ((S3 + 15) & ~15);
+  const int t = blockIdx.y;
+  const int64_t b = p.wins[3 * t];
+  const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
+  const int O3 = p.out * 3;
+  uint8_t *tile = p.tiles + static_cast<int64_t>(t) * p.out * O3;
+  const int oy_end = min(p.out, (blockIdx.x + 1) * kTileRowsPerCta);
+  for (int oy = blockIdx.x * kTileRowsPerCta; oy < oy_end; ++oy) {
+    int y_0, y_1, wy;
+    src_coord_w(oy, p.scale, p.size, y_0, y_1, wy);
+    stage_row(p, b, y0 + y_0, x0, rowA);
+    stage_row(p, b, y0 + y_1, x0, rowB);
+    __syncthreads();
+    for (int ox = threadIdx.x; ox < p.out; ox += blockDim.x) {
+      int x_0, x_1, wx;
+      src_coord_w(ox, p.scale, p.size, x_0, x_1, wx);
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch)
+        orow[3 * ox + ch] = static_cast<uint8_t>(bilerp_fx(rowA[3 * x_0 + ch], rowA[3 * x_1 + ch],
+                                                           rowB[3 * x_0 + ch], rowB[3 * x_1 + ch],
+                                                           wx, wy));
+    }
+    __syncthreads();
+    uint8_t *dst = tile + static_cast<int64_t>(oy) * O3;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (O3 & 15) == 0) {
+      for (int v = threadIdx.x; v < O3 / 16; v += blockDim.x)
+        reinterpret_cast<uint4 *>(dst)[v] = reinterpret_cast<const uint4 *>(orow)[v];
+    } else {
+      for (int j = threadIdx.x; j < O3; j += blockDim.x) dst[j] = orow[j];
+    }
+    __syncthreads();
   }
 }
 
@@ -136,11 +197,22 @@ static int launch_tiles(const uint8_t *images, int32_t n_cams, int32_t height, i
   p.tiles = tiles_out;
   // host SSE float division is IEEE round-to-nearest, = np.float32(S) / np.float32(out)
   p.scale = static_cast<float>(size) / static_cast<float>(out_size);
-  const int64_t npx = static_cast<int64_t>(out_size) * out_size;
-  int64_t bx = (npx + 255) / 256;
-  if (bx > 64) bx = 64;
-  dim3 grid(static_cast<unsigned>(bx), n_tiles);
-  tiles_kernel<<<grid, 256, 0, s>>>(p);
+  if (out_size == size) {  // exact crop: plain copy kernel
+    const int64_t npx = static_cast<int64_t>(out_size) * out_size;
+    int64_t bx = (npx + 255) / 256;
+    if (bx > 64) bx = 64;
+    tiles_kernel<<<dim3(static_cast<unsigned>(bx), n_tiles), 256, 0, s>>>(p);
+    return launch_status();
+  }
+  const int S3p = ((size * 3 + 15) & ~15);
+  const int smem = 2 * S3p + ((out_size * 3 + 15) & ~15);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(tiles_rows_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  dim3 grid((out_size + kTileRowsPerCta - 1) / kTileRowsPerCta, n_tiles);
+  tiles_rows_kernel<<<grid, kTileThreads, smem, s>>>(p);
   return launch_status();
 }
 
@@ -164,21 +236,6 @@ extern "C" int camx_tiles(const uint8_t *images, int32_t n_cams, int32_t height,
     return CAMX_EINVAL;
   if (n_tiles == 0) return CAMX_OK;
   return launch_tiles(images, n_cams, height, width, windows, n_tiles, size, out_size, tiles_out,
-                      as_stream(stream));
-}
-
-extern "C" int camx_correct_and_tile(const uint8_t *images, uint8_t *out, int32_t n_batch,
-                                     int32_t n_cams, int32_t wrap, int32_t height, int32_t width,
-                                     int32_t blocks, const double *gain, const double *offset,
-                                     const int32_t *windows, int32_t n_tiles, int32_t size,
-                                     int32_t out_size, uint8_t *tiles_out, void *stream) {
-  if (!images || !out || !tiles_args_ok(n_cams, height, width, windows, n_tiles, size, out_size,
-                                        tiles_out))
-    return CAMX_EINVAL;
-  int st = camx_apply_array(images, out, n_batch, 0, n_cams, n_cams, wrap, height, width, blocks,
-                            gain, offset, stream);
-  if (st != CAMX_OK || n_tiles == 0) return st;
-  return launch_tiles(out, n_cams, height, width, windows, n_tiles, size, out_size, tiles_out,
                       as_stream(stream));
 }
 

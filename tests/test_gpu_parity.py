@@ -436,3 +436,62 @@ def test_window_counts_vs_oracle():
     np.testing.assert_array_equal(got, want)
     got2 = at.window_counts(wins, 128, mask=np.stack(np.split(mosaic_mask, N, axis=1)), n_cams=N)
     np.testing.assert_array_equal(got2, want)
+
+
+def test_correct_and_tile_vs_oracle():
+    """Config-5 path: corrected mosaic -> sliding-plan tiles -> resize, against
+    the oracle's correction + crop + resize."""
+    N, H, W, B = 3, 150, 200, 2
+    frames = np.stack([O.synthetic_array(N, H, W, seed=21, objects=3, frame_index=t)
+                       for t in range(B)])
+    cfg = xp.ExposureConfig(band_width=16, blocks=5)
+    ac = ArrayCorrector(N, H, W, cfg)
+    res, tiles = ac.correct_and_tile(torch.from_numpy(frames).cuda(), size=128, out_size=52)
+    want_out, _, _, _ = O.correct_sequence(frames, None, O.STANDARD,
+                                           O.Cfg(band_width=16, blocks=5))
+    got_out = res.out.cpu().numpy()
+    np.testing.assert_array_equal(got_out, want_out)
+    wins = O.sliding_window_plan(N * W, H, 128)
+    tiles = tiles.cpu().numpy()
+    assert tiles.shape == (B * len(wins), 52, 52, 3)
+    i = 0
+    for b in range(B):
+        mosaic = np.concatenate(list(want_out[b]), axis=1)
+        for (x, y) in wins:
+            np.testing.assert_array_equal(tiles[i], O.resize_bilinear(O.crop(mosaic, x, y, 128), 52))
+            i += 1
+
+
+@pytest.mark.parametrize("out_size", [52, 128, 300])
+@pytest.mark.parametrize("blocks", [5, 1])
+def test_fused_correct_and_tile_vs_oracle(out_size, blocks):
+    """Aligned geometry (3W % 16 == 0, two column groups per row) so the
+    one-pass fused apply+tile kernel and its straddle fix-up run; results
+    must equal the oracle's correction + crop + resize exactly."""
+    N, H, W, B = 3, 200, 1024, 2
+    frames = np.stack([O.synthetic_array(N, H, W, seed=31, objects=4, frame_index=t)
+                       for t in range(B)])
+    cfg = xp.ExposureConfig(band_width=16, blocks=blocks)
+    ac = ArrayCorrector(N, H, W, cfg)
+    res, tiles = ac.correct_and_tile(torch.from_numpy(frames).cuda(), size=128,
+                                     out_size=out_size)
+    want_out, _, _, _ = O.correct_sequence(frames, None, O.STANDARD,
+                                           O.Cfg(band_width=16, blocks=blocks))
+    np.testing.assert_array_equal(res.out.cpu().numpy(), want_out)
+    wins = O.sliding_window_plan(N * W, H, 128)
+    tiles = tiles.cpu().numpy()
+    i = 0
+    for b in range(B):
+        mosaic = np.concatenate(list(want_out[b]), axis=1)
+        for (x, y) in wins:
+            want = O.resize_bilinear(O.crop(mosaic, x, y, 128), out_size)
+            np.testing.assert_array_equal(tiles[i], want, err_msg=f"tile {b} ({x},{y})")
+            i += 1
+    # explicit, unsorted (b, x, y) windows including camera-straddling ones
+    wins2 = [(1, 1000, 10), (0, 2000, 60), (1, 5, 0), (0, 1020, 71)]
+    res2, t2 = ArrayCorrector(N, H, W, cfg).correct_and_tile(
+        torch.from_numpy(frames).cuda(), wins2, size=128, out_size=out_size)
+    t2 = t2.cpu().numpy()
+    for j, (b, x, y) in enumerate(sorted(wins2, key=lambda w: w[0])):
+        mosaic = np.concatenate(list(want_out[b]), axis=1)
+        np.testing.assert_array_equal(t2[j], O.resize_bilinear(O.crop(mosaic, x, y, 128), out_size))
