@@ -495,3 +495,39 @@ def test_fused_correct_and_tile_vs_oracle(out_size, blocks):
     for j, (b, x, y) in enumerate(sorted(wins2, key=lambda w: w[0])):
         mosaic = np.concatenate(list(want_out[b]), axis=1)
         np.testing.assert_array_equal(t2[j], O.resize_bilinear(O.crop(mosaic, x, y, 128), out_size))
+
+
+@pytest.mark.parametrize("mode", [xp.ExposureMode.STANDARD, xp.ExposureMode.OBJECT_REMOVAL,
+                                  xp.ExposureMode.SMOOTHING])
+def test_camera_shards_match_single_gpu(mode):
+    """The sharded path (dist.py) on one device: each shard runs K1 on its
+    cameras, gets the whole array's records from `exchange` (what the NCCL
+    all-gather assembles), solves every seam and applies K3 to its cameras
+    only.  The concatenated shard outputs must equal the 1-GPU result."""
+    from paper_1910_03517_b200.dist import camera_partition
+    N, H, W, B = 5, 96, 128, 3
+    frames = np.stack([O.synthetic_array(N, H, W, seed=41, objects=3, frame_index=t)
+                       for t in range(B)])
+    cfg = xp.ExposureConfig(band_width=16, blocks=4)
+    d = torch.from_numpy(frames).cuda()
+    full = ArrayCorrector(N, H, W, cfg, mode)
+    want = [full.correct(d[:2]), full.correct(d[2:])]
+    parts = camera_partition(N, 2)
+    current = {}  # records of the whole array for the call in flight
+
+    def make_exchange(b0, c):
+        def exchange(local):
+            r = current["recs"]
+            # the shard's own K1 records equal the whole-array records of its cameras
+            assert torch.equal(local, r[:, b0:b0 + c])
+            return r
+        return exchange
+
+    shards = [ArrayCorrector(N, H, W, cfg, mode, cam_begin=b0, cam_count=c,
+                             exchange=make_exchange(b0, c)) for (b0, c) in parts]
+    outs = []
+    for call, sl in enumerate([slice(0, 2), slice(2, 3)]):
+        current["recs"] = want[call].stats.clone()
+        got = [sh.correct(d[sl, b0:b0 + c].contiguous()).out for sh, (b0, c) in zip(shards, parts)]
+        outs.append(torch.cat(got, dim=1).cpu().numpy())
+    np.testing.assert_array_equal(np.concatenate(outs), torch.cat([w.out for w in want]).cpu().numpy())
