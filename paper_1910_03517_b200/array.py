@@ -365,13 +365,16 @@ class ArrayCorrector:
         return maps
 
     # ------------------------------------------------------------ host path
-    def correct_host(self, frames_host, out_host=None, *, chunk: int = 1):
+    def correct_host(self, frames_host, out_host=None, *, chunk: int = 1, wait: bool = True):
         """End-to-end correction of host frames (B, N, H, W, 3) uint8.
 
         frames_host/out_host: pinned torch CPU tensors for full-speed async
         copies (numpy arrays are accepted and wrapped, at pageable-copy
-        speed).  Returns out_host.  H2D, kernels and D2H of consecutive
-        chunks overlap on three streams."""
+        speed).  H2D, kernels and D2H of consecutive chunks overlap on three
+        streams.  wait=True returns out_host once it is filled; wait=False
+        returns (out_host, event) right away so consecutive calls pipeline
+        (the next batch's H2D overlaps this batch's D2H) - synchronize the
+        event before reading out_host or reusing frames_host."""
         t = _dev.require_cuda()
         src = frames_host if isinstance(frames_host, t.Tensor) else t.from_numpy(
             np.ascontiguousarray(frames_host))
@@ -384,8 +387,7 @@ class ArrayCorrector:
         ring = self._host_ring(chunk)
         n_chunks = (B + chunk - 1) // chunk
         cur = t.cuda.current_stream()
-        for s in (ring["h2d"], ring["comp"], ring["d2h"]):
-            s.wait_stream(cur)
+        ring["h2d"].wait_stream(cur)  # inputs produced on the caller's stream
         for i in range(n_chunks):
             lo, hi = i * chunk, min(B, (i + 1) * chunk)
             slot = i % ring["slots"]
@@ -404,8 +406,12 @@ class ArrayCorrector:
                 ring["d2h"].wait_event(ring["comp_done"][slot])
                 dst[lo:hi].copy_(dev_out, non_blocking=True)
                 ring["out_free"][slot].record(ring["d2h"])
-        cur.wait_stream(ring["d2h"])
-        return out_host
+        done = t.cuda.Event()
+        done.record(ring["d2h"])
+        if wait:
+            done.synchronize()
+            return out_host
+        return out_host, done
 
     def _host_ring(self, chunk: int):
         ring = self._ring
