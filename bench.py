@@ -198,9 +198,16 @@ def run_camx(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink/NVSwitch; CAMX_DIST_BACKEND=gloo exercises the same
+        # code path with several ranks on one GPU (tests only)
+        backend = os.environ.get("CAMX_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     name = args.workload or ("config3" if world > 1 else "config2")
     n_cams, H, W, B0, desc = WORKLOADS[name]
     B = args.batch or B0
@@ -342,8 +349,11 @@ def run_camx(args):
             e_ms = float(tt[0])
         wall = time.perf_counter() - t0
         e_ms_step = e_ms / e_steps
+        # every rank copies its camera shard: whole-job bytes = world x this rank's
+        # (shards are equal for the benchmark configs)
         e2e = {"value": round(Be * px_per_frame / 1e6 / (e_ms_step / 1e3), 2), "unit": "MP/s",
-               "h2d_bytes_per_step": int(host_in.numel()), "d2h_bytes_per_step": int(host_out.numel()),
+               "h2d_bytes_per_step": int(host_in.numel()) * world,
+               "d2h_bytes_per_step": int(host_out.numel()) * world,
                "array_frames_per_sec": round(Be / (e_ms_step / 1e3), 2),
                "batch": Be, "steps": e_steps, "wall_s": round(wall, 3),
                "path": "ArrayCorrector.correct_host (pinned ring, 3 streams, batches pipelined)",
