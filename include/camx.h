@@ -223,8 +223,10 @@ int camx_window_counts(const uint8_t *mask, const uint8_t *cur,
 /* ---- stage 4b: attention tile crop / resize (K5) ------------------------
  * Crop of ExternalDetector.detect (detect.py:297-300) of window (x, y, S)
  * from the (virtual) mosaic of n_cams images, then bilinear resize to
- * out_size x out_size (half-pixel centres, float32, round-half-even; the
- * resize is builder-defined - the reference only crops).  out_size == S is
+ * out_size x out_size (half-pixel centres; source coordinate in float32,
+ * 8-bit fixed-point weights round(256 f), exact integer blend
+ * (h0*(256-wy) + h1*wy + 2^15) >> 16; the resize is builder-defined - the
+ * reference only crops).  out_size == S is
  * the exact crop.  images: [n_batch][n_cams][H][W][3]; windows: device
  * int32 [n_tiles][3] = (batch index, x, y); tiles_out: uint8
  * [n_tiles][out_size][out_size][3]. */
