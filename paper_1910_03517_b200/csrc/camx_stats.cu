@@ -22,6 +22,8 @@
 // word; word (channel, bin/4, lane) sits in bank `lane`, so increments
 // never conflict and need no atomics), flushed every <= 255 pixels per lane
 // into per-lane registers by a SWAR (2 x 16-bit) column sum.
+#include <algorithm>
+
 #include "camx_solve.cuh"
 
 namespace camx {
@@ -75,7 +77,7 @@ __device__ __noinline__ void fused_solve_tail(const StatsParams &p, int64_t unit
 
 constexpr int kStatsWarps = 4;  // warps per (image, side, block) unit = per CTA
 constexpr int kCounterWords = 3 * 64 * 32;  // per warp: 3 ch x 64 bin-quads x 32 lanes
-constexpr int kQuadBatch = 4;
+constexpr int kQuadBatch = 8;  // a standard 32-px x 96-row band unit: one batch
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
@@ -166,16 +168,11 @@ __device__ __forceinline__ uint32_t quad_exclusion(const StatsParams &p, const u
 }
 
 template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
-__global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const StatsParams p) {
-  extern __shared__ uint32_t smem[];
-  __shared__ uint64_t part[kStatsWarps][13];
+__device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t unit,
+                                           uint32_t *smem, uint64_t (*part)[13]) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t unit = blockIdx.x;
   constexpr int kStride = 32 * kStatsWarps;  // quads (pixels) per CTA-wide step
-  // let a programmatically dependent K3 launch early: it only prefetches
-  // raw pixels (which this kernel does not write) before griddepcontrol.wait
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int k = static_cast<int>(unit % p.K);
   const int side = static_cast<int>((unit / p.K) % 2);
   const int64_t img = unit / (2 * p.K);
@@ -355,6 +352,22 @@ __global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const Stat
   if (FUSE) fused_solve_tail(p, p.img_begin * 2 * p.K + unit);
 }
 
+// Persistent: a grid of a few CTAs per SM loops over the (image, side,
+// block) units, so the short per-unit load -> reduce phases of resident
+// CTAs overlap instead of running as many launch waves.
+template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
+__global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const StatsParams p) {
+  extern __shared__ uint32_t smem[];
+  __shared__ uint64_t part[kStatsWarps][13];
+  // let a programmatically dependent kernel launch early (K2 waits on
+  // griddepcontrol.wait; K3 only prefetches raw pixels before it)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int64_t unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
+    stats_unit<HIST, MASKMODE, QUAD, FUSE>(p, unit, smem, part);
+    __syncthreads();  // `part` / counters reused by the next unit
+  }
+}
+
 template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
 static void launch_stats(const StatsParams &p, cudaStream_t s) {
   const int warps = kStatsWarps;
@@ -363,8 +376,10 @@ static void launch_stats(const StatsParams &p, cudaStream_t s) {
     cudaFuncSetAttribute(band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   }
+  const int per_sm = HIST ? 2 : 8;
+  const int64_t grid = std::min<int64_t>(p.n_units, static_cast<int64_t>(sm_count()) * per_sm);
   band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>
-      <<<static_cast<unsigned>(p.n_units), warps * 32, smem, s>>>(p);
+      <<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(p);
 }
 
 template <bool HIST, int MASKMODE, bool FUSE = false>
