@@ -16,7 +16,8 @@ import numpy as np
 from . import _dev, _lib
 from .core import BBox, Mosaic
 
-__all__ = ["DetectorWindow", "crop_window", "tiles"]
+__all__ = ["DetectorWindow", "crop_window", "tiles", "encode_ppm", "encode_ppm_tiles",
+           "detect_requests"]
 
 
 @dataclass(frozen=True)
@@ -88,3 +89,46 @@ def crop_window(mosaic: Mosaic, window: DetectorWindow, out_size: int | None = N
     res = tiles(img, [(0, window.x, window.y)], window.size,
                 window.size if out_size is None else out_size)
     return _dev.to_host(res[0])
+
+
+# ------------------------------------------------ tile wire format
+# The detector consumes tiles as netpbm P6 payloads (imgio.encode_ppm,
+# imgio.py:14-18) framed by ExternalDetector's request line (detect.py:252-301):
+#   "DETECT v1 <x> <y> <size> <w> <h>\n" + PPM bytes of the crop.
+
+def encode_ppm(pixels) -> bytes:
+    """P6 payload of one (H, W, 3) uint8 image (header + raw RGB rows)."""
+    px = np.asarray(pixels)
+    if px.ndim != 3 or px.shape[2] != 3 or px.dtype != np.uint8:
+        raise ValueError("PPM payload must be (H, W, 3) uint8")
+    return b"P6\n%d %d\n255\n" % (px.shape[1], px.shape[0]) + np.ascontiguousarray(px).tobytes()
+
+
+def encode_ppm_tiles(tile_batch) -> list[bytes]:
+    """P6 payloads of a (T, S, S, 3) tile batch.  A CUDA batch is brought to
+    the host in ONE copy (the tiles are already the payload bytes: a P6 body
+    is raw row-major RGB), then each payload is header + a slice."""
+    t = _dev.torch()
+    if isinstance(tile_batch, t.Tensor):
+        host = tile_batch.detach().to("cpu", non_blocking=False).numpy()
+    else:
+        host = np.asarray(tile_batch)
+    if host.ndim != 4 or host.shape[-1] != 3 or host.dtype != np.uint8:
+        raise ValueError("tile batch must be (T, H, W, 3) uint8")
+    head = b"P6\n%d %d\n255\n" % (host.shape[2], host.shape[1])
+    return [head + host[i].tobytes() for i in range(host.shape[0])]
+
+
+def detect_requests(windows, tile_batch) -> list[bytes]:
+    """Full wire requests (header line + PPM) for windows and their tiles, as
+    ExternalDetector.detect would send them (detect.py:297-301); the tile's
+    own dimensions (resized or not) are the reported crop size."""
+    payloads = encode_ppm_tiles(tile_batch)
+    if len(payloads) != len(windows):
+        raise ValueError("one tile per window")
+    out = []
+    for w, ppm in zip(windows, payloads):
+        x, y, size = (w.x, w.y, w.size) if isinstance(w, DetectorWindow) else w
+        dims = ppm.split(b"\n", 2)[1].split()
+        out.append(b"DETECT v1 %d %d %d %s %s\n" % (x, y, size, dims[0], dims[1]) + ppm)
+    return out

@@ -213,3 +213,21 @@ class TestMapsTable:                  # test_exposure.py:382-399
             xp.block_bounds(4, 5)
         with pytest.raises(ValueError):
             xp.block_bounds(4, 0)
+
+
+class TestTileWire:                   # imgio.py:14-18, detect.py:297-301
+    def test_ppm_framing_matches_reference_format(self):
+        from paper_1910_03517_b200 import detect
+        rng = np.random.default_rng(3)
+        tiles = rng.integers(0, 256, (3, 4, 5, 3), dtype=np.uint8)
+        pp = detect.encode_ppm_tiles(tiles)
+        assert pp[1] == b"P6\n5 4\n255\n" + tiles[1].tobytes()
+        assert pp[2] == detect.encode_ppm(tiles[2])
+        req = detect.detect_requests([DetectorWindow(7, 8, 9), (1, 2, 3), DetectorWindow(0, 0, 4)],
+                                     tiles)
+        assert req[0].startswith(b"DETECT v1 7 8 9 5 4\nP6\n5 4\n255\n")
+        assert req[1][len(b"DETECT v1 1 2 3 5 4\n"):] == pp[1]
+        with pytest.raises(ValueError):
+            detect.encode_ppm(np.zeros((4, 4), np.uint8))
+        with pytest.raises(ValueError):
+            detect.detect_requests([DetectorWindow(0, 0, 1)], tiles)
