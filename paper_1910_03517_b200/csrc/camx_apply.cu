@@ -310,6 +310,36 @@ struct FuseSmem {  // carved from dynamic shared memory after the ring
 // + funnel shift, channel pairs by PRMT, horizontal blend by dp2a, vertical
 // by IMAD, round half up (camx_resize.cuh: bilerp_fx).  kWsUnroll > 1 is
 // for the warp-specialised kernel (latency-bound resampler warps).
+// Shared-memory carve of the fusion state after the ring; every region
+// starts 16-byte aligned (int4 records).  fuse_smem_bytes() == the total.
+__host__ __device__ __forceinline__ size_t r16(size_t v) { return (v + 15) & ~static_cast<size_t>(15); }
+__host__ __device__ __forceinline__ size_t fuse_layout(int out, int size, size_t *off) {
+  size_t o = 0;
+  off[0] = o; o += r16(2 * static_cast<size_t>(out));   // i0
+  off[1] = o; o += r16(2 * static_cast<size_t>(out));   // i1
+  off[2] = o; o += r16(4 * static_cast<size_t>(out));   // wpk
+  off[3] = o; o += r16(4 * static_cast<size_t>(size));  // rstart
+  off[4] = o; o += r16(4 * static_cast<size_t>(size));  // rlen
+  off[5] = o; o += sizeof(int4) * kFuseMaxWin;           // win
+  off[6] = o; o += sizeof(int4) * 2 * kFuseMaxHits * 2;  // hit (2 buffers)
+  off[7] = o; o += 32;                                   // counts
+  return o;
+}
+__device__ __forceinline__ FuseSmem carve_fuse(uint8_t *base, int out, int size) {
+  size_t off[8];
+  fuse_layout(out, size, off);
+  FuseSmem fs;
+  fs.i0 = reinterpret_cast<int16_t *>(base + off[0]);
+  fs.i1 = reinterpret_cast<int16_t *>(base + off[1]);
+  fs.wpk = reinterpret_cast<uint32_t *>(base + off[2]);
+  fs.rstart = reinterpret_cast<int32_t *>(base + off[3]);
+  fs.rlen = reinterpret_cast<int32_t *>(base + off[4]);
+  fs.win = reinterpret_cast<int4 *>(base + off[5]);
+  fs.hit = reinterpret_cast<int4 *>(base + off[6]);
+  fs.counts = reinterpret_cast<int32_t *>(base + off[7]);
+  return fs;
+}
+
 template <int kWsUnroll>
 __device__ __forceinline__ void resample_hit(const uint8_t *ra, const uint8_t *rb, uint32_t wyp,
                                              int xc3, uint8_t *trow, int lo, int hi, int t,
@@ -439,15 +469,8 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
   int cam = 0, cb0 = 0, px_lo = 0, px_hi = 0;
   int64_t bfr = 0;
   if (TILES) {
-    uint8_t *base = reinterpret_cast<uint8_t *>(ring + kTmaStages * kTmaRows * kApplyThreads);
-    fs.i0 = reinterpret_cast<int16_t *>(base);
-    fs.i1 = fs.i0 + q.out;
-    fs.wpk = reinterpret_cast<uint32_t *>(base + ((4 * q.out + 15) & ~15));
-    fs.rstart = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(fs.wpk) + ((4 * q.out + 15) & ~15));
-    fs.rlen = fs.rstart + q.size;
-    fs.win = reinterpret_cast<int4 *>(reinterpret_cast<uint8_t *>(fs.rlen) + ((4 * q.size + 15) & ~15));
-    fs.hit = fs.win + kFuseMaxWin;
-    fs.counts = reinterpret_cast<int32_t *>(fs.hit + 2 * kFuseMaxHits * 2);
+    fs = carve_fuse(reinterpret_cast<uint8_t *>(ring + kTmaStages * kTmaRows * kApplyThreads),
+                    q.out, q.size);
     bfr = img / p.cam_count;
     cam = p.cam_begin + static_cast<int>(img % p.cam_count);
     cb0 = cg * kApplyThreads * 16;
@@ -676,16 +699,9 @@ __global__ void __launch_bounds__(kWsThreads, 3)
   }
 
   // tables and the intersecting-window list (geometry only)
-  FuseSmem fs{};
-  uint8_t *base = reinterpret_cast<uint8_t *>(ring + kWsStages * kTmaRows * kApplyThreads);
-  fs.i0 = reinterpret_cast<int16_t *>(base);
-  fs.i1 = fs.i0 + q.out;
-  fs.wpk = reinterpret_cast<uint32_t *>(base + ((4 * q.out + 15) & ~15));
-  fs.rstart = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(fs.wpk) + ((4 * q.out + 15) & ~15));
-  fs.rlen = fs.rstart + q.size;
-  fs.win = reinterpret_cast<int4 *>(reinterpret_cast<uint8_t *>(fs.rlen) + ((4 * q.size + 15) & ~15));
-  fs.hit = fs.win + kFuseMaxWin;
-  fs.counts = reinterpret_cast<int32_t *>(fs.hit + 2 * kFuseMaxHits * 2);
+  const FuseSmem fs =
+      carve_fuse(reinterpret_cast<uint8_t *>(ring + kWsStages * kTmaRows * kApplyThreads), q.out,
+                 q.size);
   const int64_t bfr = img / p.cam_count;
   const int cam = p.cam_begin + static_cast<int>(img % p.cam_count);
   const int cb0 = cg * kApplyThreads * 16;
@@ -901,12 +917,8 @@ __global__ void apply_generic_kernel(const ApplyParams p) {
 }
 
 static size_t fuse_smem_bytes(const TileFuse &q) {
-  size_t b = 2 * ((4 * static_cast<size_t>(q.out) + 15) & ~static_cast<size_t>(15));
-  b += (4 * static_cast<size_t>(q.size) + 15) & ~static_cast<size_t>(15);
-  b += 4 * static_cast<size_t>(q.size);
-  b = (b + 15) & ~static_cast<size_t>(15);
-  b += sizeof(int4) * (kFuseMaxWin + 2 * kFuseMaxHits * 2) + 32;
-  return b;
+  size_t off[8];
+  return fuse_layout(q.out, q.size, off);
 }
 
 // Decomposition of the fast path (shared by K3 and the tile fix-up).

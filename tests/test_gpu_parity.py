@@ -531,3 +531,83 @@ def test_camera_shards_match_single_gpu(mode):
         got = [sh.correct(d[sl, b0:b0 + c].contiguous()).out for sh, (b0, c) in zip(shards, parts)]
         outs.append(torch.cat(got, dim=1).cpu().numpy())
     np.testing.assert_array_equal(np.concatenate(outs), torch.cat([w.out for w in want]).cpu().numpy())
+
+
+def _sweep_cases():
+    rng = np.random.default_rng(2024)
+    cases = []
+    for i in range(14):
+        N = int(rng.integers(2, 6))
+        H = int(rng.integers(12, 90))
+        W = int(rng.choice([9, 17, 33, 48, 64, 100, 128, 150, 256]))
+        bw = int(rng.integers(1, W // 2 + 1))
+        K = int(rng.integers(1, min(H, 9) + 1))
+        mode = [O.STANDARD, O.OBJECT_REMOVAL, O.SMOOTHING][i % 3]
+        wrap = bool(i % 4 == 1)
+        cases.append((i, N, H, W, bw, K, mode, wrap))
+    return cases
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"c{c[0]}")
+def test_random_geometry_sweep_vs_oracle(case):
+    """Random array geometries (odd widths -> generic apply path, unaligned
+    bands -> byte-load K1 path, wrap seams, all modes, histograms) against
+    the oracle's tick loop."""
+    i, N, H, W, bw, K, om, wrap = case
+    mode = {O.STANDARD: xp.ExposureMode.STANDARD, O.OBJECT_REMOVAL: xp.ExposureMode.OBJECT_REMOVAL,
+            O.SMOOTHING: xp.ExposureMode.SMOOTHING}[om]
+    rng = np.random.default_rng(100 + i)
+    B = 3
+    frames = np.stack([O.synthetic_array(N, H, W, seed=60 + i, objects=2, frame_index=t)
+                       for t in range(B)])
+    f1 = frames[1]
+    f1[rng.random((N, H, W)) < 0.05] = 255                   # noise + motion
+    mpx = int(rng.integers(1, 40))
+    cfg = xp.ExposureConfig(band_width=bw, blocks=K, min_band_pixels=mpx)
+    ac = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap, histograms=True)
+    res = ac.correct(torch.from_numpy(frames).cuda())
+    want, wg, wo, wok = O.correct_sequence(frames, None, om, O.Cfg(band_width=bw, blocks=K,
+                                                                    min_band_pixels=mpx),
+                                           None, wrap)
+    np.testing.assert_allclose(res.gain.cpu().numpy(), wg, rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    np.testing.assert_allclose(res.offset.cpu().numpy(), wo, rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    np.testing.assert_array_equal(res.fit_ok.cpu().numpy().astype(bool), wok)
+    d = np.abs(res.out.cpu().numpy().astype(int) - want.astype(int))
+    assert d.max() <= 1 and (d > 0).mean() < 1e-4
+    hist = res.hist.cpu().numpy().view(np.uint32)
+    for b in range(B):
+        mask = None
+        if om == O.OBJECT_REMOVAL and b > 0:
+            mask = [O.mask_diff(frames[b, c], frames[b - 1, c], 20) for c in range(N)]
+        for c in range(N):
+            for s, side in ((0, O.LEFT), (1, O.RIGHT)):
+                np.testing.assert_array_equal(
+                    hist[b, c, s], O.band_histograms(frames[b, c], side, bw, K,
+                                                     None if mask is None else mask[c]))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_windows_both_tile_paths(seed):
+    """Random (b, x, y) windows and output sizes through the fused
+    apply+tile path (aligned geometry) and the standalone tile kernel."""
+    rng = np.random.default_rng(seed)
+    N, H, W, B = 3, 180, 1024, 2
+    frames = np.stack([O.synthetic_array(N, H, W, seed=80 + seed, objects=3, frame_index=t)
+                       for t in range(B)])
+    S = int(rng.choice([64, 100, 150]))
+    out_size = int(rng.integers(8, S))
+    wins = [(int(rng.integers(0, B)), int(rng.integers(0, N * W - S + 1)),
+             int(rng.integers(0, H - S + 1))) for _ in range(int(rng.integers(5, 40)))]
+    cfg = xp.ExposureConfig(band_width=16, blocks=int(rng.integers(1, 7)))
+    ac = ArrayCorrector(N, H, W, cfg)
+    res, tiles = ac.correct_and_tile(torch.from_numpy(frames).cuda(), wins, size=S,
+                                     out_size=out_size)
+    out = res.out.cpu().numpy()
+    tiles = tiles.cpu().numpy()
+    order = sorted(wins, key=lambda w: w[0])
+    direct = detect.tiles(res.out, order, S, out_size).cpu().numpy()
+    for j, (b, x, y) in enumerate(order):
+        mosaic = np.concatenate(list(out[b]), axis=1)
+        want = O.resize_bilinear(O.crop(mosaic, x, y, S), out_size)
+        np.testing.assert_array_equal(tiles[j], want)
+        np.testing.assert_array_equal(direct[j], want)
