@@ -58,50 +58,57 @@ __global__ void tiles_kernel(const TileParams p) {
 }
 
 // Row-staged version: CTA = (tile, band of kTileRowsPerCta output rows).  For
-// each output row the two source rows' window segments (S*3 bytes, split
-// at camera boundaries) are staged in shared memory with 16-byte loads of
-// the aligned superset, the row is resampled from shared memory into a
-// shared output row, then stored with 16-byte stores.  Same arithmetic as
-// tiles_kernel (camx_resize.cuh).
+// each output row the two source rows' window segments (one per camera the
+// window covers) are staged in shared memory as their 16-byte-aligned
+// supersets (plain vector copies; `head` = offset of the first wanted byte),
+// then every output pixel is resampled from shared memory with the fixed-point
+// funnel/dp2a path (taps straddling two cameras: byte path), and the output
+// row is stored with 16-byte stores when aligned.  Arithmetic: camx_resize.cuh.
 constexpr int kTileThreads = 256;
-constexpr int kTileRowsPerCta = 4;
+constexpr int kTileRowsPerCta = 8;
 
-__device__ __forceinline__ void stage_row(const TileParams &p, int64_t b, int row, int x0,
-                                          uint8_t *dst) {
-  // dst[j] = byte j of the window row (j < S*3); copies per camera segment
-  int x = x0;
+struct RowSeg {   // one camera's part of a staged window row
+  int off;        // smem byte offset of the aligned superset
+  int head;       // first wanted byte within it
+  int x0;         // window-local pixel index where the segment starts
+};
+
+__device__ __forceinline__ int stage_row(const TileParams &p, int64_t b, int row, int x0,
+                                         uint8_t *buf, RowSeg &s0, RowSeg &s1) {
+  int x = x0, nseg = 0, off = 0;
   const int xe = x0 + p.size;
-  int dofs = 0;
-  while (x < xe) {  // CTA-uniform loop over camera segments
+  while (x < xe) {  // CTA-uniform: at most two camera segments when S <= W
     const int cam = x / p.W;
     const int seg_end = min(xe, (cam + 1) * p.W);
     const int nbytes = (seg_end - x) * 3;
     const uint8_t *src = p.img + (((b * p.n_cams + cam) * p.H + row) * static_cast<int64_t>(p.W) +
                                   (x - cam * p.W)) * 3;
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(src);
-    const uintptr_t base = a0 & ~static_cast<uintptr_t>(15);
-    const int head = static_cast<int>(a0 - base);
+    const uint4 *base = reinterpret_cast<const uint4 *>(a0 & ~static_cast<uintptr_t>(15));
+    const int head = static_cast<int>(a0 & 15);
     const int nvec = (head + nbytes + 15) >> 4;
-    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-      const uint4 q = __ldg(reinterpret_cast<const uint4 *>(base) + v);
-      const uint8_t *qb = reinterpret_cast<const uint8_t *>(&q);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int j = v * 16 + e - head;
-        if (j >= 0 && j < nbytes) dst[dofs + j] = qb[e];
-      }
-    }
-    dofs += nbytes;
+    uint4 *dst = reinterpret_cast<uint4 *>(buf + off);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = __ldg(base + v);
+    if (nseg == 0) s0 = RowSeg{off, head, x - x0};
+    else s1 = RowSeg{off, head, x - x0};
+    ++nseg;
+    off += nvec * 16 + 16;  // +16: slack for the 12-byte tap window reads
     x = seg_end;
   }
+  return nseg;
+}
+
+__device__ __forceinline__ int tap_addr(const RowSeg &s0, const RowSeg &s1, int nseg, int x) {
+  return (nseg > 1 && x >= s1.x0) ? s1.off + s1.head + 3 * (x - s1.x0)
+                                  : s0.off + s0.head + 3 * (x - s0.x0);
 }
 
 __global__ void __launch_bounds__(kTileThreads) tiles_rows_kernel(const TileParams p) {
   extern __shared__ __align__(16) uint8_t tsm[];
-  const int S3 = p.size * 3;
+  const int S3p = ((p.size * 3 + 15) & ~15) + 64;  // two segments + slack
   uint8_t *rowA = tsm;
-  uint8_t *rowB = tsm + ((S3 + 15) & ~15);
-  uint8_t *orow = rowB + ((S3 + 15) & ~15);
+  uint8_t *rowB = tsm + S3p;
+  uint8_t *orow = rowB + S3p;
   const int t = blockIdx.y;
   const int64_t b = p.wins[3 * t];
   const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
@@ -111,17 +118,40 @@ __global__ void __launch_bounds__(kTileThreads) tiles_rows_kernel(const TilePara
   for (int oy = blockIdx.x * kTileRowsPerCta; oy < oy_end; ++oy) {
     int y_0, y_1, wy;
     src_coord_w(oy, p.scale, p.size, y_0, y_1, wy);
-    stage_row(p, b, y0 + y_0, x0, rowA);
-    stage_row(p, b, y0 + y_1, x0, rowB);
+    RowSeg sa0{0, 0, 0}, sa1{0, 0, 0}, sb0{0, 0, 0}, sb1{0, 0, 0};
+    const int na = stage_row(p, b, y0 + y_0, x0, rowA, sa0, sa1);
+    stage_row(p, b, y0 + y_1, x0, rowB, sb0, sb1);
     __syncthreads();
+    const uint32_t wy1 = static_cast<uint32_t>(wy), wy0 = 256u - wy1;
     for (int ox = threadIdx.x; ox < p.out; ox += blockDim.x) {
       int x_0, x_1, wx;
       src_coord_w(ox, p.scale, p.size, x_0, x_1, wx);
+      const uint32_t wpk = static_cast<uint32_t>(256 - wx) | (static_cast<uint32_t>(wx) << 16);
+      uint8_t *o = orow + 3 * ox;
+      const bool same = (na == 1) || ((x_0 >= sa1.x0) == (x_1 >= sa1.x0));
+      if (same && x_1 == x_0 + 1) {  // two adjacent pixels of one segment: 6 contiguous bytes
+        const int la = tap_addr(sa0, sa1, na, x_0);
+        const int lb = tap_addr(sb0, sb1, na, x_0);
+        const uint32_t *pa = reinterpret_cast<const uint32_t *>(rowA + (la & ~3));
+        const uint32_t *pb = reinterpret_cast<const uint32_t *>(rowB + (lb & ~3));
+        const uint32_t sha = (la & 3) * 8, shb = (lb & 3) * 8;
+        const uint32_t alo = __funnelshift_r(pa[0], pa[1], sha), ahi = __funnelshift_r(pa[1], pa[2], sha);
+        const uint32_t blo = __funnelshift_r(pb[0], pb[1], shb), bhi = __funnelshift_r(pb[1], pb[2], shb);
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch)
-        orow[3 * ox + ch] = static_cast<uint8_t>(bilerp_fx(rowA[3 * x_0 + ch], rowA[3 * x_1 + ch],
-                                                           rowB[3 * x_0 + ch], rowB[3 * x_1 + ch],
-                                                           wx, wy));
+        for (int ch = 0; ch < 3; ++ch) {
+          const uint32_t sel = 0x0030u + 0x0011u * ch;
+          const uint32_t v0 = __dp2a_lo(wpk, __byte_perm(alo, ahi, sel), 0u);
+          const uint32_t v1 = __dp2a_lo(wpk, __byte_perm(blo, bhi, sel), 0u);
+          o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+        }
+      } else {  // clamped edge or taps in two cameras
+        const int a0 = tap_addr(sa0, sa1, na, x_0), a1 = tap_addr(sa0, sa1, na, x_1);
+        const int b0 = tap_addr(sb0, sb1, na, x_0), b1 = tap_addr(sb0, sb1, na, x_1);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch)
+          o[ch] = static_cast<uint8_t>(bilerp_fx(rowA[a0 + ch], rowA[a1 + ch], rowB[b0 + ch],
+                                                 rowB[b1 + ch], wx, wy));
+      }
     }
     __syncthreads();
     uint8_t *dst = tile + static_cast<int64_t>(oy) * O3;
@@ -204,7 +234,14 @@ static int launch_tiles(const uint8_t *images, int32_t n_cams, int32_t height, i
     tiles_kernel<<<dim3(static_cast<unsigned>(bx), n_tiles), 256, 0, s>>>(p);
     return launch_status();
   }
-  const int S3p = ((size * 3 + 15) & ~15);
+  if (size > width) {  // a window row spans > 2 cameras: per-pixel gather kernel
+    const int64_t npx = static_cast<int64_t>(out_size) * out_size;
+    int64_t bx = (npx + 255) / 256;
+    if (bx > 64) bx = 64;
+    tiles_kernel<<<dim3(static_cast<unsigned>(bx), n_tiles), 256, 0, s>>>(p);
+    return launch_status();
+  }
+  const int S3p = ((size * 3 + 15) & ~15) + 64;
   const int smem = 2 * S3p + ((out_size * 3 + 15) & ~15);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(tiles_rows_kernel,

@@ -611,3 +611,15 @@ def test_random_windows_both_tile_paths(seed):
         want = O.resize_bilinear(O.crop(mosaic, x, y, S), out_size)
         np.testing.assert_array_equal(tiles[j], want)
         np.testing.assert_array_equal(direct[j], want)
+
+
+def test_tiles_wider_than_a_camera():
+    """Config-1-like geometry: 960-pixel windows over 640-pixel cameras span
+    three cameras (per-pixel gather kernel)."""
+    rng = np.random.default_rng(5)
+    arr = rng.integers(0, 256, (1, 3, 480, 640, 3), dtype=np.uint8)
+    mosaic = np.concatenate(list(arr[0]), axis=1)
+    wins = [(0, 0, 0), (0, 960, 0), (0, 100, 0)]
+    got = detect.tiles(torch.from_numpy(arr).cuda(), wins, 480, 208).cpu().numpy()
+    for j, (_, x, y) in enumerate(wins):
+        np.testing.assert_array_equal(got[j], O.resize_bilinear(O.crop(mosaic, x, y, 480), 208))
