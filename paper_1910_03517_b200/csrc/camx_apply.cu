@@ -288,15 +288,20 @@ struct TileFuse {
   int32_t size, out;
   float scale;
 };
-constexpr int kFuseMaxWin = 64;  // windows per array-frame the fused path accepts
+constexpr int kFuseMaxWin = 48;  // windows per array-frame the fused path accepts
 // downscale/crop only (out <= size): a source row is the second tap of at
 // most one output row per window, so a 2-row stage has <= 2 hits per window
 constexpr int kFuseMaxHits = 2 * kFuseMaxWin;
+// ring of the fused (shared-barrier) kernel: 4-row stages halve the barriers
+// and hit builds per byte; refill lags two stages (previous row resident)
+constexpr int kFuseRows = 4;
+constexpr int kFuseStages = 4;
+static_assert(kFuseRows * kFuseMaxWin <= 2 * kFuseMaxHits, "hit buffer capacity");
 
 struct FuseSmem {  // carved from dynamic shared memory after the ring
   int16_t *i0, *i1;
   uint32_t *wpk;           // (256 - w1) | w1 << 16: dp2a operand
-  int32_t *rstart, *rlen;  // output rows whose second source row is r
+  float scale;             // S / out (candidate output row of a source row)
   int4 *win;               // intersecting windows: (tile, x0, y0, lo | hi << 16)
   int4 *hit;               // 2 buffers x kFuseMaxHits x 2 int4 (see build_hits)
   int32_t *counts;         // [0] n_win, [1]/[2] hits, [3]/[4] items of buffer 0 / 1
@@ -318,8 +323,8 @@ __host__ __device__ __forceinline__ size_t fuse_layout(int out, int size, size_t
   off[0] = o; o += r16(2 * static_cast<size_t>(out));   // i0
   off[1] = o; o += r16(2 * static_cast<size_t>(out));   // i1
   off[2] = o; o += r16(4 * static_cast<size_t>(out));   // wpk
-  off[3] = o; o += r16(4 * static_cast<size_t>(size));  // rstart
-  off[4] = o; o += r16(4 * static_cast<size_t>(size));  // rlen
+  off[3] = o;                                           // (unused)
+  off[4] = o;                                           // (unused)
   off[5] = o; o += sizeof(int4) * kFuseMaxWin;           // win
   off[6] = o; o += sizeof(int4) * 2 * kFuseMaxHits * 2;  // hit (2 buffers)
   off[7] = o; o += 32;                                   // counts
@@ -332,12 +337,24 @@ __device__ __forceinline__ FuseSmem carve_fuse(uint8_t *base, int out, int size)
   fs.i0 = reinterpret_cast<int16_t *>(base + off[0]);
   fs.i1 = reinterpret_cast<int16_t *>(base + off[1]);
   fs.wpk = reinterpret_cast<uint32_t *>(base + off[2]);
-  fs.rstart = reinterpret_cast<int32_t *>(base + off[3]);
-  fs.rlen = reinterpret_cast<int32_t *>(base + off[4]);
+  fs.scale = 0.0f;
   fs.win = reinterpret_cast<int4 *>(base + off[5]);
   fs.hit = reinterpret_cast<int4 *>(base + off[6]);
   fs.counts = reinterpret_cast<int32_t *>(base + off[7]);
   return fs;
+}
+
+// The output row whose second tap row is window-local source row lr, or -1
+// (strict downscale: at most one).  Candidate from the inverse map, verified
+// against the exact tap table.
+__device__ __forceinline__ int out_row_of(const FuseSmem &fs, int lr, int out) {
+  const int c = static_cast<int>(floorf((static_cast<float>(lr) - 0.5f) / fs.scale - 0.5f));
+#pragma unroll
+  for (int d = -1; d <= 2; ++d) {
+    const int oy = c + d;
+    if (oy >= 0 && oy < out && fs.i1[oy] == lr) return oy;
+  }
+  return -1;
 }
 
 template <int kWsUnroll>
@@ -386,14 +403,15 @@ __device__ __forceinline__ void resample_hit(const uint8_t *ra, const uint8_t *r
 // CTA: smem offsets of both (corrected) source rows, packed vertical
 // weights, window origin in segment bytes, the tile row pointer and the
 // output column range [lo, hi) whose taps are whole pixels of this CTA.
+template <int ROWS, int STAGES>
 __device__ __forceinline__ void build_hits(const FuseSmem &fs, const TileFuse &q,
                                            const ApplyParams &p, int st, int r0, int nrows,
                                            int cam, int cb0) {
   const int lane = threadIdx.x & 31;
-  const int rr = min(kTmaRows, nrows - st * kTmaRows);
-  const int rs0 = r0 + st * kTmaRows;
-  int4 *hits = fs.hit + (st & 1) * kFuseMaxHits * 2;
-  int *cnt = &fs.counts[1 + (st & 1)];
+  const int rr = min(ROWS, nrows - st * ROWS);
+  const int rs0 = r0 + st * ROWS;
+  int4 *hits = fs.hit;  // capacity ROWS * kFuseMaxWin hits (downscale: <= 1 per row per window)
+  int *cnt = &fs.counts[1];
   if (lane == 0) *cnt = 0;
   __syncwarp();
   const int nwin = fs.counts[0];
@@ -402,14 +420,15 @@ __device__ __forceinline__ void build_hits(const FuseSmem &fs, const TileFuse &q
     const int R = rs0 + e % rr;
     const int lr = R - w.z;
     if (lr < 0 || lr >= q.size) continue;
-    const int o0 = fs.rstart[lr], n = fs.rlen[lr];
-    for (int oy = o0; oy < o0 + n; ++oy) {
+    {
+      const int oy = out_row_of(fs, lr, q.out);
+      if (oy < 0) continue;
       const int Ra = w.z + fs.i0[oy];
       if (Ra < r0) continue;  // first tap row belongs to the previous CTA
       const int h = atomicAdd(cnt, 1);
       auto off = [&](int Rw) {
-        const int sidx = (Rw - r0) / kTmaRows, ri = (Rw - r0) % kTmaRows;
-        return ((sidx % kTmaStages) * kTmaRows + ri) * kApplyThreads * 16;
+        const int sidx = (Rw - r0) / ROWS, ri = (Rw - r0) % ROWS;
+        return ((sidx % STAGES) * ROWS + ri) * kApplyThreads * 16;
       };
       const uint64_t trow = reinterpret_cast<uint64_t>(
           q.tiles + (static_cast<int64_t>(w.x) * q.out + oy) * q.out * 3);
@@ -422,11 +441,11 @@ __device__ __forceinline__ void build_hits(const FuseSmem &fs, const TileFuse &q
   __syncwarp();
 }
 
-template <bool TILES>
+template <bool TILES, int ROWS, int STAGES>
 __global__ void __launch_bounds__(kApplyThreads, 4)
     apply_tma_kernel(const ApplyParams p, const TileFuse q) {
-  extern __shared__ __align__(128) uint4 ring[];  // [kTmaStages][kTmaRows][kApplyThreads]
-  __shared__ __align__(8) uint64_t full[kTmaStages];
+  extern __shared__ __align__(128) uint4 ring[];  // [STAGES][ROWS][kApplyThreads]
+  __shared__ __align__(8) uint64_t full[STAGES];
   int64_t item = blockIdx.x;
   const int cg = static_cast<int>(item % p.col_groups);
   item /= p.col_groups;
@@ -447,21 +466,21 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
   const uint8_t *src0 = p.src + img * p.img_bytes + static_cast<int64_t>(r0) * rb +
                         static_cast<int64_t>(cg) * kApplyThreads * 16;
   const int nrows = r1 - r0;
-  const int nst = (nrows + kTmaRows - 1) / kTmaRows;
+  const int nst = (nrows + ROWS - 1) / ROWS;
 
   auto issue = [&](int st) {
-    const int slot = st % kTmaStages;
-    const int rr = min(kTmaRows, nrows - st * kTmaRows);
+    const int slot = st % STAGES;
+    const int rr = min(ROWS, nrows - st * ROWS);
     mbar_expect_tx(&full[slot], seg * rr);
     for (int i = 0; i < rr; ++i)
-      bulk_g2s(ring + (slot * kTmaRows + i) * kApplyThreads,
-               src0 + static_cast<int64_t>(st * kTmaRows + i) * rb, seg, &full[slot]);
+      bulk_g2s(ring + (slot * ROWS + i) * kApplyThreads,
+               src0 + static_cast<int64_t>(st * ROWS + i) * rb, seg, &full[slot]);
   };
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kTmaStages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int st = 0; st < min(kTmaStages, nst); ++st) issue(st);
+    for (int st = 0; st < min(STAGES, nst); ++st) issue(st);
   }
 
   // ---- tile fusion prologue (independent of the maps: overlaps the PDL wait)
@@ -469,7 +488,7 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
   int cam = 0, cb0 = 0, px_lo = 0, px_hi = 0;
   int64_t bfr = 0;
   if (TILES) {
-    fs = carve_fuse(reinterpret_cast<uint8_t *>(ring + kTmaStages * kTmaRows * kApplyThreads),
+    fs = carve_fuse(reinterpret_cast<uint8_t *>(ring + STAGES * ROWS * kApplyThreads),
                     q.out, q.size);
     bfr = img / p.cam_count;
     cam = p.cam_begin + static_cast<int>(img % p.cam_count);
@@ -483,17 +502,9 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
       fs.i1[i] = static_cast<int16_t>(b);
       fs.wpk[i] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
     }
-    for (int r = threadIdx.x; r < q.size; r += blockDim.x) {
-      fs.rstart[r] = 0x7FFFFFFF;
-      fs.rlen[r] = 0;
-    }
     if (threadIdx.x == 0) fs.counts[0] = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
-      const int r = fs.i1[i];
-      atomicMin(&fs.rstart[r], i);
-      atomicAdd(&fs.rlen[r], 1);
-    }
+    fs.scale = q.scale;
+    __syncthreads();  // tap tables complete before the window scan reads them
     __syncthreads();
     // windows of this array-frame that overlap the CTA region (mosaic coords),
     // with the contiguous range [lo, hi) of output columns whose two column
@@ -557,32 +568,32 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
 
   uint8_t *dst = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
   for (int st = 0; st < nst; ++st) {
-    const int slot = st % kTmaStages;
-    mbar_wait(&full[slot], (st / kTmaStages) & 1);
-    const int rr = min(kTmaRows, nrows - st * kTmaRows);
+    const int slot = st % STAGES;
+    mbar_wait(&full[slot], (st / STAGES) & 1);
+    const int rr = min(ROWS, nrows - st * ROWS);
     if (active) {
-      uint4 v[kTmaRows];
+      uint4 v[ROWS];
 #pragma unroll
-      for (int i = 0; i < kTmaRows; ++i)
-        if (i < rr) v[i] = ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x];
+      for (int i = 0; i < ROWS; ++i)
+        if (i < rr) v[i] = ring[(slot * ROWS + i) * kApplyThreads + threadIdx.x];
 #pragma unroll
-      for (int i = 0; i < kTmaRows; ++i)
+      for (int i = 0; i < ROWS; ++i)
         if (i < rr) {
           const uint4 o = correct16(v[i], cf);
-          st_stream_v4(dst + static_cast<int64_t>(st * kTmaRows + i) * rb, o);
-          if (TILES) ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x] = o;
+          st_stream_v4(dst + static_cast<int64_t>(st * ROWS + i) * rb, o);
+          if (TILES) ring[(slot * ROWS + i) * kApplyThreads + threadIdx.x] = o;
         }
     }
     __syncthreads();  // slot consumed (and, with TILES, corrected rows visible)
     if (TILES) {
       // every thread has finished the previous stage's resample (it came
       // before this barrier): the slot of stage st-2 is free
-      if (threadIdx.x == 0 && st >= 2 && st - 2 + kTmaStages < nst) issue(st - 2 + kTmaStages);
+      if (threadIdx.x == 0 && st >= 2 && st - 2 + STAGES < nst) issue(st - 2 + STAGES);
       // warp 0 builds this stage's hit records, then everyone resamples
-      if (threadIdx.x < 32) build_hits(fs, q, p, st, r0, nrows, cam, cb0);
+      if (threadIdx.x < 32) build_hits<ROWS, STAGES>(fs, q, p, st, r0, nrows, cam, cb0);
       __syncthreads();
-      const int4 *hits = fs.hit + (st & 1) * kFuseMaxHits * 2;
-      const int nhit = fs.counts[1 + (st & 1)];
+      const int4 *hits = fs.hit;
+      const int nhit = fs.counts[1];
       const uint8_t *ringb = reinterpret_cast<const uint8_t *>(ring);
       for (int hh = 0; hh < nhit; ++hh) {
         const int4 h0 = hits[2 * hh], h1 = hits[2 * hh + 1];
@@ -593,7 +604,7 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
                         h1.z & 0xFFFF, h1.z >> 16, threadIdx.x, kApplyThreads, fs);
       }
     } else {
-      if (threadIdx.x == 0 && st + kTmaStages < nst) issue(st + kTmaStages);
+      if (threadIdx.x == 0 && st + STAGES < nst) issue(st + STAGES);
     }
   }
 }
@@ -634,8 +645,9 @@ __device__ __forceinline__ void build_hits_ws(const FuseSmem &fs, const TileFuse
     const int R = rs0 + e % rr;
     const int lr = R - w.z;
     if (lr < 0 || lr >= q.size) continue;
-    const int o0 = fs.rstart[lr], n = fs.rlen[lr];
-    for (int oy = o0; oy < o0 + n; ++oy) {
+    {
+      const int oy = out_row_of(fs, lr, q.out);
+      if (oy < 0) continue;
       const int Ra = w.z + fs.i0[oy];
       if (Ra < r0) continue;  // first tap row belongs to the previous CTA
       const int h = atomicAdd(cnt, 1);
@@ -699,7 +711,7 @@ __global__ void __launch_bounds__(kWsThreads, 3)
   }
 
   // tables and the intersecting-window list (geometry only)
-  const FuseSmem fs =
+  FuseSmem fs =
       carve_fuse(reinterpret_cast<uint8_t *>(ring + kWsStages * kTmaRows * kApplyThreads), q.out,
                  q.size);
   const int64_t bfr = img / p.cam_count;
@@ -714,17 +726,9 @@ __global__ void __launch_bounds__(kWsThreads, 3)
     fs.i1[i] = static_cast<int16_t>(b);
     fs.wpk[i] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
   }
-  for (int r = threadIdx.x; r < q.size; r += blockDim.x) {
-    fs.rstart[r] = 0x7FFFFFFF;
-    fs.rlen[r] = 0;
-  }
   if (threadIdx.x == 0) fs.counts[0] = 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
-    const int r = fs.i1[i];
-    atomicMin(&fs.rstart[r], i);
-    atomicAdd(&fs.rlen[r], 1);
-  }
+  fs.scale = q.scale;
+  __syncthreads();  // tap tables complete before the window scan reads them
   {
     const int w_lo = q.frame_off[bfr], w_hi = q.frame_off[bfr + 1];
     const int mx0 = cam * p.W + px_lo, mx1 = cam * p.W + px_hi;
@@ -940,11 +944,11 @@ static bool plan_fast(ApplyParams &p) {
   return true;
 }
 
-template <bool TILES>
+template <bool TILES, int ROWS = kTmaRows, int STAGES = kTmaStages>
 static int launch_tma(const ApplyParams &p, const TileFuse &q, cudaStream_t stream) {
   const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
-  const size_t smem = kTmaStages * kTmaRows * kApplyThreads * 16 + (TILES ? fuse_smem_bytes(q) : 0);
-  cudaError_t e = cudaFuncSetAttribute(apply_tma_kernel<TILES>,
+  const size_t smem = STAGES * ROWS * kApplyThreads * 16 + (TILES ? fuse_smem_bytes(q) : 0);
+  cudaError_t e = cudaFuncSetAttribute(apply_tma_kernel<TILES, ROWS, STAGES>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
@@ -958,7 +962,7 @@ static int launch_tma(const ApplyParams &p, const TileFuse &q, cudaStream_t stre
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = p.pdl ? 1 : 0;
-  e = cudaLaunchKernelEx(&lc, apply_tma_kernel<TILES>, p, q);
+  e = cudaLaunchKernelEx(&lc, apply_tma_kernel<TILES, ROWS, STAGES>, p, q);
   return e == cudaSuccess ? launch_status() : static_cast<int>(e);
 }
 
@@ -998,7 +1002,7 @@ static int launch_apply_tiles(ApplyParams &p, TileFuse &q, int32_t n_tiles,
   }();
   int st;
   if (!use_ws) {
-    st = launch_tma<true>(p, q, stream);
+    st = launch_tma<true, kFuseRows, kFuseStages>(p, q, stream);
   } else {
     const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
     const size_t smem = kWsStages * kTmaRows * kApplyThreads * 16 + fuse_smem_bytes(q);
