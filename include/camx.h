@@ -267,6 +267,21 @@ int camx_correct_batch_tiles(
     int32_t max_tiles_per_frame, int32_t size, int32_t out_size,
     uint8_t *tiles_out, void *stream);
 
+/* ---- next: motion-blob components -------------------------
+ * BlobDetector.detect (detect.py:192-249): 8-connected components of the
+ * motion mask inside the window (x0, y0, size) of the virtual mosaic of
+ * n_cams (H, W) masks (nonzero = on), as scipy.ndimage.label with a 3x3
+ * structure.  comp_out: int32 [max_comp][6] = (raster index of the
+ * component's first pixel, xmin, ymin, xmax, ymax (window coordinates,
+ * inclusive), on-pixels of ANY component inside that box (detect.py:241)),
+ * in scipy label order; *n_comp_out = number of components (may exceed
+ * max_comp).  scratch: 16-byte aligned int32 [6 * size * size + 2 * size + 1]
+ * device memory. */
+int camx_blob_components(const uint8_t *mask, int32_t n_cams, int32_t height,
+                         int32_t width, int32_t x0, int32_t y0, int32_t size,
+                         int32_t *scratch, int32_t *comp_out, int32_t max_comp,
+                         int32_t *n_comp_out, void *stream);
+
 /* ---- next: seam quality metric ------------------------------
  * seam_cost (exposure.py:417-445) of n_pairs (left, right) image pairs of
  * equal height: box-downsample by `factor`, per-row trend discrepancy,

@@ -77,6 +77,7 @@ SIGNATURES = {
     "camx_correct_batch_tiles": [P, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P, P,
                                  P, P, P, I32, I32, I32, I32, P, P],
     "camx_seam_cost": [P, P, I64, I32, I32, I32, I32, P, P],
+    "camx_blob_components": [P, I32, I32, I32, I32, I32, I32, P, P, I32, P, P],
 }
 
 _lib = None

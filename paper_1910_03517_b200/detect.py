@@ -9,15 +9,18 @@ tiles and are out of scope ("tile consumer").
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import enum
+import threading
+from dataclasses import dataclass, replace
 
 import numpy as np
 
 from . import _dev, _lib
-from .core import BBox, Mosaic
+from .core import BBox, Category, Mosaic, iou
 
 __all__ = ["DetectorWindow", "crop_window", "tiles", "encode_ppm", "encode_ppm_tiles",
-           "detect_requests"]
+           "detect_requests", "Detection", "DetectionSource", "BlobDetector", "nms",
+           "TOL_DETECT", "TOL_NMS"]
 
 
 @dataclass(frozen=True)
@@ -132,3 +135,149 @@ def detect_requests(windows, tile_batch) -> list[bytes]:
         dims = ppm.split(b"\n", 2)[1].split()
         out.append(b"DETECT v1 %d %d %d %s %s\n" % (x, y, size, dims[0], dims[1]) + ppm)
     return out
+
+
+# ------------------------------------------------ motion-blob detector
+
+TOL_DETECT = 0.65   # detect.py:35
+TOL_NMS = 0.45      # detect.py:36
+
+
+class DetectionSource(enum.Enum):
+    ORACLE = "oracle"
+    BLOB = "blob"
+    EXTERNAL = "external"
+
+
+@dataclass(frozen=True)
+class Detection:
+    """Classified box in mosaic coordinates with confidence (detect.py:45-57)."""
+
+    category: Category
+    bbox: BBox
+    probability: float
+    frame_index: int
+    source: DetectionSource
+
+    def __post_init__(self) -> None:
+        if not (0.0 <= self.probability <= 1.0):
+            raise ValueError(f"probability {self.probability} outside [0, 1]")
+
+
+def nms(dets: list[Detection], tol_nms: float = TOL_NMS) -> list[Detection]:
+    """Greedy per-category suppression, highest probability first, ties by
+    input order (detect.py:75-95).  Host logic on a handful of boxes."""
+    order = sorted(range(len(dets)), key=lambda i: (-dets[i].probability, i))
+    dead = set()
+    kept = []
+    for i in order:
+        if i in dead:
+            continue
+        kept.append(dets[i])
+        dead.update(j for j in order if j != i and j not in dead
+                    and dets[j].category is dets[i].category
+                    and iou(dets[j].bbox, dets[i].bbox) > tol_nms)
+    return kept
+
+
+def _finalize(dets, mosaic_w, mosaic_h, tol_detect, tol_nms):
+    """Clip to the mosaic, confidence gate, NMS (detect.py:104-114)."""
+    keep = []
+    for d in dets:
+        box = d.bbox.clipped(mosaic_w, mosaic_h)
+        if box.area > 0 and d.probability > tol_detect:
+            keep.append(replace(d, bbox=box))
+    return nms(keep, tol_nms)
+
+
+def blob_components(mask, window: DetectorWindow, n_cams: int = 1, max_comp: int = 4096,
+                    stream=None):
+    """8-connected components of the motion mask inside `window` (GPU,
+    camx_blob_components).  mask: (n_cams, H, W) (or (H, W)) bool/uint8,
+    numpy or CUDA; the mosaic of the n_cams masks is virtual.  Returns an
+    int array (n, 6): raster index of the first pixel, xmin, ymin, xmax,
+    ymax (window coordinates, inclusive), on-pixels inside the box - in
+    scipy.ndimage.label order."""
+    t = _dev.require_cuda()
+    m = mask if isinstance(mask, t.Tensor) else _dev.to_device(
+        np.asarray(mask, dtype=bool).view(np.uint8))
+    if m.dtype == t.bool:
+        m = m.view(t.uint8)
+    m = m.reshape(n_cams, *m.shape[-2:]).contiguous()
+    H, W = m.shape[-2:]
+    S = int(window.size)
+    scratch = t.empty((6 * S * S + 2 * S + 1 + 3,), dtype=t.int32, device="cuda")
+    comp = t.empty((max_comp, 6), dtype=t.int32, device="cuda")
+    n = t.zeros((1,), dtype=t.int32, device="cuda")
+    _lib.call("camx_blob_components", m.data_ptr(), int(n_cams), int(H), int(W), int(window.x),
+              int(window.y), S, scratch.data_ptr(), comp.data_ptr(), int(max_comp), n.data_ptr(),
+              _dev.stream_handle(stream))
+    count = int(n.item())
+    if count > max_comp:
+        return blob_components(mask, window, n_cams, count, stream)
+    return _dev.to_host(comp[:count])
+
+
+class BlobDetector:
+    """Motion-blob detector (detect.py:192-249): connected components of the
+    frame-difference mask of consecutive mosaics, one detection per
+    component of at least `min_area` on-pixels (counted over its box, as
+    the reference).  The mask and the components are computed on the GPU."""
+
+    def __init__(self, *, t_diff: int = 20, min_area: int = 4,
+                 category: Category = Category.VEHICLE, p_saturation_area: float = 400.0,
+                 tol_detect: float = TOL_DETECT, tol_nms: float = TOL_NMS):
+        self.t_diff = t_diff
+        self.min_area = min_area
+        self.category = category
+        self.p_saturation_area = p_saturation_area
+        self.tol_detect = tol_detect
+        self.tol_nms = tol_nms
+        self._lock = threading.Lock()
+        self._prev = None          # previous mosaic pixels on the device
+        self._prev_index = None
+        self._mask = None          # (H, W) uint8 CUDA mask of this tick
+        self._mask_index = None
+
+    def _mask_for(self, mosaic: Mosaic):
+        t = _dev.require_cuda()
+        with self._lock:
+            if self._mask_index == mosaic.frame_index:
+                return self._mask
+            cur = _dev.to_device(mosaic.pixels)
+            mask = None
+            if self._prev is not None and self._prev_index < mosaic.frame_index:
+                if self._prev.shape != cur.shape:
+                    raise ValueError("pixel dimensions differ")
+                h, w = cur.shape[:2]
+                mask = t.empty((h, w), dtype=t.uint8, device="cuda")
+                _lib.call("camx_mask_diff", cur.data_ptr(), self._prev.data_ptr(), h * w,
+                          int(self.t_diff), mask.data_ptr(), _dev.stream_handle())
+            self._prev, self._prev_index = cur, mosaic.frame_index
+            self._mask, self._mask_index = mask, mosaic.frame_index
+            return mask
+
+    def detect(self, window: DetectorWindow, mosaic: Mosaic) -> list[Detection]:
+        mask = self._mask_for(mosaic)
+        if mask is None:
+            return []
+        x0, y0 = max(window.x, 0), max(window.y, 0)
+        x1 = min(window.x + window.size, mosaic.width)
+        y1 = min(window.y + window.size, mosaic.height)
+        if x1 - x0 != y1 - y0:  # clipped non-square window: label the exact slice
+            sub = mask[y0:y1, x0:x1].contiguous()
+            side = max(x1 - x0, y1 - y0)
+            pad = _dev.torch().zeros((side, side), dtype=sub.dtype, device="cuda")
+            pad[: y1 - y0, : x1 - x0] = sub
+            comps = blob_components(pad, DetectorWindow(0, 0, side))
+        else:
+            comps = blob_components(mask, DetectorWindow(x0, y0, x1 - x0))
+        dets = []
+        for _, bx0, by0, bx1, by1, area in comps:
+            if area < self.min_area:
+                continue
+            box = BBox(x0 + int(bx0), y0 + int(by0), int(bx1 - bx0 + 1), int(by1 - by0 + 1))
+            p = min(1.0, 0.66 + 0.34 * min(1.0, int(area) / self.p_saturation_area))
+            dets.append(Detection(self.category, box, p, mosaic.frame_index,
+                                  DetectionSource.BLOB))
+        return _finalize(dets, mosaic.width, mosaic.height, self.tol_detect, self.tol_nms)

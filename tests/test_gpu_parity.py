@@ -623,3 +623,40 @@ def test_tiles_wider_than_a_camera():
     got = detect.tiles(torch.from_numpy(arr).cuda(), wins, 480, 208).cpu().numpy()
     for j, (_, x, y) in enumerate(wins):
         np.testing.assert_array_equal(got[j], O.resize_bilinear(O.crop(mosaic, x, y, 480), 208))
+
+
+class TestBlobDetector:               # test_detect.py:155-179 + scipy oracle
+    def test_two_patches(self):
+        base = gray(64, 48, 100)
+        moved = base.pixels.copy()
+        moved[10:15, 5:10] = 200
+        moved[30:35, 40:45] = 200
+        nxt = core.Frame(0, 1, 0, moved)
+        det = detect.BlobDetector(t_diff=20, min_area=4)
+        det.detect(detect.DetectorWindow(0, 0, 48), core.concat_mosaic([base]))
+        out = det.detect(detect.DetectorWindow(0, 0, 48), core.concat_mosaic([nxt]))
+        boxes = sorted((d.bbox for d in out), key=lambda b: b.y)
+        assert boxes == [core.BBox(5, 10, 5, 5), core.BBox(40, 30, 5, 5)]
+        assert all(d.category is core.Category.VEHICLE for d in out)
+        assert all(d.source is detect.DetectionSource.BLOB for d in out)
+
+    def test_no_previous_and_static(self):
+        f = gray(64, 48, 100)
+        assert detect.BlobDetector().detect(detect.DetectorWindow(0, 0, 48),
+                                            core.concat_mosaic([f])) == []
+        d = detect.BlobDetector()
+        d.detect(detect.DetectorWindow(0, 0, 48), core.concat_mosaic([gray(64, 48, 100)]))
+        g = core.Frame(0, 1, 0, np.full((48, 64, 3), 100, np.uint8))
+        assert d.detect(detect.DetectorWindow(0, 0, 48), core.concat_mosaic([g])) == []
+
+    @pytest.mark.parametrize("seed", [0, 1, 2, 3])
+    def test_components_vs_scipy(self, seed):
+        rng = np.random.default_rng(seed)
+        N, H, W = 3, 120, 90
+        p = [0.02, 0.2, 0.45, 0.6][seed]
+        masks = rng.random((N, H, W)) < p
+        mosaic = np.concatenate(list(masks), axis=1)
+        for (x, y, s) in [(0, 0, 120), (40, 0, 100), (150, 10, 110), (N * W - 64, H - 64, 64)]:
+            got = detect.blob_components(masks, detect.DetectorWindow(x, y, s), n_cams=N)
+            want = O.blob_components(mosaic[y:y + s, x:x + s])
+            np.testing.assert_array_equal(got[:, 1:], want)
