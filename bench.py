@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-batch", type=int, default=8)
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     return ap.parse_args()
 
 
@@ -238,9 +239,13 @@ def run_camx(args):
         n_tiles = len(ac.tile_windows(960)) * B
         tiles_buf = torch.empty((n_tiles, 416, 416, 3), dtype=torch.uint8, device="cuda")
 
+    use_graph = not args.no_graph and world == 1 and not tiles_mode
+
     def step():
         if tiles_mode:
             return ac.correct_and_tile(frames, out=out, tiles=tiles_buf, stream=stream)[0]
+        if use_graph:  # CUDA graph replay of K1 -> K2 -> K3 (+ state carry)
+            return ac.correct_graphed(frames, out)
         return ac.correct(frames, out, stream=stream)
 
     with torch.cuda.stream(stream):
@@ -278,6 +283,9 @@ def run_camx(args):
             barrier()
     finally:
         _lib.call = orig_call
+    if use_graph:  # replays do not pass through _lib.call: same kernels as an eager step
+        per_step = 3 + (1 if (mode is ExposureMode.OBJECT_REMOVAL and B > 1) else 0)
+        n_launch[0] = per_step * args.steps
 
     # roofline leg: the dominant kernel (K3 apply) alone, same buffers and
     # maps as the last step, CUDA events on its stream around each launch
@@ -389,7 +397,8 @@ def run_camx(args):
                        "cameras_per_gpu": count, "frame": f"{W}x{H}",
                        "step": "K1 band stats + K2 seam solve + K3 apply per array-frame",
                        "l2": "inputs larger than L2 (batch >> 126 MB)",
-                       "parallelism": f"camera-shard{world}" if world > 1 else "single"},
+                       "parallelism": f"camera-shard{world}" if world > 1 else "single",
+                       "launch": "cuda-graph replay" if use_graph else "eager (PDL-chained)"},
             "roofline": {"bound": "hbm", "kernel": "camx apply_tma_kernel (K3)",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,

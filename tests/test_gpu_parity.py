@@ -660,3 +660,25 @@ class TestBlobDetector:               # test_detect.py:155-179 + scipy oracle
             got = detect.blob_components(masks, detect.DetectorWindow(x, y, s), n_cams=N)
             want = O.blob_components(mosaic[y:y + s, x:x + s])
             np.testing.assert_array_equal(got[:, 1:], want)
+
+
+@pytest.mark.parametrize("mode", [xp.ExposureMode.SMOOTHING, xp.ExposureMode.OBJECT_REMOVAL])
+def test_graph_replay_matches_eager(mode):
+    """correct_graphed (CUDA graph replay, buffers refilled in place) follows
+    the same tick loop as eager correct() over a stream of batches."""
+    N, H, W, B = 3, 96, 128, 2
+    seq = [np.stack([O.synthetic_array(N, H, W, seed=90, objects=3, frame_index=2 * i + t)
+                     for t in range(B)]) for i in range(4)]
+    cfg = xp.ExposureConfig(band_width=16, blocks=4)
+    eager = ArrayCorrector(N, H, W, cfg, mode)
+    graphed = ArrayCorrector(N, H, W, cfg, mode)
+    buf = torch.empty((B, N, H, W, 3), dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(buf)
+    for batch in seq:
+        d = torch.from_numpy(batch).cuda()
+        want = eager.correct(d)
+        buf.copy_(d)
+        got = graphed.correct_graphed(buf, out)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got.out.cpu().numpy(), want.out.cpu().numpy())
+        np.testing.assert_array_equal(got.gain.cpu().numpy(), want.gain.cpu().numpy())
