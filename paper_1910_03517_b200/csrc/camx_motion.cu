@@ -143,7 +143,9 @@ extern "C" int camx_window_counts(const uint8_t *mask, const uint8_t *cur, const
   if (n_cams < 1 || height < 1 || width < 1 || size < 1 || n_windows < 0 || !counts_out)
     return CAMX_EINVAL;
   if ((mask == nullptr) == (cur == nullptr || prev == nullptr)) return CAMX_EINVAL;
-  if (size > height || size > n_cams * width) return CAMX_EINVAL;
+  // windows may extend past this (sharded) mosaic: columns outside it are
+  // skipped, so a rank counts only its own cameras' share
+  if (size > height) return CAMX_EINVAL;
   cudaStream_t s = as_stream(stream);
   if (n_windows == 0) return CAMX_OK;
   if (!windows) return CAMX_EINVAL;

@@ -73,3 +73,30 @@ def sharded_corrector(n_cams: int, height: int, width: int,
     ex = make_stats_exchange(n_cams, group) if world > 1 else None
     return ArrayCorrector(n_cams, height, width, cfg, mode, wrap=wrap, histograms=histograms,
                           cam_begin=begin, cam_count=count, exchange=ex)
+
+
+def sharded_window_counts(origins, size: int, *, cur=None, prev=None, mask=None,
+                          t_diff: int = 20, n_cams: int, width: int, group=None, counts_fn=None):
+    """difference_plan's per-window on-pixel counts (attention.py:96-100) over
+    a camera-sharded array: this rank counts the window pixels that fall on
+    its own cameras (origins shifted into its local mosaic; columns outside
+    it are skipped by K4), then one all-reduce(sum) of the int64 counts gives
+    every rank the whole-array counts - and so the same ranking.
+    cur/prev (or mask) hold only this rank's cameras.  `counts_fn` replaces
+    the K4 call (tests)."""
+    import numpy as np
+    import torch.distributed as dist
+    t = _dev.torch()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    begin, count = camera_partition(n_cams, world)[rank]
+    local = [(x - begin * width, y) for (x, y) in origins]
+    if counts_fn is None:
+        from .attention import window_counts
+        counts_fn = lambda org, s: window_counts(org, s, cur=cur, prev=prev, mask=mask,  # noqa: E731
+                                                 t_diff=t_diff, n_cams=count)
+    part = t.as_tensor(np.asarray(counts_fn(local, size), dtype=np.int64))
+    if dist.get_backend(group) == "nccl":
+        part = part.cuda()
+    dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+    return part.cpu().numpy()

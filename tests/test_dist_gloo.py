@@ -69,3 +69,48 @@ def test_stats_allgather_reassembles_array(n_cams):
     for rank, same, shape in res:
         assert same, f"rank {rank} re-assembled records differ"
         assert shape == (B, n_cams, 2, K, 112)
+
+
+def _counts_worker(rank, world, port, q):
+    """Each rank counts its own cameras' share of every window on the CPU
+    (numpy stand-in for K4 with the same local-coordinate clipping), then the
+    all-reduce must give the whole-array counts."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1910_03517_b200.dist import camera_partition, sharded_window_counts
+        n_cams, H, W, S = 5, 40, 30, 25
+        rng = np.random.default_rng(7)
+        mosaic = rng.random((H, n_cams * W)) < 0.3
+        origins = [(x, y) for y in (0, 15) for x in range(0, n_cams * W - S + 1, 17)]
+        begin, count = camera_partition(n_cams, world)[rank]
+        local_mask = mosaic[:, begin * W:(begin + count) * W]
+
+        def cpu_counts(org, s):
+            out = []
+            for (x, y) in org:
+                x0, x1 = max(x, 0), min(x + s, local_mask.shape[1])
+                out.append(int(local_mask[y:y + s, x0:x1].sum()) if x1 > x0 else 0)
+            return out
+
+        got = sharded_window_counts(origins, S, n_cams=n_cams, width=W, counts_fn=cpu_counts)
+        want = [int(mosaic[y:y + S, x:x + S].sum()) for (x, y) in origins]
+        q.put((rank, list(map(int, got)) == want))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_window_counts_allreduce():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_counts_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res

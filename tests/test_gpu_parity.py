@@ -682,3 +682,22 @@ def test_graph_replay_matches_eager(mode):
         torch.cuda.synchronize()
         np.testing.assert_array_equal(got.out.cpu().numpy(), want.out.cpu().numpy())
         np.testing.assert_array_equal(got.gain.cpu().numpy(), want.gain.cpu().numpy())
+
+
+def test_window_counts_on_a_camera_shard():
+    """K4 on one rank's cameras with origins shifted into local coordinates
+    counts exactly that shard's share of each window (dist.sharded_window_counts)."""
+    from paper_1910_03517_b200.dist import camera_partition
+    rng = np.random.default_rng(17)
+    N, H, W, S = 5, 120, 100, 96
+    cur = rng.integers(0, 256, (N, H, W, 3), dtype=np.uint8)
+    prev = cur.copy()
+    prev[rng.random((N, H, W)) < 0.1] ^= 0x80
+    full = np.concatenate([O.mask_diff(cur[c], prev[c], 20) for c in range(N)], axis=1)
+    origins = [(x, y) for y in (0, 24) for x in range(0, N * W - S + 1, 37)]
+    total = np.zeros(len(origins), np.int64)
+    for (b, c) in camera_partition(N, 2):
+        local = [(x - b * W, y) for (x, y) in origins]
+        total += at.window_counts(local, S, cur=cur[b:b + c], prev=prev[b:b + c], n_cams=c)
+    want = np.array([full[y:y + S, x:x + S].sum() for (x, y) in origins])
+    np.testing.assert_array_equal(total, want)
