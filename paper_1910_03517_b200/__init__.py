@@ -14,4 +14,6 @@ All arithmetic runs in libcamx.so (sm_100a); see include/camx.h.
 
 __version__ = "0.1.0"
 
-from .core import BBox, Category, Frame, Mosaic, abs_diff_threshold, concat_mosaic, iou  # noqa: F401
+from .core import BBox, Category, Frame, Mosaic, abs_diff_threshold, concat_mosaic, iou
+
+__all__ = ["BBox", "Category", "Frame", "Mosaic", "abs_diff_threshold", "concat_mosaic", "iou"]

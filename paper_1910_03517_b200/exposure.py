@@ -17,8 +17,9 @@ reference's per-call numpy API; the batched device-resident path is
 
 from __future__ import annotations
 
+import ctypes
 import enum
-from dataclasses import dataclass, field, replace
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -319,7 +320,6 @@ def _solve_pair(rec, prev_maps, mode, cfg, use_prev, seam_id) -> SeamMaps:
     gain = t.empty((1, 1, 2, K, 3), dtype=t.float64, device="cuda")
     off = t.empty_like(gain)
     sc = _solve_config(mode, cfg, prev_maps is not None, use_prev)
-    import ctypes
     _lib.call("camx_seam_solve", rec.data_ptr(), 1, 2, 0, ctypes.byref(sc), _dev.ptr(pg),
               _dev.ptr(po), gain.data_ptr(), off.data_ptr(), None, _dev.stream_handle())
     g, o = _dev.to_host(gain)[0, 0], _dev.to_host(off)[0, 0]
@@ -442,7 +442,3 @@ def read_maps_table(text: str, band_width: int = 32) -> list[SeamMaps]:
             gain[bi, ci], off[bi, ci] = a, b
         sides.setdefault(sid, {})[side] = ExposureMap(sid, side, band_width, gain, off)
     return [SeamMaps(sides[s][Side.LEFT], sides[s][Side.RIGHT]) for s in sorted(sides)]
-
-
-def _replace_map(m: ExposureMap, **kw) -> ExposureMap:
-    return replace(m, _cache={}, **kw)
