@@ -77,7 +77,19 @@ __device__ __noinline__ void fused_solve_tail(const StatsParams &p, int64_t unit
 
 constexpr int kStatsWarps = 4;  // warps per (image, side, block) unit = per CTA
 constexpr int kCounterWords = 3 * 64 * 32;  // per warp: 3 ch x 64 bin-quads x 32 lanes
-constexpr int kQuadBatch = 8;  // a standard 32-px x 96-row band unit: one batch
+constexpr int kQuadBatch = 8;
+// dp4a byte selectors of channel c in word k of a 12-byte pixel quad
+// (bytes r g b r | g b r g | b r g b)
+//   r: w0 b0,b3  w1 b2  w2 b1;  g: w0 b1  w1 b0,b3  w2 b2;  b: w0 b2  w1 b1  w2 b0,b3
+__host__ __device__ constexpr uint32_t quad_sel(int c, int k) {
+  return ((c + 3 - k) % 3 == 0) ? 0x01000001u : ((c + 3 - k) % 3 == 1) ? 0x00000100u : 0x00010000u;
+}  // a standard 32-px x 96-row band unit: one batch
+
+__device__ __forceinline__ uint64_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
@@ -205,6 +217,8 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
   if (QUAD) {
     const int qpr = p.bw >> 2;
     const int nq = rows * qpr;
+    const bool pow2 = (qpr & (qpr - 1)) == 0;
+    const int qsh = __ffs(qpr) - 1;
     for (int i0 = warp * 32; i0 < nq; i0 += kStride * kQuadBatch) {
       uint32_t w[kQuadBatch][3], pw[kQuadBatch][3], mw[kQuadBatch];
       bool live[kQuadBatch];
@@ -213,8 +227,9 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
         const int i = i0 + u * kStride + lane;
         live[u] = i < nq;
         const int ii = live[u] ? i : 0;
-        const int row = r0 + ii / qpr;
-        const int col = col0 + (ii - (ii / qpr) * qpr) * 4;
+        const int rq = pow2 ? (ii >> qsh) : ii / qpr;
+        const int row = r0 + rq;
+        const int col = col0 + (ii - rq * qpr) * 4;
         const int64_t off = row * row_bytes + static_cast<int64_t>(col) * 3;
         const uint32_t *wp = reinterpret_cast<const uint32_t *>(base + off);
         w[u][0] = __ldg(wp);
@@ -229,15 +244,73 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
         if (MASKMODE == 1)
           mw[u] = __ldg(reinterpret_cast<const uint32_t *>(mbase + static_cast<int64_t>(row) * p.W + col));
       }
+      if (!HIST && MASKMODE != 1) {
+        // Channel sums / sums of squares with dp4a: in a quad the byte
+        // positions of each channel are fixed (r g b r | g b r g | b r g b),
+        // so constant byte masks select them.  32-bit per batch (<= 32 px
+        // per lane), widened once per batch.
+        uint32_t rs[3] = {0, 0, 0}, rq[3] = {0, 0, 0}, vs[3] = {0, 0, 0}, vq[3] = {0, 0, 0};
+        uint32_t nv = 0;
 #pragma unroll
-      for (int u = 0; u < kQuadBatch; ++u) {
-        if (!live[u]) continue;
-        const uint32_t ex = quad_exclusion<MASKMODE>(p, w[u], pw[u], mw[u]);
-        const uint32_t *q = w[u];
-        add_pixel<HIST>(a, cnt, lane, q[0] & 0xFF, (q[0] >> 8) & 0xFF, (q[0] >> 16) & 0xFF, ex & 1);
-        add_pixel<HIST>(a, cnt, lane, q[0] >> 24, q[1] & 0xFF, (q[1] >> 8) & 0xFF, ex & 2);
-        add_pixel<HIST>(a, cnt, lane, (q[1] >> 16) & 0xFF, q[1] >> 24, q[2] & 0xFF, ex & 4);
-        add_pixel<HIST>(a, cnt, lane, (q[2] >> 8) & 0xFF, (q[2] >> 16) & 0xFF, q[2] >> 24, ex & 8);
+        for (int u = 0; u < kQuadBatch; ++u) {
+          if (!live[u]) continue;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              const uint32_t sel = quad_sel(c, k);
+              rs[c] = __dp4a(w[u][k], sel, rs[c]);
+              const uint32_t m = w[u][k] & (sel * 0xFFu);
+              rq[c] = __dp4a(m, m, rq[c]);
+            }
+          }
+          if (MASKMODE == 2) {
+            const uint32_t ex = quad_exclusion<MASKMODE>(p, w[u], pw[u], mw[u]);
+            nv += 4 - __popc(ex);
+            // keep-masks of the 12 bytes: pixel e kept -> its 3 bytes
+            const uint32_t kp = (~ex) & 0xFu;
+            const uint32_t kb = (kp & 1 ? 0xFFu : 0u) | (kp & 2 ? 0xFF00u : 0u) |
+                                (kp & 4 ? 0xFF0000u : 0u) | (kp & 8 ? 0xFF000000u : 0u);
+            const uint32_t km0 = __byte_perm(kb, 0, 0x1000);  // px 0 0 0 1
+            const uint32_t km1 = __byte_perm(kb, 0, 0x2211);  // px 1 1 2 2
+            const uint32_t km2 = __byte_perm(kb, 0, 0x3332);  // px 2 3 3 3
+            const uint32_t mw0 = w[u][0] & km0, mw1 = w[u][1] & km1, mw2 = w[u][2] & km2;
+            const uint32_t mm[3] = {mw0, mw1, mw2};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+#pragma unroll
+              for (int k = 0; k < 3; ++k) {
+                const uint32_t sel = quad_sel(c, k);
+                vs[c] = __dp4a(mm[k], sel, vs[c]);
+                const uint32_t m = mm[k] & (sel * 0xFFu);
+                vq[c] = __dp4a(m, m, vq[c]);
+              }
+            }
+          } else {
+            nv += 4;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          a.raw_s[c] += rs[c];
+          a.raw_q[c] += rq[c];
+          if (MASKMODE == 2) {
+            a.val_s[c] += vs[c];
+            a.val_q[c] += vq[c];
+          }
+        }
+        a.nvalid += nv;
+      } else {
+#pragma unroll
+        for (int u = 0; u < kQuadBatch; ++u) {
+          if (!live[u]) continue;
+          const uint32_t ex = quad_exclusion<MASKMODE>(p, w[u], pw[u], mw[u]);
+          const uint32_t *q = w[u];
+          add_pixel<HIST>(a, cnt, lane, q[0] & 0xFF, (q[0] >> 8) & 0xFF, (q[0] >> 16) & 0xFF, ex & 1);
+          add_pixel<HIST>(a, cnt, lane, q[0] >> 24, q[1] & 0xFF, (q[1] >> 8) & 0xFF, ex & 2);
+          add_pixel<HIST>(a, cnt, lane, (q[1] >> 16) & 0xFF, q[1] >> 24, q[2] & 0xFF, ex & 4);
+          add_pixel<HIST>(a, cnt, lane, (q[2] >> 8) & 0xFF, (q[2] >> 16) & 0xFF, q[2] >> 24, ex & 8);
+        }
       }
       if (HIST) {
         since_flush += 4 * kQuadBatch;
@@ -319,15 +392,25 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
       a.val_q[c] = a.raw_q[c];
     }
   }
+  // Warp sums.  A unit of <= 66051 pixels has every sum of squares below
+  // 2^32, so the shuffles run on 32-bit halves; MASKMODE 0 (no exclusion)
+  // reduces only the raw sums (valid == raw, count == area).
   uint64_t r[13];
+  const bool narrow = static_cast<int64_t>(rows) * p.bw <= 66051;
+  constexpr bool kMasked = HIST || MASKMODE != 0;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    r[c] = warp_sum_u64(a.val_s[c]);
-    r[3 + c] = warp_sum_u64(a.val_q[c]);
-    r[6 + c] = warp_sum_u64(a.raw_s[c]);
-    r[9 + c] = warp_sum_u64(a.raw_q[c]);
+    r[6 + c] = narrow ? warp_sum_u32(static_cast<uint32_t>(a.raw_s[c])) : warp_sum_u64(a.raw_s[c]);
+    r[9 + c] = narrow ? warp_sum_u32(static_cast<uint32_t>(a.raw_q[c])) : warp_sum_u64(a.raw_q[c]);
+    if (kMasked) {
+      r[c] = narrow ? warp_sum_u32(static_cast<uint32_t>(a.val_s[c])) : warp_sum_u64(a.val_s[c]);
+      r[3 + c] = narrow ? warp_sum_u32(static_cast<uint32_t>(a.val_q[c])) : warp_sum_u64(a.val_q[c]);
+    } else {
+      r[c] = 0;
+      r[3 + c] = 0;
+    }
   }
-  r[12] = warp_sum_u64(a.nvalid);
+  r[12] = kMasked ? warp_sum_u32(a.nvalid) : 0;
   if (lane == 0) {
 #pragma unroll
     for (int i = 0; i < 13; ++i) part[warp][i] = r[i];
@@ -339,11 +422,11 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
       for (int w2 = 1; w2 < kStatsWarps; ++w2) r[i] += part[w2][i];
     camx_band_stat o;
     o.area = static_cast<int64_t>(rows) * p.bw;
-    o.valid = static_cast<int64_t>(r[12]);
+    o.valid = kMasked ? static_cast<int64_t>(r[12]) : o.area;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      o.sum[c] = r[c];
-      o.sumsq[c] = r[3 + c];
+      o.sum[c] = kMasked ? r[c] : r[6 + c];
+      o.sumsq[c] = kMasked ? r[3 + c] : r[9 + c];
       o.raw_sum[c] = r[6 + c];
       o.raw_sumsq[c] = r[9 + c];
     }
