@@ -188,6 +188,7 @@ def run_reference(args):
 # ------------------------------------------------------------------ GPU arm
 
 def run_camx(args):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -289,16 +290,35 @@ def run_camx(args):
 
     # roofline leg: the dominant kernel (K3 apply) alone, same buffers and
     # maps as the last step, CUDA events on its stream around each launch
+    # (config 5: the fused apply+tile kernel and its fix-up, whose
+    # algorithmic bytes add the tile writes to K3's read + write)
     k3_ev = []
     k3_launch_bytes = 6 * B * count * H * W
+    k3_name = "camx apply_tma_kernel (K3)"
+    if tiles_mode:
+        wins = sorted((b, x, y) for b in range(B) for (x, y) in ac.tile_windows(960))
+        wins = sorted(wins, key=lambda w: w[0])
+        per_b = np.bincount(np.asarray([w[0] for w in wins]), minlength=B)
+        w_dev = torch.as_tensor(np.asarray(wins, dtype=np.int32).reshape(-1, 3), device="cuda")
+        off_dev = torch.as_tensor(np.concatenate([[0], np.cumsum(per_b)]).astype(np.int32),
+                                  device="cuda")
+        k3_launch_bytes += tiles_buf.numel()
+        k3_name = "camx apply_tma_kernel<fused tiles> + tile_fixup (K3+K5)"
     with torch.cuda.stream(stream):
         for _ in range(max(3, min(args.steps, 20))):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            _lib.call("camx_apply_array", frames.data_ptr(), out.data_ptr(), B, begin, count,
-                      n_cams, int(wrap), H, W, cfg.blocks, res.gain.data_ptr(),
-                      res.offset.data_ptr(), stream.cuda_stream)
+            if tiles_mode:
+                _lib.call("camx_correct_and_tile", frames.data_ptr(), out.data_ptr(), B, n_cams,
+                          int(wrap), H, W, cfg.blocks, res.gain.data_ptr(),
+                          res.offset.data_ptr(), w_dev.data_ptr(), off_dev.data_ptr(),
+                          len(wins), int(per_b.max()), 960, 416, tiles_buf.data_ptr(),
+                          stream.cuda_stream)
+            else:
+                _lib.call("camx_apply_array", frames.data_ptr(), out.data_ptr(), B, begin, count,
+                          n_cams, int(wrap), H, W, cfg.blocks, res.gain.data_ptr(),
+                          res.offset.data_ptr(), stream.cuda_stream)
             e1.record(stream)
             k3_ev.append((e0, e1))
     torch.cuda.synchronize()
@@ -399,7 +419,7 @@ def run_camx(args):
                        "l2": "inputs larger than L2 (batch >> 126 MB)",
                        "parallelism": f"camera-shard{world}" if world > 1 else "single",
                        "launch": "cuda-graph replay" if use_graph else "eager (PDL-chained)"},
-            "roofline": {"bound": "hbm", "kernel": "camx apply_tma_kernel (K3)",
+            "roofline": {"bound": "hbm", "kernel": k3_name,
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_kind": peak_kind, "k3_ms_per_launch": round(k3_ms, 4),

@@ -235,6 +235,20 @@ int camx_tiles(const uint8_t *images, int32_t n_cams, int32_t height,
                int32_t size, int32_t out_size, uint8_t *tiles_out,
                void *stream);
 
+/* Tiles over a camera shard (multi-GPU).  images: this rank's
+ * cameras [n_batch][n_cams][H][W][3], holding mosaic columns
+ * [col_begin, col_begin + n_cams*W); windows: (batch, x, y) in GLOBAL mosaic
+ * coordinates.  Writes exactly the output columns whose first column tap
+ * lies on this shard (every output pixel has one owner); the second tap may
+ * be the next shard's first column, passed as halo [n_batch][H][3] (NULL
+ * only for the last shard).  Other pixels of tiles_out are not written:
+ * zero-fill and sum the ranks' partials (dist.sharded_tiles).  Replaces the
+ * crop of ExternalDetector.detect (detect.py:297-300) on a sharded mosaic. */
+int camx_tiles_shard(const uint8_t *images, int32_t n_cams, int32_t height,
+                     int32_t width, int32_t col_begin, const uint8_t *halo,
+                     const int32_t *windows, int32_t n_tiles, int32_t size,
+                     int32_t out_size, uint8_t *tiles_out, void *stream);
+
 /* Stage 3 + 4b (config 5): apply the array correction AND cut the tiles
  * from the corrected pixels.  When the geometry allows (aligned rows, at
  * most 64 windows per array-frame, out_size <= 3*size) this is ONE pass

@@ -72,6 +72,7 @@ SIGNATURES = {
     "camx_mask_diff": [P, P, I64, I32, P, P],
     "camx_window_counts": [P, P, P, I32, I32, I32, I32, P, I32, I32, P, P],
     "camx_tiles": [P, I32, I32, I32, P, I32, I32, I32, P, P],
+    "camx_tiles_shard": [P, I32, I32, I32, I32, P, P, I32, I32, I32, P, P],
     "camx_correct_and_tile": [P, P, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, I32, I32, I32,
                               P, P],
     "camx_correct_batch_tiles": [P, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P, P,

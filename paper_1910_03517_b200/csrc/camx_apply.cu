@@ -618,7 +618,8 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
 // is done, refill the slot of stage st-1 (its last row was stage st's
 // "previous row").  No CTA-wide barrier inside the loop: correctors only
 // ever wait for TMA data.
-constexpr int kWsStages = 8;
+constexpr int kWsStages = 6;   // raw TMA ring (refilled as soon as corrected)
+constexpr int kWsCStages = 8;  // corrected-row ring read by the resamplers
 constexpr int kWsResamplers = 96;  // 3 warps (4 + 3 warps x 92 regs: 3 CTAs per SM)
 constexpr int kWsThreads = kApplyThreads + kWsResamplers;
 
@@ -653,7 +654,7 @@ __device__ __forceinline__ void build_hits_ws(const FuseSmem &fs, const TileFuse
       const int h = atomicAdd(cnt, 1);
       auto off = [&](int Rw) {
         const int sidx = (Rw - r0) / kTmaRows, ri = (Rw - r0) % kTmaRows;
-        return ((sidx % kWsStages) * kTmaRows + ri) * kApplyThreads * 16;
+        return ((sidx % kWsCStages) * kTmaRows + ri) * kApplyThreads * 16;
       };
       const uint64_t trow = reinterpret_cast<uint64_t>(
           q.tiles + (static_cast<int64_t>(w.x) * q.out + oy) * q.out * 3);
@@ -667,9 +668,11 @@ __device__ __forceinline__ void build_hits_ws(const FuseSmem &fs, const TileFuse
 
 __global__ void __launch_bounds__(kWsThreads, 3)
     apply_tile_ws_kernel(const ApplyParams p, const TileFuse q) {
-  extern __shared__ __align__(128) uint4 ring[];  // [kWsStages][kTmaRows][kApplyThreads]
-  __shared__ __align__(8) uint64_t full[kWsStages];
-  __shared__ __align__(8) uint64_t corr[kWsStages];
+  extern __shared__ __align__(128) uint4 ring[];  // raw [kWsStages][2][128], then corrected
+  __shared__ __align__(8) uint64_t full[kWsStages];   // raw slot filled (TMA)
+  __shared__ __align__(8) uint64_t corr[kWsCStages];  // corrected slot written (4 warps)
+  __shared__ __align__(8) uint64_t cfree[kWsCStages]; // corrected slot released (resamplers)
+  uint4 *cring = ring + kWsStages * kTmaRows * kApplyThreads;
   int64_t item = blockIdx.x;
   const int cg = static_cast<int>(item % p.col_groups);
   item /= p.col_groups;
@@ -702,9 +705,10 @@ __global__ void __launch_bounds__(kWsThreads, 3)
   };
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kWsStages; ++i) {
-      mbar_init(&full[i], 1);
+    for (int i = 0; i < kWsStages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < kWsCStages; ++i) {
       mbar_init(&corr[i], kApplyThreads / 32);  // one arrival per corrector warp
+      mbar_init(&cfree[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int st = 0; st < min(kWsStages, nst); ++st) issue(st);
@@ -712,7 +716,7 @@ __global__ void __launch_bounds__(kWsThreads, 3)
 
   // tables and the intersecting-window list (geometry only)
   FuseSmem fs =
-      carve_fuse(reinterpret_cast<uint8_t *>(ring + kWsStages * kTmaRows * kApplyThreads), q.out,
+      carve_fuse(reinterpret_cast<uint8_t *>(cring + kWsCStages * kTmaRows * kApplyThreads), q.out,
                  q.size);
   const int64_t bfr = img / p.cam_count;
   const int cam = p.cam_begin + static_cast<int>(img % p.cam_count);
@@ -788,31 +792,37 @@ __global__ void __launch_bounds__(kWsThreads, 3)
     uint8_t *dst = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
     for (int st = 0; st < nst; ++st) {
       const int slot = st % kWsStages;
+      const int cslot = st % kWsCStages;
       mbar_wait(&full[slot], (st / kWsStages) & 1);
       const int rr = min(kTmaRows, nrows - st * kTmaRows);
+      uint4 v[kTmaRows];
       if (active) {
-        uint4 v[kTmaRows];
 #pragma unroll
         for (int i = 0; i < kTmaRows; ++i)
           if (i < rr) v[i] = ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x];
+      }
+      named_bar(2, kApplyThreads);  // raw slot consumed by every corrector: refill now
+      if (threadIdx.x == 0 && st + kWsStages < nst) issue(st + kWsStages);
+      if (st >= kWsCStages) mbar_wait(&cfree[cslot], ((st / kWsCStages) - 1) & 1);
+      if (active) {
 #pragma unroll
         for (int i = 0; i < kTmaRows; ++i)
           if (i < rr) {
             const uint4 o = correct16(v[i], cf);
             st_stream_v4(dst + static_cast<int64_t>(st * kTmaRows + i) * rb, o);
-            ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x] = o;
+            cring[(cslot * kTmaRows + i) * kApplyThreads + threadIdx.x] = o;
           }
       }
       __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&corr[slot]);
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&corr[cslot]);
     }
   } else {
     // ---------------------------------------------------------- resamplers
     const int rt = threadIdx.x - kApplyThreads;  // 0..kWsResamplers-1
-    const uint8_t *ringb = reinterpret_cast<const uint8_t *>(ring);
+    const uint8_t *ringb = reinterpret_cast<const uint8_t *>(cring);
     for (int st = 0; st < nst; ++st) {
-      const int slot = st % kWsStages;
-      mbar_wait(&corr[slot], (st / kWsStages) & 1);
+      const int cslot = st % kWsCStages;
+      mbar_wait(&corr[cslot], (st / kWsCStages) & 1);
       if (rt < 32) build_hits_ws(fs, q, p, st, r0, nrows, cam, cb0);
       named_bar(1, kWsResamplers);
       const int nhit = fs.counts[1];
@@ -824,8 +834,9 @@ __global__ void __launch_bounds__(kWsThreads, 3)
                             static_cast<uint32_t>(h1.x)),
                         h1.z & 0xFFFF, h1.z >> 16, rt, kWsResamplers, fs);
       }
-      named_bar(1, kWsResamplers);  // stage st resampled: hits reusable, slot st-1 free
-      if (rt == 0 && st >= 1 && st - 1 + kWsStages < nst) issue(st - 1 + kWsStages);
+      named_bar(1, kWsResamplers);  // stage st resampled: hits reusable
+      // the corrected rows of stage st-1 (previous-row taps) are no longer needed
+      if (rt == 0 && st >= 1) mbar_arrive(&cfree[(st - 1) % kWsCStages]);
     }
   }
 }
@@ -995,7 +1006,8 @@ static int launch_apply_tiles(ApplyParams &p, TileFuse &q, int32_t n_tiles,
   if (!plan_fast(p)) return CAMX_EINVAL;
   // strict downscale: no clamped taps, each source row is the second tap of <= 1 output row
   if (max_tiles_per_frame > kFuseMaxWin || q.out >= q.size || q.size > 4096) return CAMX_EINVAL;
-  if (fuse_smem_bytes(q) + kWsStages * kTmaRows * kApplyThreads * 16 > 110 * 1024) return CAMX_EINVAL;
+  if (fuse_smem_bytes(q) + (kWsStages + kWsCStages) * kTmaRows * kApplyThreads * 16 > 200 * 1024)
+    return CAMX_EINVAL;
   static const bool use_ws = [] {
     const char *e = getenv("CAMX_TILE_WS");
     return e != nullptr && e[0] == '1';
@@ -1005,7 +1017,7 @@ static int launch_apply_tiles(ApplyParams &p, TileFuse &q, int32_t n_tiles,
     st = launch_tma<true, kFuseRows, kFuseStages>(p, q, stream);
   } else {
     const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
-    const size_t smem = kWsStages * kTmaRows * kApplyThreads * 16 + fuse_smem_bytes(q);
+    const size_t smem = (kWsStages + kWsCStages) * kTmaRows * kApplyThreads * 16 + fuse_smem_bytes(q);
     cudaError_t e = cudaFuncSetAttribute(apply_tile_ws_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));

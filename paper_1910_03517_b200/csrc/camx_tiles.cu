@@ -165,6 +165,56 @@ __global__ void __launch_bounds__(kTileThreads) tiles_rows_kernel(const TilePara
   }
 }
 
+// ---- camera-sharded tiles ---------------------------------------
+// Rank g holds cameras [c0, c0 + n_cams) of the array, i.e. mosaic columns
+// [col_begin, col_begin + n_cams * W).  Output column ox of a window belongs
+// to the rank that holds its first column tap (x0 + i0(ox)); its second tap
+// may be the first column of the next rank, supplied as `halo` (B, H, 3) -
+// the 1-pixel corrected halo column.  Output pixels of other ranks' columns
+// are left untouched (the caller zero-fills and sums the partials).
+// Per-pixel gather: this path runs only for windows that touch a shard.
+struct ShardTileParams {
+  TileParams t;
+  int32_t col_begin;    // global mosaic column of local column 0
+  int32_t local_cols;   // n_cams * W
+  const uint8_t *halo;  // (B, H, 3) or nullptr
+};
+
+__device__ __forceinline__ const uint8_t *shard_px(const ShardTileParams &p, int64_t b, int row,
+                                                   int gx) {
+  const int lx = gx - p.col_begin;
+  if (lx == p.local_cols) return p.halo + (b * p.t.H + row) * 3;
+  return mosaic_px(p.t, b, row, lx);
+}
+
+__global__ void tiles_shard_kernel(const ShardTileParams p) {
+  const int t = blockIdx.y;
+  const int64_t b = p.t.wins[3 * t];
+  const int x0 = p.t.wins[3 * t + 1], y0 = p.t.wins[3 * t + 2];
+  const int out = p.t.out;
+  const int64_t npx = static_cast<int64_t>(out) * out;
+  uint8_t *dst = p.t.tiles + static_cast<int64_t>(t) * npx * 3;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < npx;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int oy = static_cast<int>(q / out);
+    const int ox = static_cast<int>(q - static_cast<int64_t>(oy) * out);
+    int x_0 = ox, x_1 = ox, wx = 0, y_0 = oy, y_1 = oy, wy = 0;
+    if (out != p.t.size) {
+      src_coord_w(ox, p.t.scale, p.t.size, x_0, x_1, wx);
+      src_coord_w(oy, p.t.scale, p.t.size, y_0, y_1, wy);
+    }
+    const int g0 = x0 + x_0;
+    if (g0 < p.col_begin || g0 >= p.col_begin + p.local_cols) continue;  // another rank's column
+    const uint8_t *a = shard_px(p, b, y0 + y_0, g0);
+    const uint8_t *bb = shard_px(p, b, y0 + y_0, x0 + x_1);
+    const uint8_t *c = shard_px(p, b, y0 + y_1, g0);
+    const uint8_t *d = shard_px(p, b, y0 + y_1, x0 + x_1);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+      dst[3 * q + ch] = static_cast<uint8_t>(bilerp_fx(a[ch], bb[ch], c[ch], d[ch], wx, wy));
+  }
+}
+
 // ---- seam cost ------------------------------------------------------------
 __device__ __forceinline__ void box_mean(const uint8_t *img, int W, int f, int row2, int col2,
                                          double out[3]) {
@@ -284,5 +334,35 @@ extern "C" int camx_seam_cost(const uint8_t *left, const uint8_t *right, int64_t
   if (n_pairs == 0) return CAMX_OK;
   seam_cost_kernel<<<static_cast<unsigned>(n_pairs), 128, 0, as_stream(stream)>>>(
       left, right, height, left_width, right_width, factor, cost_out);
+  return launch_status();
+}
+
+extern "C" int camx_tiles_shard(const uint8_t *images, int32_t n_cams, int32_t height,
+                                int32_t width, int32_t col_begin, const uint8_t *halo,
+                                const int32_t *windows, int32_t n_tiles, int32_t size,
+                                int32_t out_size, uint8_t *tiles_out, void *stream) {
+  if (!images || col_begin < 0 || n_cams < 1 || height < 1 || width < 1 || size < 1 ||
+      out_size < 1 || n_tiles < 0 || size > height)
+    return CAMX_EINVAL;
+  if (n_tiles > 0 && (windows == nullptr || tiles_out == nullptr)) return CAMX_EINVAL;
+  if (n_tiles == 0) return CAMX_OK;
+  ShardTileParams p{};
+  p.t.img = images;
+  p.t.n_cams = n_cams;
+  p.t.H = height;
+  p.t.W = width;
+  p.t.size = size;
+  p.t.out = out_size;
+  p.t.wins = windows;
+  p.t.tiles = tiles_out;
+  p.t.scale = static_cast<float>(size) / static_cast<float>(out_size);
+  p.col_begin = col_begin;
+  p.local_cols = n_cams * width;
+  p.halo = halo;
+  const int64_t npx = static_cast<int64_t>(out_size) * out_size;
+  int64_t bx = (npx + 255) / 256;
+  if (bx > 128) bx = 128;
+  tiles_shard_kernel<<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(n_tiles)), 256, 0,
+                       as_stream(stream)>>>(p);
   return launch_status();
 }

@@ -100,3 +100,100 @@ def sharded_window_counts(origins, size: int, *, cur=None, prev=None, mask=None,
         part = part.cuda()
     dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
     return part.cpu().numpy()
+
+
+def tile_homes(windows, size: int, n_cams: int, width: int, world: int):
+    """Per window (b, x, y): (home rank, straddles).  Home = the rank holding
+    the window's first column; a window straddles when its last column lies
+    on another rank (its output columns are then split by first-tap owner)."""
+    parts = camera_partition(n_cams, world)
+    owner = [0] * n_cams
+    for g, (b0, c) in enumerate(parts):
+        for cam in range(b0, b0 + c):
+            owner[cam] = g
+    out = []
+    for (_, x, _) in windows:
+        h = owner[x // width]
+        out.append((h, owner[(x + size - 1) // width] != h))
+    return out
+
+
+def sharded_tiles(out_local, windows, *, size: int = 960, out_size: int = 416, n_cams: int,
+                  group=None, tiles_fn=None):
+    """Attention tiles over a camera-sharded array.
+
+    out_local: this rank's corrected cameras, (B, c_local, H, W, 3) uint8;
+    windows: (b, x, y) in global mosaic coordinates (the same list on every
+    rank).  Steps: (1) all-gather of every rank's first corrected column
+    (B x H x 3 bytes) - the 1-pixel halo the previous rank's last output
+    columns tap; (2) each rank resamples the output columns whose first tap
+    it holds (camx_tiles_shard) - whole tiles for windows inside its
+    cameras, column slices of straddling ones into a zero-filled buffer;
+    (3) one all-reduce(sum) of the straddling partials (disjoint columns, so
+    the sum is the assembled tile).  Returns (ids, tiles): the indices into
+    `windows` of the tiles homed on this rank (first column here), ascending,
+    and those tiles (len(ids), out_size, out_size, 3) - byte-identical to the
+    1-GPU tiles.  `tiles_fn(local, halo, wins, col_begin, size, out_size,
+    dst)` replaces the kernel call (CPU tests)."""
+    import numpy as np
+    import torch.distributed as dist
+    t = _dev.torch()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    B, c_local, H, W = (int(v) for v in out_local.shape[:4])
+    begin, count = camera_partition(n_cams, world)[rank]
+    if count != c_local:
+        raise ValueError(f"rank {rank} holds {c_local} cameras, partition says {count}")
+    wins = [tuple(int(v) for v in w) for w in windows]
+    for (b, x, y) in wins:
+        if not (0 <= b < B and 0 <= x and 0 <= y and x + size <= n_cams * W and y + size <= H):
+            raise ValueError(f"window ({b}, {x}, {y}, {size}) outside the array")
+    col_begin = begin * W
+    dev = out_local.device
+    nccl = dist.get_backend(group) == "nccl"
+
+    # (1) halo: every rank's first corrected column
+    first = out_local[:, 0, :, 0, :].contiguous()  # (B, H, 3)
+    cols = [t.empty_like(first) for _ in range(world)]
+    dist.all_gather(cols, first, group=group)
+    halo = cols[rank + 1] if rank + 1 < world else None
+
+    if tiles_fn is None:
+        def tiles_fn(local, hal, wl, cb, s, o, dst):
+            from . import _lib
+            wd = t.as_tensor(np.asarray(wl, dtype=np.int32).reshape(-1, 3), device=local.device)
+            _lib.call("camx_tiles_shard", local.data_ptr(), local.shape[1], local.shape[2],
+                      local.shape[3], cb, 0 if hal is None else hal.data_ptr(), wd.data_ptr(),
+                      len(wl), s, o, dst.data_ptr(), _dev.stream_handle(None))
+
+    homes = tile_homes(wins, size, n_cams, W, world)
+    lo, hi = col_begin, col_begin + count * W
+    touches = [x < hi and x + size > lo for (_, x, _) in wins]
+    own = [i for i, (h, s) in enumerate(homes) if h == rank and not s]
+    strad = [i for i, (_, s) in enumerate(homes) if s]
+    tile_shape = (out_size, out_size, 3)
+
+    whole = t.empty((len(own), *tile_shape), dtype=t.uint8, device=dev)
+    if own:
+        tiles_fn(out_local, halo, [wins[i] for i in own], col_begin, size, out_size, whole)
+    part = t.zeros((len(strad), *tile_shape), dtype=t.uint8, device=dev)
+    mine = [k for k, i in enumerate(strad) if touches[i]]
+    if mine:
+        sub = t.zeros((len(mine), *tile_shape), dtype=t.uint8, device=dev)
+        tiles_fn(out_local, halo, [wins[strad[k]] for k in mine], col_begin, size, out_size, sub)
+        part[t.as_tensor(mine, device=dev)] = sub
+    if strad:
+        if not nccl and part.dtype == t.uint8:  # gloo sums int32
+            acc = part.to(t.int32)
+            dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+            part = acc.to(t.uint8)
+        else:
+            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+
+    ids = sorted(own + [i for i in strad if homes[i][0] == rank])
+    pos_own = {i: k for k, i in enumerate(own)}
+    pos_str = {i: k for k, i in enumerate(strad)}
+    res = t.empty((len(ids), *tile_shape), dtype=t.uint8, device=dev)
+    for k, i in enumerate(ids):
+        res[k] = whole[pos_own[i]] if i in pos_own else part[pos_str[i]]
+    return ids, res

@@ -114,3 +114,66 @@ def test_sharded_window_counts_allreduce():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok for _, ok in res), res
+
+
+def _tiles_worker(rank, world, port, n_cams, q):
+    """Camera-sharded tiles: each rank resamples the output columns whose
+    first tap it holds (numpy stand-in for camx_tiles_shard, same ownership
+    rule, halo column from the next rank), straddling partials are summed;
+    every window's tile must equal the whole-array oracle tile exactly, and
+    every window must be homed on exactly one rank."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.camarray_oracle import resize_bilinear, resize_coords
+        from paper_1910_03517_b200.dist import camera_partition, sharded_tiles
+        B, H, W, S, O = 2, 30, 40, 24, 10
+        rng = np.random.default_rng(11)
+        full = rng.integers(0, 256, (B, n_cams, H, W, 3), dtype=np.uint8)
+        mosaic = np.concatenate(list(full.transpose(1, 0, 2, 3, 4)), axis=2)  # (B, H, N*W, 3)
+        wins = [(b, x, y) for b in range(B) for y in (0, 6)
+                for x in list(range(0, n_cams * W - S + 1, 13)) + [W - S // 2, 2 * W - 1]]
+        begin, count = camera_partition(n_cams, world)[rank]
+        local = torch.from_numpy(full[:, begin:begin + count].copy())
+        i0, _, _ = resize_coords(S, O)
+
+        def cpu_tiles(loc, halo, wl, cb, s, o, dst):
+            lm = np.concatenate(list(loc.numpy().transpose(1, 0, 2, 3, 4)), axis=2)
+            if halo is not None:
+                lm = np.concatenate([lm, halo.numpy()[:, :, None, :]], axis=2)
+            glob = np.zeros((B, H, n_cams * W + 1, 3), np.uint8)
+            glob[:, :, cb:cb + lm.shape[2]] = lm
+            for k, (b, x, y) in enumerate(wl):
+                tile = resize_bilinear(glob[b, y:y + s, x:x + s], o)
+                owned = (x + i0 >= cb) & (x + i0 < cb + loc.shape[1] * loc.shape[3])
+                d = dst[k].numpy()
+                d[:, owned] = tile[:, owned]
+
+        ids, tiles = sharded_tiles(local, wins, size=S, out_size=O, n_cams=n_cams,
+                                   tiles_fn=cpu_tiles)
+        ok = all(np.array_equal(tiles[k].numpy(),
+                                resize_bilinear(mosaic[wins[i][0], wins[i][2]:wins[i][2] + S,
+                                                       wins[i][1]:wins[i][1] + S], O))
+                 for k, i in enumerate(ids))
+        q.put((rank, ok, ids, len(wins)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_cams", [(2, 4), (3, 5)])
+def test_sharded_tiles_assemble_exactly(world, n_cams):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tiles_worker, args=(r, world, port, n_cams, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _, _ in res), res
+    homed = sorted(i for _, _, ids, _ in res for i in ids)
+    assert homed == list(range(res[0][3]))  # every window on exactly one rank

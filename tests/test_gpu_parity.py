@@ -701,3 +701,40 @@ def test_window_counts_on_a_camera_shard():
         total += at.window_counts(local, S, cur=cur[b:b + c], prev=prev[b:b + c], n_cams=c)
     want = np.array([full[y:y + S, x:x + S].sum() for (x, y) in origins])
     np.testing.assert_array_equal(total, want)
+
+
+@pytest.mark.parametrize("world,n_cams,size,out", [(2, 4, 96, 40), (3, 5, 96, 96), (4, 8, 150, 64)])
+def test_tiles_on_camera_shards_sum_to_array_tiles(world, n_cams, size, out):
+    """camx_tiles_shard on each rank's cameras (halo = next shard's first
+    column) writes disjoint output columns whose sum is the whole-array
+    camx_tiles result, for windows inside one shard and straddling ones."""
+    from paper_1910_03517_b200 import _lib
+    from paper_1910_03517_b200.dist import camera_partition
+    rng = np.random.default_rng(23 + world)
+    B, H, W = 2, 160, 100
+    full = torch.as_tensor(rng.integers(0, 256, (B, n_cams, H, W, 3), dtype=np.uint8),
+                           device="cuda")
+    wins = [(b, x, y) for b in range(B) for y in (0, H - size)
+            for x in list(range(0, n_cams * W - size + 1, 29)) + [W - 1, 2 * W - size // 2]]
+    wd = torch.as_tensor(np.asarray(wins, np.int32), device="cuda")
+    T = len(wins)
+    want = torch.empty((T, out, out, 3), dtype=torch.uint8, device="cuda")
+    _lib.call("camx_tiles", full.data_ptr(), n_cams, H, W, wd.data_ptr(), T, size, out,
+              want.data_ptr(), None)
+    acc = torch.zeros((T, out, out, 3), dtype=torch.int32, device="cuda")
+    cover = torch.zeros((T, out, out, 3), dtype=torch.int32, device="cuda")
+    for g, (b0, c) in enumerate(camera_partition(n_cams, world)):
+        local = full[:, b0:b0 + c].contiguous()
+        halo = full[:, b0 + c, :, 0, :].contiguous() if g + 1 < world else None
+        # two fills: a pixel is written iff it differs from its fill in either
+        p0 = torch.zeros((T, out, out, 3), dtype=torch.uint8, device="cuda")
+        p1 = torch.full((T, out, out, 3), 7, dtype=torch.uint8, device="cuda")
+        for pb in (p0, p1):
+            _lib.call("camx_tiles_shard", local.data_ptr(), c, H, W, b0 * W,
+                      0 if halo is None else halo.data_ptr(), wd.data_ptr(), T, size, out,
+                      pb.data_ptr(), None)
+        acc += p0.to(torch.int32)
+        cover += ((p0 != 0) | (p1 != 7)).to(torch.int32)
+    torch.cuda.synchronize()
+    assert int(cover.min()) == 1 and int(cover.max()) == 1  # one owner per output pixel
+    np.testing.assert_array_equal(acc.to(torch.uint8).cpu().numpy(), want.cpu().numpy())
