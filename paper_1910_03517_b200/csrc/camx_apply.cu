@@ -307,14 +307,6 @@ struct FuseSmem {  // carved from dynamic shared memory after the ring
   int32_t *counts;         // [0] n_win, [1]/[2] hits, [3]/[4] items of buffer 0 / 1
 };
 
-// Resample one hit (an output row segment [lo, hi) of one tile) from the
-// corrected source rows ra (first tap row) and rb (second tap row) in shared
-// memory; threads t, t + nt, ... of the group, kWsUnroll independent pixels
-// per iteration (all shared loads hoisted for ILP).  Per pixel: the 6 bytes
-// of the two column taps (adjacent pixels) of each row via 3 aligned words
-// + funnel shift, channel pairs by PRMT, horizontal blend by dp2a, vertical
-// by IMAD, round half up (camx_resize.cuh: bilerp_fx).  kWsUnroll > 1 is
-// for the warp-specialised kernel (latency-bound resampler warps).
 // Shared-memory carve of the fusion state after the ring; every region
 // starts 16-byte aligned (int4 records).  fuse_smem_bytes() == the total.
 __host__ __device__ __forceinline__ size_t r16(size_t v) { return (v + 15) & ~static_cast<size_t>(15); }
@@ -357,15 +349,23 @@ __device__ __forceinline__ int out_row_of(const FuseSmem &fs, int lr, int out) {
   return -1;
 }
 
-template <int kWsUnroll>
+// Resample one hit (an output row segment [lo, hi) of one tile) from the
+// corrected source rows ra (first tap row) and rb (second tap row) in shared
+// memory; threads t, t + nt, ... of the group, kUnrollPx independent pixels
+// per iteration (all shared loads hoisted for ILP).  Per pixel: the 6 bytes
+// of the two column taps (adjacent pixels) of each row via 3 aligned words
+// + funnel shift, channel pairs by PRMT, horizontal blend by dp2a, vertical
+// by IMAD, round half up (camx_resize.cuh: bilerp_fx).  kUnrollPx > 1 served
+// the warp-specialised variants (removed: slower on B200, profiles/r01).
+template <int kUnrollPx>
 __device__ __forceinline__ void resample_hit(const uint8_t *ra, const uint8_t *rb, uint32_t wyp,
                                              int xc3, uint8_t *trow, int lo, int hi, int t,
                                              int nt, const FuseSmem &fs) {
   const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
-  for (int ox0 = lo + t; ox0 < hi; ox0 += nt * kWsUnroll) {
-    uint32_t wa[kWsUnroll][3], wb[kWsUnroll][3], wx[kWsUnroll], shv[kWsUnroll];
+  for (int ox0 = lo + t; ox0 < hi; ox0 += nt * kUnrollPx) {
+    uint32_t wa[kUnrollPx][3], wb[kUnrollPx][3], wx[kUnrollPx], shv[kUnrollPx];
 #pragma unroll
-    for (int u = 0; u < kWsUnroll; ++u) {
+    for (int u = 0; u < kUnrollPx; ++u) {
       const int ox = min(ox0 + u * nt, hi - 1);
       wx[u] = fs.wpk[ox];
       const int la = xc3 + 3 * fs.i0[ox];
@@ -379,7 +379,7 @@ __device__ __forceinline__ void resample_hit(const uint8_t *ra, const uint8_t *r
       }
     }
 #pragma unroll
-    for (int u = 0; u < kWsUnroll; ++u) {
+    for (int u = 0; u < kUnrollPx; ++u) {
       const int ox = ox0 + u * nt;
       if (ox >= hi) break;
       const uint32_t alo = __funnelshift_r(wa[u][0], wa[u][1], shv[u]);
@@ -609,238 +609,6 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
   }
 }
 
-// ---------------------------------------------- warp-specialised fusion
-// CTA = 224 threads.  Warps 0-3 (correctors) run exactly the plain K3 loop
-// over the TMA ring and additionally write each corrected stage back into
-// its ring slot, then arrive on corr[slot].  Warps 4-6 (resamplers) trail:
-// they wait corr[slot], build the stage's hit records (warp 4), resample
-// them (named barrier 1 among the resamplers only) and, once stage st
-// is done, refill the slot of stage st-1 (its last row was stage st's
-// "previous row").  No CTA-wide barrier inside the loop: correctors only
-// ever wait for TMA data.
-constexpr int kWsStages = 6;   // raw TMA ring (refilled as soon as corrected)
-constexpr int kWsCStages = 8;  // corrected-row ring read by the resamplers
-constexpr int kWsResamplers = 96;  // 3 warps (4 + 3 warps x 92 regs: 3 CTAs per SM)
-constexpr int kWsThreads = kApplyThreads + kWsResamplers;
-
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void build_hits_ws(const FuseSmem &fs, const TileFuse &q,
-                                              const ApplyParams &p, int st, int r0, int nrows,
-                                              int cam, int cb0) {
-  const int lane = threadIdx.x & 31;
-  const int rr = min(kTmaRows, nrows - st * kTmaRows);
-  const int rs0 = r0 + st * kTmaRows;
-  int4 *hits = fs.hit;
-  int *cnt = &fs.counts[1];
-  if (lane == 0) *cnt = 0;
-  __syncwarp();
-  const int nwin = fs.counts[0];
-  for (int e = lane; e < nwin * rr; e += 32) {
-    const int4 w = fs.win[e / rr];
-    const int R = rs0 + e % rr;
-    const int lr = R - w.z;
-    if (lr < 0 || lr >= q.size) continue;
-    {
-      const int oy = out_row_of(fs, lr, q.out);
-      if (oy < 0) continue;
-      const int Ra = w.z + fs.i0[oy];
-      if (Ra < r0) continue;  // first tap row belongs to the previous CTA
-      const int h = atomicAdd(cnt, 1);
-      auto off = [&](int Rw) {
-        const int sidx = (Rw - r0) / kTmaRows, ri = (Rw - r0) % kTmaRows;
-        return ((sidx % kWsCStages) * kTmaRows + ri) * kApplyThreads * 16;
-      };
-      const uint64_t trow = reinterpret_cast<uint64_t>(
-          q.tiles + (static_cast<int64_t>(w.x) * q.out + oy) * q.out * 3);
-      hits[2 * h] = make_int4(off(Ra), off(R), static_cast<int>(fs.wpk[oy]),
-                              3 * (w.y - cam * p.W) - cb0);
-      hits[2 * h + 1] = make_int4(static_cast<int>(trow & 0xFFFFFFFFu), static_cast<int>(trow >> 32),
-                                  w.w, 0);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kWsThreads, 3)
-    apply_tile_ws_kernel(const ApplyParams p, const TileFuse q) {
-  extern __shared__ __align__(128) uint4 ring[];  // raw [kWsStages][2][128], then corrected
-  __shared__ __align__(8) uint64_t full[kWsStages];   // raw slot filled (TMA)
-  __shared__ __align__(8) uint64_t corr[kWsCStages];  // corrected slot written (4 warps)
-  __shared__ __align__(8) uint64_t cfree[kWsCStages]; // corrected slot released (resamplers)
-  uint4 *cring = ring + kWsStages * kTmaRows * kApplyThreads;
-  int64_t item = blockIdx.x;
-  const int cg = static_cast<int>(item % p.col_groups);
-  item /= p.col_groups;
-  const int rs = static_cast<int>(item % p.row_splits);
-  item /= p.row_splits;
-  const int k = static_cast<int>(item % p.K);
-  const int64_t img = item / p.K;
-
-  const int blk_r0 = k * p.bh;
-  const int blk_r1 = (k == p.K - 1) ? p.H : blk_r0 + p.bh;
-  const int r0 = blk_r0 + rs * p.rows_per_split;
-  const int r1 = min(blk_r1, r0 + p.rows_per_split);
-  if (r0 >= r1) return;  // CTA-uniform
-  const int chunks = min(kApplyThreads, p.chunks_per_row - cg * kApplyThreads);
-  const uint32_t seg = static_cast<uint32_t>(chunks) * 16u;
-  const int64_t rb = p.row_bytes;
-  const uint8_t *src0 = p.src + img * p.img_bytes + static_cast<int64_t>(r0) * rb +
-                        static_cast<int64_t>(cg) * kApplyThreads * 16;
-  const int nrows = r1 - r0;
-  const int nst = (nrows + kTmaRows - 1) / kTmaRows;
-  const bool corrector = threadIdx.x < kApplyThreads;
-
-  auto issue = [&](int st) {
-    const int slot = st % kWsStages;
-    const int rr = min(kTmaRows, nrows - st * kTmaRows);
-    mbar_expect_tx(&full[slot], seg * rr);
-    for (int i = 0; i < rr; ++i)
-      bulk_g2s(ring + (slot * kTmaRows + i) * kApplyThreads,
-               src0 + static_cast<int64_t>(st * kTmaRows + i) * rb, seg, &full[slot]);
-  };
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kWsStages; ++i) mbar_init(&full[i], 1);
-    for (int i = 0; i < kWsCStages; ++i) {
-      mbar_init(&corr[i], kApplyThreads / 32);  // one arrival per corrector warp
-      mbar_init(&cfree[i], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int st = 0; st < min(kWsStages, nst); ++st) issue(st);
-  }
-
-  // tables and the intersecting-window list (geometry only)
-  FuseSmem fs =
-      carve_fuse(reinterpret_cast<uint8_t *>(cring + kWsCStages * kTmaRows * kApplyThreads), q.out,
-                 q.size);
-  const int64_t bfr = img / p.cam_count;
-  const int cam = p.cam_begin + static_cast<int>(img % p.cam_count);
-  const int cb0 = cg * kApplyThreads * 16;
-  const int px_lo = (cb0 + 2) / 3;
-  const int px_hi = (cb0 + static_cast<int>(seg)) / 3;
-  for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
-    int a, b, w1;
-    src_coord_w(i, q.scale, q.size, a, b, w1);
-    fs.i0[i] = static_cast<int16_t>(a);
-    fs.i1[i] = static_cast<int16_t>(b);
-    fs.wpk[i] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
-  }
-  if (threadIdx.x == 0) fs.counts[0] = 0;
-  fs.scale = q.scale;
-  __syncthreads();  // tap tables complete before the window scan reads them
-  {
-    const int w_lo = q.frame_off[bfr], w_hi = q.frame_off[bfr + 1];
-    const int mx0 = cam * p.W + px_lo, mx1 = cam * p.W + px_hi;
-    for (int t = w_lo + threadIdx.x; t < w_hi; t += blockDim.x) {
-      const int x0 = q.wins[3 * t + 1], y0 = q.wins[3 * t + 2];
-      if (x0 < mx1 && x0 + q.size > mx0 && y0 < r1 && y0 + q.size > r0) {
-        const int xc = x0 - cam * p.W;
-        int lo = 0, hi = q.out;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (xc + fs.i0[mid] >= px_lo) hi = mid; else lo = mid + 1;
-        }
-        int lo2 = lo, hi2 = q.out;
-        while (lo2 < hi2) {
-          const int mid = (lo2 + hi2) >> 1;
-          if (xc + fs.i1[mid] >= px_hi) hi2 = mid; else lo2 = mid + 1;
-        }
-        if (lo2 > lo) {
-          const int slot = atomicAdd(&fs.counts[0], 1);
-          fs.win[slot] = make_int4(t, x0, y0, lo | (lo2 << 16));
-        }
-      }
-    }
-  }
-  __syncthreads();
-
-  if (corrector) {
-    // ---------------------------------------------------------- correctors
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int j = cg * kApplyThreads + threadIdx.x;
-    const bool active = threadIdx.x < chunks;
-    const double *gl, *bl, *gr, *br;
-    map_ptrs(p, img, gl, bl, gr, br);
-    Coef16 cf;
-    if (active) {
-      float m[16], a[16];
-      const int q0 = j * 16;
-      int col = q0 / 3;
-      int ch = q0 - col * 3;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        coef_f32(col, ch, k, p.W, gl, bl, gr, br, m[i], a[i]);
-        if (++ch == 3) {
-          ch = 0;
-          ++col;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 16; i += 2) {
-        cf.m[i >> 1] = pack2(m[i] * 0.00390625f, m[i + 1] * 0.00390625f);
-        cf.c[i >> 1] = pack2(m[i] * -32768.0f, m[i + 1] * -32768.0f);
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        cf.a[i] = fabsf(a[i]) < 7.7037197787136e-34f ? 0.0f : a[i] * 0.00390625f;
-    }
-    uint8_t *dst = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
-    for (int st = 0; st < nst; ++st) {
-      const int slot = st % kWsStages;
-      const int cslot = st % kWsCStages;
-      mbar_wait(&full[slot], (st / kWsStages) & 1);
-      const int rr = min(kTmaRows, nrows - st * kTmaRows);
-      uint4 v[kTmaRows];
-      if (active) {
-#pragma unroll
-        for (int i = 0; i < kTmaRows; ++i)
-          if (i < rr) v[i] = ring[(slot * kTmaRows + i) * kApplyThreads + threadIdx.x];
-      }
-      named_bar(2, kApplyThreads);  // raw slot consumed by every corrector: refill now
-      if (threadIdx.x == 0 && st + kWsStages < nst) issue(st + kWsStages);
-      if (st >= kWsCStages) mbar_wait(&cfree[cslot], ((st / kWsCStages) - 1) & 1);
-      if (active) {
-#pragma unroll
-        for (int i = 0; i < kTmaRows; ++i)
-          if (i < rr) {
-            const uint4 o = correct16(v[i], cf);
-            st_stream_v4(dst + static_cast<int64_t>(st * kTmaRows + i) * rb, o);
-            cring[(cslot * kTmaRows + i) * kApplyThreads + threadIdx.x] = o;
-          }
-      }
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&corr[cslot]);
-    }
-  } else {
-    // ---------------------------------------------------------- resamplers
-    const int rt = threadIdx.x - kApplyThreads;  // 0..kWsResamplers-1
-    const uint8_t *ringb = reinterpret_cast<const uint8_t *>(cring);
-    for (int st = 0; st < nst; ++st) {
-      const int cslot = st % kWsCStages;
-      mbar_wait(&corr[cslot], (st / kWsCStages) & 1);
-      if (rt < 32) build_hits_ws(fs, q, p, st, r0, nrows, cam, cb0);
-      named_bar(1, kWsResamplers);
-      const int nhit = fs.counts[1];
-      for (int hh = 0; hh < nhit; ++hh) {
-        const int4 h0 = fs.hit[2 * hh], h1 = fs.hit[2 * hh + 1];
-        resample_hit<4>(ringb + h0.x, ringb + h0.y, static_cast<uint32_t>(h0.z), h0.w,
-                        reinterpret_cast<uint8_t *>(
-                            (static_cast<uint64_t>(static_cast<uint32_t>(h1.y)) << 32) |
-                            static_cast<uint32_t>(h1.x)),
-                        h1.z & 0xFFFF, h1.z >> 16, rt, kWsResamplers, fs);
-      }
-      named_bar(1, kWsResamplers);  // stage st resampled: hits reusable
-      // the corrected rows of stage st-1 (previous-row taps) are no longer needed
-      if (rt == 0 && st >= 1) mbar_arrive(&cfree[(st - 1) % kWsCStages]);
-    }
-  }
-}
-
 // Tile outputs the fused kernel could not produce (taps straddling CTA rows
 // or column groups), resampled from the corrected frame.  One CTA per tile.
 __device__ __forceinline__ int row_cta(const ApplyParams &p, int r) {
@@ -1006,35 +774,7 @@ static int launch_apply_tiles(ApplyParams &p, TileFuse &q, int32_t n_tiles,
   if (!plan_fast(p)) return CAMX_EINVAL;
   // strict downscale: no clamped taps, each source row is the second tap of <= 1 output row
   if (max_tiles_per_frame > kFuseMaxWin || q.out >= q.size || q.size > 4096) return CAMX_EINVAL;
-  if (fuse_smem_bytes(q) + (kWsStages + kWsCStages) * kTmaRows * kApplyThreads * 16 > 200 * 1024)
-    return CAMX_EINVAL;
-  static const bool use_ws = [] {
-    const char *e = getenv("CAMX_TILE_WS");
-    return e != nullptr && e[0] == '1';
-  }();
-  int st;
-  if (!use_ws) {
-    st = launch_tma<true, kFuseRows, kFuseStages>(p, q, stream);
-  } else {
-    const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
-    const size_t smem = (kWsStages + kWsCStages) * kTmaRows * kApplyThreads * 16 + fuse_smem_bytes(q);
-    cudaError_t e = cudaFuncSetAttribute(apply_tile_ws_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return static_cast<int>(e);
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(static_cast<unsigned>(grid));
-    lc.blockDim = dim3(kWsThreads);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    lc.attrs = at;
-    lc.numAttrs = p.pdl ? 1 : 0;
-    e = cudaLaunchKernelEx(&lc, apply_tile_ws_kernel, p, q);
-    st = e == cudaSuccess ? launch_status() : static_cast<int>(e);
-  }
+  int st = launch_tma<true, kFuseRows, kFuseStages>(p, q, stream);
   if (st != CAMX_OK || n_tiles == 0) return st;
   const size_t smem = 2 * sizeof(int32_t) * q.out;
   if (smem > 48 * 1024) {
