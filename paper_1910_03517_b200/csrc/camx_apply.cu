@@ -156,6 +156,52 @@ __device__ __forceinline__ uint32_t correct_word(uint32_t w, const Coef16 &cf, i
   return __byte_perm(p01, p23, 0x6420u);
 }
 
+// Same arithmetic with 16 fewer live registers (for the fused tile kernel,
+// which is occupancy-bound): X - 2^23 = p exactly, then p * (M/256) =
+// rn(p*M)/256 (power-of-two scale) - one more instruction per sub-pixel pair.
+__device__ __forceinline__ uint32_t correct_word_lean(uint32_t w, const Coef16 &cf, int base) {
+  const uint64_t kScale = pack2(256.0f, 256.0f);
+  const uint64_t kMagic = pack2(8388608.0f, 8388608.0f);
+  const uint64_t kUnmagic = pack2(-8388608.0f, -8388608.0f);
+  uint32_t z[4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = base + 2 * h;
+    const uint32_t x0 = __byte_perm(w, 0x4B00u, 0x5440u + 2 * h);
+    const uint32_t x1 = __byte_perm(w, 0x4B00u, 0x5441u + 2 * h);
+    const uint64_t y1 = mul2_rn(add2_rn(pack2u(x0, x1), kUnmagic), cf.m[i >> 1]);
+    uint32_t lo, hi;
+    unpack2u(y1, lo, hi);
+    const float s0 = add_sat_rn(__uint_as_float(lo), cf.a[i]);
+    const float s1 = add_sat_rn(__uint_as_float(hi), cf.a[i + 1]);
+    const uint64_t q = fma2_rn(pack2(s0, s1), kScale, kMagic);
+    unpack2u(q, z[2 * h], z[2 * h + 1]);
+  }
+  uint32_t p01 = __byte_perm(z[0], z[1], 0x5410u);
+  uint32_t p23 = __byte_perm(z[2], z[3], 0x5410u);
+  p01 = __vminu2(p01, 0x00FF00FFu);
+  p23 = __vminu2(p23, 0x00FF00FFu);
+  return __byte_perm(p01, p23, 0x6420u);
+}
+
+template <bool LEAN>
+__device__ __forceinline__ uint4 correct16_t(uint4 v, const Coef16 &cf) {
+  if (!LEAN) {
+    uint4 r;
+    r.x = correct_word(v.x, cf, 0);
+    r.y = correct_word(v.y, cf, 4);
+    r.z = correct_word(v.z, cf, 8);
+    r.w = correct_word(v.w, cf, 12);
+    return r;
+  }
+  uint4 r;
+  r.x = correct_word_lean(v.x, cf, 0);
+  r.y = correct_word_lean(v.y, cf, 4);
+  r.z = correct_word_lean(v.z, cf, 8);
+  r.w = correct_word_lean(v.w, cf, 12);
+  return r;
+}
+
 __device__ __forceinline__ uint4 correct16(uint4 v, const Coef16 &cf) {
   uint4 r;
   r.x = correct_word(v.x, cf, 0);
@@ -289,64 +335,46 @@ struct TileFuse {
   float scale;
 };
 constexpr int kFuseMaxWin = 48;  // windows per array-frame the fused path accepts
-// downscale/crop only (out <= size): a source row is the second tap of at
-// most one output row per window, so a 2-row stage has <= 2 hits per window
-constexpr int kFuseMaxHits = 2 * kFuseMaxWin;
+// strict downscale only (out < size): i0 is strictly increasing and i1 =
+// i0 + 1, so a source row is the second tap of at most one output row per
+// window (orow[] is well defined)
 // ring of the fused (shared-barrier) kernel: 4-row stages halve the barriers
 // and hit builds per byte; refill lags two stages (previous row resident)
 constexpr int kFuseRows = 4;
 constexpr int kFuseStages = 4;
-static_assert(kFuseRows * kFuseMaxWin <= 2 * kFuseMaxHits, "hit buffer capacity");
+static_assert(kFuseRows == 4, "hit enumeration uses e >> 2 / e & 3");
 
 struct FuseSmem {  // carved from dynamic shared memory after the ring
-  int16_t *i0, *i1;
-  uint32_t *wpk;           // (256 - w1) | w1 << 16: dp2a operand
-  float scale;             // S / out (candidate output row of a source row)
+  uint32_t *tap;           // [out] i0 | w1 << 16 (i1 = i0 + 1: strict downscale)
+  int16_t *orow;           // [size] output row whose second tap is window row lr, or -1
   int4 *win;               // intersecting windows: (tile, x0, y0, lo | hi << 16)
-  int4 *hit;               // 2 buffers x kFuseMaxHits x 2 int4 (see build_hits)
-  int32_t *counts;         // [0] n_win, [1]/[2] hits, [3]/[4] items of buffer 0 / 1
+  int32_t *counts;         // [0] n_win
 };
+
+// dp2a operand of a tap entry: (256 - w1) | w1 << 16 = w1 * 65535 + 256.
+__device__ __forceinline__ uint32_t tap_wpk(uint32_t tv) { return (tv >> 16) * 65535u + 256u; }
+__device__ __forceinline__ int tap_i0(uint32_t tv) { return static_cast<int>(tv & 0xFFFFu); }
 
 // Shared-memory carve of the fusion state after the ring; every region
 // starts 16-byte aligned (int4 records).  fuse_smem_bytes() == the total.
 __host__ __device__ __forceinline__ size_t r16(size_t v) { return (v + 15) & ~static_cast<size_t>(15); }
 __host__ __device__ __forceinline__ size_t fuse_layout(int out, int size, size_t *off) {
   size_t o = 0;
-  off[0] = o; o += r16(2 * static_cast<size_t>(out));   // i0
-  off[1] = o; o += r16(2 * static_cast<size_t>(out));   // i1
-  off[2] = o; o += r16(4 * static_cast<size_t>(out));   // wpk
-  off[3] = o;                                           // (unused)
-  off[4] = o;                                           // (unused)
-  off[5] = o; o += sizeof(int4) * kFuseMaxWin;           // win
-  off[6] = o; o += sizeof(int4) * 2 * kFuseMaxHits * 2;  // hit (2 buffers)
-  off[7] = o; o += 32;                                   // counts
+  off[0] = o; o += r16(4 * static_cast<size_t>(out));   // tap
+  off[1] = o; o += r16(2 * static_cast<size_t>(size));  // orow
+  off[2] = o; o += sizeof(int4) * kFuseMaxWin;           // win
+  off[3] = o; o += 16;                                   // counts
   return o;
 }
 __device__ __forceinline__ FuseSmem carve_fuse(uint8_t *base, int out, int size) {
-  size_t off[8];
+  size_t off[4];
   fuse_layout(out, size, off);
   FuseSmem fs;
-  fs.i0 = reinterpret_cast<int16_t *>(base + off[0]);
-  fs.i1 = reinterpret_cast<int16_t *>(base + off[1]);
-  fs.wpk = reinterpret_cast<uint32_t *>(base + off[2]);
-  fs.scale = 0.0f;
-  fs.win = reinterpret_cast<int4 *>(base + off[5]);
-  fs.hit = reinterpret_cast<int4 *>(base + off[6]);
-  fs.counts = reinterpret_cast<int32_t *>(base + off[7]);
+  fs.tap = reinterpret_cast<uint32_t *>(base + off[0]);
+  fs.orow = reinterpret_cast<int16_t *>(base + off[1]);
+  fs.win = reinterpret_cast<int4 *>(base + off[2]);
+  fs.counts = reinterpret_cast<int32_t *>(base + off[3]);
   return fs;
-}
-
-// The output row whose second tap row is window-local source row lr, or -1
-// (strict downscale: at most one).  Candidate from the inverse map, verified
-// against the exact tap table.
-__device__ __forceinline__ int out_row_of(const FuseSmem &fs, int lr, int out) {
-  const int c = static_cast<int>(floorf((static_cast<float>(lr) - 0.5f) / fs.scale - 0.5f));
-#pragma unroll
-  for (int d = -1; d <= 2; ++d) {
-    const int oy = c + d;
-    if (oy >= 0 && oy < out && fs.i1[oy] == lr) return oy;
-  }
-  return -1;
 }
 
 // Resample one hit (an output row segment [lo, hi) of one tile) from the
@@ -367,8 +395,9 @@ __device__ __forceinline__ void resample_hit(const uint8_t *ra, const uint8_t *r
 #pragma unroll
     for (int u = 0; u < kUnrollPx; ++u) {
       const int ox = min(ox0 + u * nt, hi - 1);
-      wx[u] = fs.wpk[ox];
-      const int la = xc3 + 3 * fs.i0[ox];
+      const uint32_t tv = fs.tap[ox];
+      wx[u] = tap_wpk(tv);
+      const int la = xc3 + 3 * tap_i0(tv);
       shv[u] = (la & 3) * 8;
       const uint32_t *pa = reinterpret_cast<const uint32_t *>(ra + (la & ~3));
       const uint32_t *pb = reinterpret_cast<const uint32_t *>(rb + (la & ~3));
@@ -403,46 +432,8 @@ __device__ __forceinline__ void resample_hit(const uint8_t *ra, const uint8_t *r
 // CTA: smem offsets of both (corrected) source rows, packed vertical
 // weights, window origin in segment bytes, the tile row pointer and the
 // output column range [lo, hi) whose taps are whole pixels of this CTA.
-template <int ROWS, int STAGES>
-__device__ __forceinline__ void build_hits(const FuseSmem &fs, const TileFuse &q,
-                                           const ApplyParams &p, int st, int r0, int nrows,
-                                           int cam, int cb0) {
-  const int lane = threadIdx.x & 31;
-  const int rr = min(ROWS, nrows - st * ROWS);
-  const int rs0 = r0 + st * ROWS;
-  int4 *hits = fs.hit;  // capacity ROWS * kFuseMaxWin hits (downscale: <= 1 per row per window)
-  int *cnt = &fs.counts[1];
-  if (lane == 0) *cnt = 0;
-  __syncwarp();
-  const int nwin = fs.counts[0];
-  for (int e = lane; e < nwin * rr; e += 32) {
-    const int4 w = fs.win[e / rr];
-    const int R = rs0 + e % rr;
-    const int lr = R - w.z;
-    if (lr < 0 || lr >= q.size) continue;
-    {
-      const int oy = out_row_of(fs, lr, q.out);
-      if (oy < 0) continue;
-      const int Ra = w.z + fs.i0[oy];
-      if (Ra < r0) continue;  // first tap row belongs to the previous CTA
-      const int h = atomicAdd(cnt, 1);
-      auto off = [&](int Rw) {
-        const int sidx = (Rw - r0) / ROWS, ri = (Rw - r0) % ROWS;
-        return ((sidx % STAGES) * ROWS + ri) * kApplyThreads * 16;
-      };
-      const uint64_t trow = reinterpret_cast<uint64_t>(
-          q.tiles + (static_cast<int64_t>(w.x) * q.out + oy) * q.out * 3);
-      hits[2 * h] = make_int4(off(Ra), off(R), static_cast<int>(fs.wpk[oy]),
-                              3 * (w.y - cam * p.W) - cb0);
-      hits[2 * h + 1] = make_int4(static_cast<int>(trow & 0xFFFFFFFFu), static_cast<int>(trow >> 32),
-                                  w.w, 0);
-    }
-  }
-  __syncwarp();
-}
-
 template <bool TILES, int ROWS, int STAGES>
-__global__ void __launch_bounds__(kApplyThreads, 4)
+__global__ void __launch_bounds__(kApplyThreads, TILES ? 5 : 4)
     apply_tma_kernel(const ApplyParams p, const TileFuse q) {
   extern __shared__ __align__(128) uint4 ring[];  // [STAGES][ROWS][kApplyThreads]
   __shared__ __align__(8) uint64_t full[STAGES];
@@ -498,14 +489,13 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
     for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
       int a, b, w1;
       src_coord_w(i, q.scale, q.size, a, b, w1);
-      fs.i0[i] = static_cast<int16_t>(a);
-      fs.i1[i] = static_cast<int16_t>(b);
-      fs.wpk[i] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
+      fs.tap[i] = static_cast<uint32_t>(a) | (static_cast<uint32_t>(w1) << 16);
+      (void)b;  // = a + 1 (strict downscale)
     }
+    for (int i = threadIdx.x; i < q.size; i += blockDim.x) fs.orow[i] = -1;
     if (threadIdx.x == 0) fs.counts[0] = 0;
-    fs.scale = q.scale;
     __syncthreads();  // tap tables complete before the window scan reads them
-    __syncthreads();
+    for (int i = threadIdx.x; i < q.out; i += blockDim.x) fs.orow[tap_i0(fs.tap[i]) + 1] = static_cast<int16_t>(i);
     // windows of this array-frame that overlap the CTA region (mosaic coords),
     // with the contiguous range [lo, hi) of output columns whose two column
     // taps are whole pixels of this CTA (i0, i1 are nondecreasing in ox)
@@ -518,12 +508,12 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
         int lo = 0, hi = q.out;  // first ox with xc + i0 >= px_lo
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if (xc + fs.i0[mid] >= px_lo) hi = mid; else lo = mid + 1;
+          if (xc + tap_i0(fs.tap[mid]) >= px_lo) hi = mid; else lo = mid + 1;
         }
         int lo2 = lo, hi2 = q.out;  // first ox with xc + i1 >= px_hi
         while (lo2 < hi2) {
           const int mid = (lo2 + hi2) >> 1;
-          if (xc + fs.i1[mid] >= px_hi) hi2 = mid; else lo2 = mid + 1;
+          if (xc + tap_i0(fs.tap[mid]) + 1 >= px_hi) hi2 = mid; else lo2 = mid + 1;
         }
         if (lo2 > lo) {
           const int slot = atomicAdd(&fs.counts[0], 1);
@@ -533,6 +523,8 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
     }
   }
   __syncthreads();
+  const int nwin = TILES ? fs.counts[0] : 0;
+  const int xbase = 3 * cam * p.W + cb0;  // window column -> CTA byte offset
   // maps come from the preceding stats/solve grid (programmatic dependent
   // launch): only the raw-pixel prefetch above may run before it completes
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -559,7 +551,7 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
 #pragma unroll
     for (int i = 0; i < 16; i += 2) {
       cf.m[i >> 1] = pack2(m[i] * 0.00390625f, m[i + 1] * 0.00390625f);
-      cf.c[i >> 1] = pack2(m[i] * -32768.0f, m[i + 1] * -32768.0f);
+      if (!TILES) cf.c[i >> 1] = pack2(m[i] * -32768.0f, m[i + 1] * -32768.0f);
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i)
@@ -579,7 +571,7 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
 #pragma unroll
       for (int i = 0; i < ROWS; ++i)
         if (i < rr) {
-          const uint4 o = correct16(v[i], cf);
+          const uint4 o = correct16_t<TILES>(v[i], cf);
           st_stream_v4(dst + static_cast<int64_t>(st * ROWS + i) * rb, o);
           if (TILES) ring[(slot * ROWS + i) * kApplyThreads + threadIdx.x] = o;
         }
@@ -589,19 +581,57 @@ __global__ void __launch_bounds__(kApplyThreads, 4)
       // every thread has finished the previous stage's resample (it came
       // before this barrier): the slot of stage st-2 is free
       if (threadIdx.x == 0 && st >= 2 && st - 2 + STAGES < nst) issue(st - 2 + STAGES);
-      // warp 0 builds this stage's hit records, then everyone resamples
-      if (threadIdx.x < 32) build_hits<ROWS, STAGES>(fs, q, p, st, r0, nrows, cam, cb0);
-      __syncthreads();
-      const int4 *hits = fs.hit;
-      const int nhit = fs.counts[1];
+      // Hits of this stage (one output-row segment of one tile each): every
+      // warp enumerates the same (window, row) pairs in the same order in
+      // registers, so the 128 threads split each hit's columns consistently
+      // with no shared hit list and no second barrier.
       const uint8_t *ringb = reinterpret_cast<const uint8_t *>(ring);
-      for (int hh = 0; hh < nhit; ++hh) {
-        const int4 h0 = hits[2 * hh], h1 = hits[2 * hh + 1];
-        resample_hit<1>(ringb + h0.x, ringb + h0.y, static_cast<uint32_t>(h0.z), h0.w,
-                        reinterpret_cast<uint8_t *>(
-                            (static_cast<uint64_t>(static_cast<uint32_t>(h1.y)) << 32) |
-                            static_cast<uint32_t>(h1.x)),
-                        h1.z & 0xFFFF, h1.z >> 16, threadIdx.x, kApplyThreads, fs);
+      const int lane = threadIdx.x & 31;
+      const int rs0 = st * ROWS;  // CTA-relative first row of the stage
+      for (int e0 = 0; e0 < 4 * nwin; e0 += 32) {
+        const int e = e0 + lane;
+        const int ri = e & 3;
+        bool ok = false;
+        uint32_t offs = 0, wpk = 0;
+        int xc3 = 0, lohi = 0;
+        uint64_t trow = 0;
+        if (e < 4 * nwin && ri < rr) {
+          const int4 w = fs.win[e >> 2];
+          const int R = r0 + rs0 + ri;
+          const int lr = R - w.z;
+          const int oy = (lr >= 0 && lr < q.size) ? fs.orow[lr] : -1;
+          if (oy >= 0) {
+            const uint32_t tv = fs.tap[oy];
+            const int ra = w.z + tap_i0(tv) - r0;  // first tap row, CTA-relative
+            if (ra >= 0) {  // else it belongs to the previous CTA (fix-up kernel)
+              ok = true;
+              const int rb = rs0 + ri;
+              offs = static_cast<uint32_t>(((ra / ROWS) % STAGES * ROWS + ra % ROWS) *
+                                           kApplyThreads * 16) |
+                     (static_cast<uint32_t>(((rb / ROWS) % STAGES * ROWS + ri) * kApplyThreads * 16)
+                      << 16);
+              wpk = tap_wpk(tv);
+              xc3 = 3 * w.y - xbase;
+              lohi = w.w;
+              trow = reinterpret_cast<uint64_t>(
+                  q.tiles + (static_cast<int64_t>(w.x) * q.out + oy) * q.out * 3);
+            }
+          }
+        }
+        unsigned bal = __ballot_sync(0xffffffffu, ok);
+        while (bal) {
+          const int src = __ffs(bal) - 1;
+          bal &= bal - 1u;
+          const uint32_t o = __shfl_sync(0xffffffffu, offs, src);
+          const uint32_t wp = __shfl_sync(0xffffffffu, wpk, src);
+          const int x3 = __shfl_sync(0xffffffffu, xc3, src);
+          const int lh = __shfl_sync(0xffffffffu, lohi, src);
+          const uint32_t tl = __shfl_sync(0xffffffffu, static_cast<uint32_t>(trow), src);
+          const uint32_t th = __shfl_sync(0xffffffffu, static_cast<uint32_t>(trow >> 32), src);
+          resample_hit<1>(ringb + (o & 0xFFFFu), ringb + (o >> 16), wp, x3,
+                          reinterpret_cast<uint8_t *>((static_cast<uint64_t>(th) << 32) | tl),
+                          lh & 0xFFFF, lh >> 16, threadIdx.x, kApplyThreads, fs);
+        }
       }
     } else {
       if (threadIdx.x == 0 && st + STAGES < nst) issue(st + STAGES);
