@@ -345,22 +345,21 @@ constexpr int kFuseStages = 4;
 static_assert(kFuseRows == 4, "hit enumeration uses e >> 2 / e & 3");
 
 struct FuseSmem {  // carved from dynamic shared memory after the ring
-  uint32_t *tap;           // [out] i0 | w1 << 16 (i1 = i0 + 1: strict downscale)
+  uint2 *tap;              // [out] (3 * i0, dp2a weights (256 - w1) | w1 << 16);
+                           // i1 = i0 + 1 (strict downscale)
   int16_t *orow;           // [size] output row whose second tap is window row lr, or -1
   int4 *win;               // intersecting windows: (tile, x0, y0, lo | hi << 16)
   int32_t *counts;         // [0] n_win
 };
 
-// dp2a operand of a tap entry: (256 - w1) | w1 << 16 = w1 * 65535 + 256.
-__device__ __forceinline__ uint32_t tap_wpk(uint32_t tv) { return (tv >> 16) * 65535u + 256u; }
-__device__ __forceinline__ int tap_i0(uint32_t tv) { return static_cast<int>(tv & 0xFFFFu); }
+__device__ __forceinline__ int tap_i0(uint2 tv) { return static_cast<int>(tv.x) / 3; }
 
 // Shared-memory carve of the fusion state after the ring; every region
 // starts 16-byte aligned (int4 records).  fuse_smem_bytes() == the total.
 __host__ __device__ __forceinline__ size_t r16(size_t v) { return (v + 15) & ~static_cast<size_t>(15); }
 __host__ __device__ __forceinline__ size_t fuse_layout(int out, int size, size_t *off) {
   size_t o = 0;
-  off[0] = o; o += r16(4 * static_cast<size_t>(out));   // tap
+  off[0] = o; o += r16(8 * static_cast<size_t>(out));   // tap
   off[1] = o; o += r16(2 * static_cast<size_t>(size));  // orow
   off[2] = o; o += sizeof(int4) * kFuseMaxWin;           // win
   off[3] = o; o += 16;                                   // counts
@@ -370,7 +369,7 @@ __device__ __forceinline__ FuseSmem carve_fuse(uint8_t *base, int out, int size)
   size_t off[4];
   fuse_layout(out, size, off);
   FuseSmem fs;
-  fs.tap = reinterpret_cast<uint32_t *>(base + off[0]);
+  fs.tap = reinterpret_cast<uint2 *>(base + off[0]);
   fs.orow = reinterpret_cast<int16_t *>(base + off[1]);
   fs.win = reinterpret_cast<int4 *>(base + off[2]);
   fs.counts = reinterpret_cast<int32_t *>(base + off[3]);
@@ -379,59 +378,39 @@ __device__ __forceinline__ FuseSmem carve_fuse(uint8_t *base, int out, int size)
 
 // Resample one hit (an output row segment [lo, hi) of one tile) from the
 // corrected source rows ra (first tap row) and rb (second tap row) in shared
-// memory; threads t, t + nt, ... of the group, kUnrollPx independent pixels
-// per iteration (all shared loads hoisted for ILP).  Per pixel: the 6 bytes
+// memory; threads t, t + nt, ... of the group.  Per pixel: the 6 bytes
 // of the two column taps (adjacent pixels) of each row via 3 aligned words
 // + funnel shift, channel pairs by PRMT, horizontal blend by dp2a, vertical
-// by IMAD, round half up (camx_resize.cuh: bilerp_fx).  kUnrollPx > 1 served
-// the warp-specialised variants (removed: slower on B200, profiles/r01).
-template <int kUnrollPx>
-__device__ __forceinline__ void resample_hit(const uint8_t *ra, const uint8_t *rb, uint32_t wyp,
-                                             int xc3, uint8_t *trow, int lo, int hi, int t,
-                                             int nt, const FuseSmem &fs) {
+// by IMAD, round half up (camx_resize.cuh: bilerp_fx).
+__device__ __forceinline__ void resample_hit(const uint8_t *ringb, uint32_t offa, uint32_t offb,
+                                             uint32_t wyp, int xc3, uint8_t *trow, int lo, int hi,
+                                             int t, int nt, const FuseSmem &fs) {
   const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
-  for (int ox0 = lo + t; ox0 < hi; ox0 += nt * kUnrollPx) {
-    uint32_t wa[kUnrollPx][3], wb[kUnrollPx][3], wx[kUnrollPx], shv[kUnrollPx];
+  // byte offsets into the ring (128-byte aligned), so (offset & 3) is the
+  // word shift and the loads stay in shared memory
+  const uint32_t a0off = offa + static_cast<uint32_t>(xc3);
+  const uint32_t db = offb - offa;
+  uint8_t *o = trow + 3 * (lo + t);
+  for (int ox = lo + t; ox < hi; ox += nt, o += 3 * nt) {
+    const uint2 tv = fs.tap[ox];
+    const uint32_t la = a0off + tv.x;
+    const uint32_t sh = la * 8u;  // funnel shifts use the low 5 bits
+    const uint32_t *wa = reinterpret_cast<const uint32_t *>(ringb + (la & ~3u));
+    const uint32_t *wb = reinterpret_cast<const uint32_t *>(ringb + (la & ~3u) + db);
+    const uint32_t a0 = wa[0], a1 = wa[1], a2 = wa[2];
+    const uint32_t b0 = wb[0], b1 = wb[1], b2 = wb[2];
+    const uint32_t alo = __funnelshift_r(a0, a1, sh), ahi = __funnelshift_r(a1, a2, sh);
+    const uint32_t blo = __funnelshift_r(b0, b1, sh), bhi = __funnelshift_r(b1, b2, sh);
 #pragma unroll
-    for (int u = 0; u < kUnrollPx; ++u) {
-      const int ox = min(ox0 + u * nt, hi - 1);
-      const uint32_t tv = fs.tap[ox];
-      wx[u] = tap_wpk(tv);
-      const int la = xc3 + 3 * tap_i0(tv);
-      shv[u] = (la & 3) * 8;
-      const uint32_t *pa = reinterpret_cast<const uint32_t *>(ra + (la & ~3));
-      const uint32_t *pb = reinterpret_cast<const uint32_t *>(rb + (la & ~3));
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        wa[u][i] = pa[i];
-        wb[u][i] = pb[i];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnrollPx; ++u) {
-      const int ox = ox0 + u * nt;
-      if (ox >= hi) break;
-      const uint32_t alo = __funnelshift_r(wa[u][0], wa[u][1], shv[u]);
-      const uint32_t ahi = __funnelshift_r(wa[u][1], wa[u][2], shv[u]);
-      const uint32_t blo = __funnelshift_r(wb[u][0], wb[u][1], shv[u]);
-      const uint32_t bhi = __funnelshift_r(wb[u][1], wb[u][2], shv[u]);
-      uint8_t *o = trow + 3 * ox;
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
-        const uint32_t v0 = __dp2a_lo(wx[u], __byte_perm(alo, ahi, sel), 0u);
-        const uint32_t v1 = __dp2a_lo(wx[u], __byte_perm(blo, bhi, sel), 0u);
-        o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
-      }
+    for (int ch = 0; ch < 3; ++ch) {
+      const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
+      const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
+      const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
+      o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
     }
   }
 }
 
-// Warp 0: records of the output rows whose second source row lies in stage
-// `st` (rows r0 + 2st, r0 + 2st + 1) and whose first source row is in this
-// CTA: smem offsets of both (corrected) source rows, packed vertical
-// weights, window origin in segment bytes, the tile row pointer and the
-// output column range [lo, hi) whose taps are whole pixels of this CTA.
 template <bool TILES, int ROWS, int STAGES>
 __global__ void __launch_bounds__(kApplyThreads, TILES ? 5 : 4)
     apply_tma_kernel(const ApplyParams p, const TileFuse q) {
@@ -489,7 +468,8 @@ __global__ void __launch_bounds__(kApplyThreads, TILES ? 5 : 4)
     for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
       int a, b, w1;
       src_coord_w(i, q.scale, q.size, a, b, w1);
-      fs.tap[i] = static_cast<uint32_t>(a) | (static_cast<uint32_t>(w1) << 16);
+      fs.tap[i] = make_uint2(3u * static_cast<uint32_t>(a),
+                             static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16));
       (void)b;  // = a + 1 (strict downscale)
     }
     for (int i = threadIdx.x; i < q.size; i += blockDim.x) fs.orow[i] = -1;
@@ -601,7 +581,7 @@ __global__ void __launch_bounds__(kApplyThreads, TILES ? 5 : 4)
           const int lr = R - w.z;
           const int oy = (lr >= 0 && lr < q.size) ? fs.orow[lr] : -1;
           if (oy >= 0) {
-            const uint32_t tv = fs.tap[oy];
+            const uint2 tv = fs.tap[oy];
             const int ra = w.z + tap_i0(tv) - r0;  // first tap row, CTA-relative
             if (ra >= 0) {  // else it belongs to the previous CTA (fix-up kernel)
               ok = true;
@@ -610,7 +590,7 @@ __global__ void __launch_bounds__(kApplyThreads, TILES ? 5 : 4)
                                            kApplyThreads * 16) |
                      (static_cast<uint32_t>(((rb / ROWS) % STAGES * ROWS + ri) * kApplyThreads * 16)
                       << 16);
-              wpk = tap_wpk(tv);
+              wpk = tv.y;
               xc3 = 3 * w.y - xbase;
               lohi = w.w;
               trow = reinterpret_cast<uint64_t>(
@@ -628,7 +608,7 @@ __global__ void __launch_bounds__(kApplyThreads, TILES ? 5 : 4)
           const int lh = __shfl_sync(0xffffffffu, lohi, src);
           const uint32_t tl = __shfl_sync(0xffffffffu, static_cast<uint32_t>(trow), src);
           const uint32_t th = __shfl_sync(0xffffffffu, static_cast<uint32_t>(trow >> 32), src);
-          resample_hit<1>(ringb + (o & 0xFFFFu), ringb + (o >> 16), wp, x3,
+          resample_hit(ringb, o & 0xFFFFu, o >> 16, wp, x3,
                           reinterpret_cast<uint8_t *>((static_cast<uint64_t>(th) << 32) | tl),
                           lh & 0xFFFF, lh >> 16, threadIdx.x, kApplyThreads, fs);
         }
