@@ -63,7 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         obj = BUILD / (src.stem + ".o")
         objs.append(obj)
         if force or _stale(obj, [src, *hdrs]):
-            cmd = [cc, *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-I", str(CSRC), "-c", str(src),
+            extra = os.environ.get("CAMX_NVCC_EXTRA", "").split()  # experiments only
+            cmd = [cc, *ARCH, *NVCC_FLAGS, *extra, "-I", str(INCLUDE), "-I", str(CSRC), "-c", str(src),
                    "-o", str(obj)]
             jobs.append((src, cmd))
 
