@@ -152,6 +152,49 @@ def cpu_reference_sample(frames_np, n_frames: int, threads: int):
     return times
 
 
+def cpu_cached_apply_sample(frames_np, n_frames: int, threads: int, gain, offset,
+                            wrap: bool = False):
+    """Steady state of the reference (maps unchanged: the _apply_arrays cache
+    hits, exposure.py:363-381): apply_exposure per camera side with the f32
+    tables built once; seconds per array-frame."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import camarray_oracle as O
+    n, H, W = frames_np.shape[1:4]
+    S = n if wrap else n - 1
+    tabs = {(s, side): O.apply_tables(gain[s, side], offset[s, side], H, W,
+                                      O.LEFT if side == 0 else O.RIGHT)
+            for s in range(S) for side in (0, 1)}
+
+    def one(args):
+        res, c = args
+        if c < S:
+            O.apply_exposure_inplace(res[c], gain[c, 0], offset[c, 0], O.LEFT, tables=tabs[(c, 0)])
+        sr = c - 1 if c >= 1 else (S - 1 if wrap else -1)
+        if sr >= 0:
+            O.apply_exposure_inplace(res[c], gain[sr, 1], offset[sr, 1], O.RIGHT,
+                                     tables=tabs[(sr, 1)])
+
+    times = []
+    with ThreadPoolExecutor(threads) as ex:
+        for i in range(n_frames):
+            t0 = time.perf_counter()
+            res = frames_np[i % frames_np.shape[0]].copy()  # apply_exposure copies its input
+            list(ex.map(one, [(res, c) for c in range(n)]))
+            times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
     """--impl reference: the reference CPU path, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
@@ -177,7 +220,8 @@ def run_reference(args):
         "array_frames_per_sec": round(1.0 / sec, 4),
         "config": {"workload": f"{name}: {desc}", "step": "1 array-frame, STANDARD update + apply"},
         "cpu_baseline": {"value": round(val, 3), "unit": "MP/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} array-frames of {name} after {args.warmup} warm-up"},
+                         "sample": f"{args.steps} array-frames of {name} after {args.warmup} warm-up",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": round(val, 3), "unit": "MP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -395,12 +439,29 @@ def run_camx(args):
             sample = 3 if H * W <= 4_000_000 else 2
             times = cpu_reference_sample(fr, sample + 1, threads)[1:]
             sec = sum(times) / len(times)
-            cpu = {"value": round(n_cams * H * W / 1e6 / sec, 3), "unit": "MP/s", "cores": threads,
+            mp_frame = n_cams * H * W / 1e6
+            cpu = {"value": round(mp_frame / sec, 3), "unit": "MP/s", "cores": threads,
                    "kind": "port",
                    "sample": f"{sample} array-frames of {name} (numpy restatement of the "
                              f"reference: update_exposure per seam + apply_exposure per side, "
                              f"fresh maps, {threads} threads)",
-                   "array_frames_per_sec": round(1.0 / sec, 4)}
+                   "array_frames_per_sec": round(1.0 / sec, 4),
+                   "cpu_model": cpu_model(), "nproc": threads}
+            # SURVEY 8d variants: one thread, and steady state (cached maps)
+            try:
+                t1 = cpu_reference_sample(fr, 1, 1)
+                g = res.gain[0].cpu().numpy()
+                o = res.offset[0].cpu().numpy()
+                tc = cpu_cached_apply_sample(fr, sample + 1, threads, g, o, wrap)[1:]
+                tc1 = cpu_cached_apply_sample(fr, 2, 1, g, o, wrap)[1:]
+                cpu["variants"] = {
+                    "fresh_maps_all_threads_mp_s": cpu["value"],
+                    "fresh_maps_1_thread_mp_s": round(mp_frame / t1[0], 3),
+                    "cached_maps_all_threads_mp_s": round(mp_frame / (sum(tc) / len(tc)), 3),
+                    "cached_maps_1_thread_mp_s": round(mp_frame / tc1[0], 3),
+                }
+            except Exception as e:  # pragma: no cover
+                cpu["variants"] = {"failed": str(e)}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "MP/s", "cores": 0, "kind": "port", "sample": f"failed: {e}"}
 
