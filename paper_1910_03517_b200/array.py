@@ -457,3 +457,41 @@ class ArrayCorrector:
                     comp_done=[t.cuda.Event() for _ in range(slots)])
         self._ring = ring
         return ring
+
+
+def correct_array(frames, cfg: ExposureConfig = ExposureConfig(), prev_maps=None,
+                  mode: ExposureMode = ExposureMode.STANDARD, *, prev_frames=None,
+                  wrap: bool = False, histograms: bool = False, camera_ids=None):
+    """One array-frame through update_exposure (every seam) + apply_exposure
+    (both halves of every camera) - the batched extension of SURVEY 8b.
+
+    frames: (N, H, W, 3) uint8, host numpy (copied to the GPU and back) or a
+    CUDA tensor (stays on the device).  prev_maps: list of SeamMaps of the
+    previous tick (seam s = cameras (s, s+1 mod N)) or None; prev_frames:
+    (N, H, W, 3) of the previous tick for OBJECT_REMOVAL.  Returns
+    (corrected, maps, histograms): corrected like `frames`, maps a list of
+    SeamMaps with seam_id from `camera_ids` (default 0..N-1), histograms
+    uint32 (N, 2, K, 3, 256) of the band pixels (side 0 = LEFT band, cols
+    [W-bw, W); side 1 = RIGHT band) as numpy, or None."""
+    t = _dev.require_cuda()
+    on_host = isinstance(frames, np.ndarray)
+    dev = _dev.to_device(np.ascontiguousarray(frames)) if on_host else frames
+    if dev.dim() != 4 or dev.shape[-1] != 3 or dev.dtype != t.uint8:
+        raise ValueError("frames must be uint8 (N, H, W, 3)")
+    N, H, W = (int(v) for v in dev.shape[:3])
+    ac = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap, histograms=histograms)
+    if prev_maps is not None:
+        ac.set_prev_maps(list(prev_maps))
+    pf = None
+    if prev_frames is not None:
+        pf = (_dev.to_device(np.ascontiguousarray(prev_frames))
+              if isinstance(prev_frames, np.ndarray) else prev_frames)
+        if tuple(pf.shape) != (N, H, W, 3):
+            raise ValueError("prev_frames must match frames")
+    res = ac.correct(dev[None].contiguous(), prev_frames=pf)
+    maps = ac.maps(res, 0, camera_ids)
+    hist = None
+    if res.hist is not None:
+        hist = _dev.to_host(res.hist[0]).view(np.uint32)
+    out = res.out[0]
+    return (_dev.to_host(out) if on_host else out), maps, hist

@@ -738,3 +738,35 @@ def test_tiles_on_camera_shards_sum_to_array_tiles(world, n_cams, size, out):
     torch.cuda.synchronize()
     assert int(cover.min()) == 1 and int(cover.max()) == 1  # one owner per output pixel
     np.testing.assert_array_equal(acc.to(torch.uint8).cpu().numpy(), want.cpu().numpy())
+
+
+@pytest.mark.parametrize("om", [O.SMOOTHING, O.OBJECT_REMOVAL, O.STANDARD])
+def test_correct_array_one_tick_with_previous_state(om):
+    """array.correct_array (the batched drop-in extension) on host
+    numpy: one tick with the previous tick's maps and frames, against the
+    oracle's solve_array + apply_array; histograms bit-exact."""
+    from paper_1910_03517_b200.array import correct_array
+    mode = {O.STANDARD: xp.ExposureMode.STANDARD, O.OBJECT_REMOVAL: xp.ExposureMode.OBJECT_REMOVAL,
+            O.SMOOTHING: xp.ExposureMode.SMOOTHING}[om]
+    N, H, W, K = 4, 96, 160, 8
+    prev = O.synthetic_array(N, H, W, seed=5, objects=2, frame_index=0)
+    cur = O.synthetic_array(N, H, W, seed=5, objects=2, frame_index=1)
+    cfg = xp.ExposureConfig(blocks=K)
+    ocfg = O.Cfg(blocks=K)
+    pg, po, _ = O.solve_array(prev, None, O.STANDARD, ocfg)
+    prev_maps = [xp.SeamMaps(xp.ExposureMap((s, s + 1), xp.Side.LEFT, 32, pg[s, 0], po[s, 0]),
+                             xp.ExposureMap((s, s + 1), xp.Side.RIGHT, 32, pg[s, 1], po[s, 1]))
+                 for s in range(N - 1)]
+    out, maps, hist = correct_array(cur, cfg, prev_maps, mode, prev_frames=prev, histograms=True)
+    wg, wo, _ = O.solve_array(cur, (pg, po), om, ocfg, prev)
+    want = O.apply_array(cur, wg, wo)
+    for s in range(N - 1):
+        assert maps[s].left.seam_id == (s, s + 1)
+        np.testing.assert_allclose(maps[s].left.gain, wg[s, 0], rtol=GAIN_RTOL, atol=GAIN_ATOL)
+        np.testing.assert_allclose(maps[s].right.offset, wo[s, 1], rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    d = np.abs(out.astype(int) - want.astype(int))
+    assert isinstance(out, np.ndarray) and d.max() <= 1 and (d > 0).mean() < 1e-4
+    for c in range(N):
+        mask = O.mask_diff(cur[c], prev[c], 20) if om == O.OBJECT_REMOVAL else None
+        for s, side in ((0, O.LEFT), (1, O.RIGHT)):
+            np.testing.assert_array_equal(hist[c, s], O.band_histograms(cur[c], side, 32, K, mask))
