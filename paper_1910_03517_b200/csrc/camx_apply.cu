@@ -322,8 +322,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 // Tile fusion (config 5): the corrected rows of every stage are written back
 // into their ring slot; each output row of each attention tile whose two
-// source rows the CTA holds (the previous stage's last row stays resident:
-// a slot is refilled one stage late) is resampled from shared memory for
+// source rows the CTA holds (the previous stage stays resident: a slot is
+// refilled two stages late) is resampled from shared memory for
 // the output columns whose two column taps are whole pixels of the CTA's
 // byte range.  Outputs whose taps straddle CTAs are produced afterwards by
 // tile_fixup_kernel from the corrected frame.
@@ -338,8 +338,8 @@ constexpr int kFuseMaxWin = 48;  // windows per array-frame the fused path accep
 // strict downscale only (out < size): i0 is strictly increasing and i1 =
 // i0 + 1, so a source row is the second tap of at most one output row per
 // window (orow[] is well defined)
-// ring of the fused (shared-barrier) kernel: 4-row stages halve the barriers
-// and hit builds per byte; refill lags two stages (previous row resident)
+// ring of the fused kernel: 4-row stages (one CTA barrier and one hit
+// enumeration per stage); refill lags two stages (previous row resident)
 constexpr int kFuseRows = 4;
 constexpr int kFuseStages = 4;
 static_assert(kFuseRows == 4, "hit enumeration uses e >> 2 / e & 3");
