@@ -44,6 +44,9 @@ extern "C" {
 #define CAMX_EINVAL (-1)      /* bad shape / size / config -> ValueError  */
 #define CAMX_EALIGN (-2)      /* pointer alignment not met                 */
 #define CAMX_ENOMEM (-3)      /* scratch allocation failed                 */
+/* positive, like CUDA errors (RuntimeError): */
+#define CAMX_ENCCL_BASE 100000 /* + ncclResult_t of a failed NCCL call       */
+#define CAMX_ENONCCL 199999    /* libnccl.so.2 could not be loaded           */
 
 #define CAMX_SIDE_LEFT 0
 #define CAMX_SIDE_RIGHT 1
@@ -194,6 +197,55 @@ int camx_correct_batch(const uint8_t *images, uint8_t *out,
                        const double *prev_offset, camx_band_stat *stats,
                        uint32_t *hist, double *gain_out, double *offset_out,
                        uint8_t *fit_ok_out, int32_t *counters, void *stream);
+
+/* ---- camera-sharded arrays (multi-GPU) ------------------------
+ * One process per GPU; rank g owns the contiguous camera group
+ * [begin(g), begin(g) + count(g)) of dist.camera_partition (counts differ by
+ * at most one; cmax = ceil(n_cams / world)).  The seam statistics are
+ * exchanged with one NCCL all-gather; NCCL is resolved at run time from the
+ * process's libnccl.so.2 (PyTorch's).  The 128-byte unique id is created on
+ * one rank (camx_comm_unique_id) and broadcast by the caller. */
+int camx_comm_available(void);
+int camx_comm_unique_id(uint8_t *id_out /* 128 bytes */);
+int camx_comm_init(void **comm_out, const uint8_t *id, int32_t n_ranks, int32_t rank);
+int camx_comm_destroy(void *comm);
+
+/* K2 on the all-gathered records: stats_all = [world][n_batch][cmax][2][K]
+ * (rank-major, each rank's block padded to cmax cameras).  Otherwise as
+ * camx_seam_solve (update_exposure for every seam, exposure.py:245-344). */
+int camx_seam_solve_sharded(const camx_band_stat *stats_all, int32_t n_batch,
+                            int32_t n_cams, int32_t world, int32_t wrap,
+                            const camx_solve_config *cfg,
+                            const double *prev_gain, const double *prev_offset,
+                            double *gain_out, double *offset_out,
+                            uint8_t *fit_ok_out, void *stream);
+
+/* camx_correct_batch for this rank's cameras: K1 on images [n_batch]
+ * [cam_count][H][W][3] -> stats_local [n_batch][cmax][2][K] (dense over
+ * cam_count), ncclAllGather into stats_all [world][n_batch][cmax][2][K],
+ * K2 for every seam of the whole array (redundant on every rank, tiny),
+ * K3 on this rank's cameras.  Corrected pixels are byte-identical to the
+ * one-GPU camx_correct_batch.  comm = camx_comm_init handle (NULL only when
+ * world == 1); prev_frame = this rank's cameras of the previous frame
+ * (OBJECT_REMOVAL); hist (optional) [n_batch][cam_count][2][K][3][256];
+ * gain/offset/fit_ok for all seams as camx_correct_batch.  n_chunks (1..8)
+ * > 1 splits the batch: K1 + all-gather + K2 of chunk c+1 run on a
+ * library-owned side stream under K3 of chunk c; stats_all then holds the
+ * chunks' [world][n_c][cmax][2][K] blocks one after another. */
+int camx_correct_batch_sharded(const uint8_t *images, uint8_t *out,
+                               const uint8_t *prev_frame, int32_t n_batch,
+                               int32_t n_cams, int32_t cam_begin,
+                               int32_t cam_count, int32_t world, int32_t wrap,
+                               int32_t height, int32_t width,
+                               int32_t band_width, int32_t t_diff,
+                               const camx_solve_config *cfg,
+                               const double *prev_gain,
+                               const double *prev_offset,
+                               camx_band_stat *stats_local,
+                               camx_band_stat *stats_all, uint32_t *hist,
+                               double *gain_out, double *offset_out,
+                               uint8_t *fit_ok_out, int32_t n_chunks,
+                               void *comm, void *stream);
 
 /* One map on n_images images (apply_exposure / apply_exposure_inplace):
  * gain/offset [K][3], side CAMX_SIDE_*. */

@@ -21,6 +21,8 @@ LIB_PATH = PKG / "libcamx.so"
 CAMX_OK = 0
 CAMX_EINVAL = -1
 CAMX_EALIGN = -2
+CAMX_ENCCL_BASE = 100000
+CAMX_ENONCCL = 199999
 SIDE_LEFT, SIDE_RIGHT = 0, 1
 MODE_STANDARD, MODE_OBJECT_REMOVAL, MODE_SMOOTHING = 0, 1, 2
 
@@ -61,6 +63,13 @@ SIGNATURES = {
     "camx_band_stats": [P, P, P, I64, I32, I32, I32, I32, I32, P, P, P],
     "camx_band_moments": [P, I64, I32, P, P, P, P, P],
     "camx_seam_solve": [P, I32, I32, I32, P, P, P, P, P, P, P],
+    "camx_seam_solve_sharded": [P, I32, I32, I32, I32, P, P, P, P, P, P, P],
+    "camx_comm_available": [],
+    "camx_comm_unique_id": [P],
+    "camx_comm_init": [P, P, I32, I32],
+    "camx_comm_destroy": [P],
+    "camx_correct_batch_sharded": [P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, I32,
+                                   P, P, P, P, P, P, P, P, P, I32, P, P],
     "camx_band_stats_solve": [P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P,
                               P, P, P, P, P],
     "camx_correct_batch": [P, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P,

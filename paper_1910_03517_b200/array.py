@@ -51,11 +51,13 @@ class ArrayCorrector:
                  cfg: ExposureConfig = ExposureConfig(),
                  mode: ExposureMode = ExposureMode.STANDARD, *, wrap: bool = False,
                  histograms: bool = False, cam_begin: int = 0, cam_count: int | None = None,
-                 exchange=None):
-        """cam_begin/cam_count: the cameras this GPU owns (default all);
-        `exchange(stats_local) -> stats_full` assembles the (B, n_cams, 2, K)
-        stat records of every camera (an NCCL all-gather, see dist.py) when
-        the array is sharded across GPUs."""
+                 exchange=None, comm=None):
+        """cam_begin/cam_count: the cameras this GPU owns (default all).  A
+        camera shard needs the other ranks' seam statistics, either through
+        `comm` (dist.NcclComm: camx's own NCCL all-gather inside one
+        camx_correct_batch_sharded call per batch) or `exchange(stats_local)
+        -> stats_full` assembling the (B, n_cams, 2, K) records in Python
+        (any torch.distributed backend, e.g. gloo)."""
         if n_cams < 1:
             raise ValueError("need at least one camera")
         if wrap and n_cams < 2:
@@ -68,9 +70,14 @@ class ArrayCorrector:
         cam_count = n_cams - cam_begin if cam_count is None else cam_count
         if cam_begin < 0 or cam_count < 1 or cam_begin + cam_count > n_cams:
             raise ValueError("camera shard outside the array")
-        if cam_count != n_cams and exchange is None:
+        if cam_count != n_cams and exchange is None and comm is None:
             raise ValueError("a camera shard needs a stats exchange")
+        if comm is not None:
+            from .dist import camera_partition
+            if camera_partition(n_cams, comm.world)[comm.rank] != (cam_begin, cam_count):
+                raise ValueError("camera shard does not match the communicator's rank")
         self.cam_begin, self.cam_count, self.exchange = cam_begin, cam_count, exchange
+        self.comm = comm
         self.n_cams, self.height, self.width = n_cams, height, width
         self.cfg, self.mode, self.wrap = cfg, mode, bool(wrap)
         self.histograms = histograms
@@ -137,6 +144,9 @@ class ArrayCorrector:
         main = stream if stream is not None else t.cuda.current_stream()
         removal = self.mode is ExposureMode.OBJECT_REMOVAL
         pf = prev_frames if prev_frames is not None else self._prev_frame
+        if self.comm is not None and self.S > 0:
+            self._correct_sharded(frames, out, buf, _dev.stream_handle(main), pf)
+            return self._finish(frames, out, buf, main, removal)
         if self.exchange is None and self.S > 0 and self.pipeline_chunks <= 1 and self.fused:
             self._correct_fused(frames, out, buf, _dev.stream_handle(main), pf, _tile_args)
             return self._finish(frames, out, buf, main, removal)
@@ -184,7 +194,13 @@ class ArrayCorrector:
                 if self._prev_frame is None:
                     self._prev_frame = t.empty_like(frames[0])
                 self._prev_frame.copy_(frames[B - 1], non_blocking=True)
-        full = buf["stats"] if self.exchange is None else buf["full"]
+        if self.comm is not None and "stats_all" in buf:
+            R = _lib.STAT_BYTES
+            with t.cuda.stream(main):
+                full = buf["stats_all"].view(-1, 2, self.K, R).index_select(
+                    0, buf["gather_index"]).view(B, self.n_cams, 2, self.K, R)
+        else:
+            full = buf["stats"] if self.exchange is None else buf["full"]
         return CorrectResult(out, gain[:, : self.S], off[:, : self.S], buf["fit_ok"][:, : self.S],
                              full, buf["hist"])
 
@@ -237,6 +253,57 @@ class ArrayCorrector:
             _lib.call("camx_correct_batch_tiles", *common, *tile_args, sh)
         else:
             _lib.call("camx_correct_batch", *common, buf["counters"].data_ptr(), sh)
+
+    def _correct_sharded(self, frames, out, buf, sh, pf):
+        """camx_correct_batch_sharded: K1 on this rank's cameras, NCCL
+        all-gather of the records, K2 for all seams, K3 (one C call)."""
+        t = _dev.torch()
+        cfg = self.cfg
+        B = frames.shape[0]
+        world = self.comm.world
+        cmax = -(-self.n_cams // world)
+        if "stats_all" not in buf:
+            R = _lib.STAT_BYTES
+            buf["stats_local"] = t.empty((B, cmax, 2, self.K, R), dtype=t.uint8, device="cuda")
+            buf["stats_all"] = t.empty((world, B, cmax, 2, self.K, R), dtype=t.uint8,
+                                       device="cuda")
+            # gathered records (per chunk: rank-major [world][n_c][cmax]) ->
+            # (B, n_cams) camera order
+            from .dist import camera_partition
+            parts = camera_partition(self.n_cams, world)
+            nch = min(self.shard_chunks(world), B)
+            idx = []
+            for ci in range(nch):
+                lo, hi = B * ci // nch, B * (ci + 1) // nch
+                idx += [world * cmax * lo + (g * (hi - lo) + (b - lo)) * cmax + l
+                        for b in range(lo, hi) for g, (_, c) in enumerate(parts) for l in range(c)]
+            buf["gather_index"] = t.as_tensor(idx, dtype=t.int64, device="cuda")
+        removal = self.mode is ExposureMode.OBJECT_REMOVAL
+        have_prev = self._prev_maps is not None
+        sc = _lib.SolveConfig(_MODE_CODE[self.mode], self.K, int(cfg.min_band_pixels),
+                              float(cfg.sigma_min), float(cfg.alpha),
+                              float(cfg.min_valid_fraction), int(have_prev),
+                              int(removal and pf is not None))
+        pg, po = self._prev_maps if have_prev else (None, None)
+        _lib.call("camx_correct_batch_sharded", frames.data_ptr(), out.data_ptr(),
+                  _dev.ptr(pf) if removal else None, B, self.n_cams, self.cam_begin,
+                  self.cam_count, world, int(self.wrap), self.height, self.width, cfg.band_width,
+                  cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),
+                  buf["stats_local"].data_ptr(), buf["stats_all"].data_ptr(),
+                  _dev.ptr(buf["hist"]), buf["gain"].data_ptr(), buf["offset"].data_ptr(),
+                  buf["fit_ok"].data_ptr(), min(self.shard_chunks(world), B), self.comm.handle,
+                  sh)
+
+    @staticmethod
+    def shard_chunks(world: int) -> int:
+        """Chunks of the sharded batch (K1 + all-gather + K2 of chunk c+1
+        under K3 of chunk c).  Measured slower at every N on B200 (smaller
+        K3 launches, per-chunk launch and collective latency:
+        tools/shard_probe_native.py), so 1 unless CAMX_SHARD_CHUNKS says."""
+        env = os.environ.get("CAMX_SHARD_CHUNKS")
+        if env:
+            return max(1, min(8, int(env)))
+        return 1
 
     def _side_stream(self):
         if getattr(self, "_side", None) is None:

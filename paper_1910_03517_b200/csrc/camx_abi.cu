@@ -3,6 +3,11 @@
 
 extern "C" int camx_abi_version(void) { return CAMX_ABI_VERSION; }
 
+namespace camx {
+const char *nccl_error_string(int r);  // camx_comm.cu
+}
+using camx::nccl_error_string;
+
 extern "C" const char *camx_status_string(int status) {
   switch (status) {
     case CAMX_OK:
@@ -16,6 +21,9 @@ extern "C" const char *camx_status_string(int status) {
     default:
       break;
   }
+  if (status == CAMX_ENONCCL) return "NCCL library (libnccl.so.2) not loadable";
+  if (status > CAMX_ENCCL_BASE && status < CAMX_ENONCCL)
+    return nccl_error_string(status - CAMX_ENCCL_BASE);
   if (status > 0) return cudaGetErrorString(static_cast<cudaError_t>(status));
   return "unknown camx status";
 }

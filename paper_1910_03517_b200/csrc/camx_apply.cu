@@ -21,6 +21,7 @@
 //   min(., 255) on the 16-bit lanes (VIMNMX.U16x2), then byte pack.
 // Since clamp bounds are integers, clip(rint(y)) == rint(clip(y)).
 #include <cstdlib>
+#include <mutex>
 
 #include "camx_resize.cuh"
 
@@ -805,7 +806,8 @@ namespace camx {
 int launch_seam_solve(const camx_band_stat *stats, int32_t n_batch, int32_t n_cams, int32_t wrap,
                       const camx_solve_config *cfg, const double *prev_gain,
                       const double *prev_offset, double *gain_out, double *offset_out,
-                      uint8_t *fit_ok_out, cudaStream_t stream, bool pdl);
+                      uint8_t *fit_ok_out, cudaStream_t stream, bool pdl, int32_t world = 1,
+                      int32_t cmax = 0);
 }
 
 extern "C" int camx_apply_array(const uint8_t *images, uint8_t *out, int32_t n_batch,
@@ -869,6 +871,28 @@ extern "C" int camx_apply_map(const uint8_t *images, uint8_t *out, int64_t n_ima
 namespace camx {
 
 // K1 (+ K2 as a programmatic dependent) for a whole batch.
+// K1 over a batch: n_batch frames of `per_frame` images, frames 1.. against
+// their predecessors and frame 0 against prev_frame when `removal`.
+static int band_stats_frames(const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch,
+                             int32_t per_frame, int32_t height, int32_t width, int32_t band_width,
+                             int32_t blocks, int32_t t_diff, bool removal, camx_band_stat *stats,
+                             uint32_t *hist, void *stream) {
+  const int64_t frame_bytes = static_cast<int64_t>(height) * width * 3 * per_frame;
+  const int64_t rec_frame = static_cast<int64_t>(per_frame) * 2 * blocks;
+  int st;
+  if (removal && n_batch > 1) {
+    st = camx_band_stats(images + frame_bytes, images, nullptr, (n_batch - 1) * int64_t(per_frame),
+                         height, width, band_width, blocks, t_diff, stats + rec_frame,
+                         hist == nullptr ? nullptr : hist + rec_frame * 768, stream);
+    if (st != CAMX_OK) return st;
+    return camx_band_stats(images, prev_frame, nullptr, per_frame, height, width, band_width,
+                           blocks, t_diff, stats, hist, stream);
+  }
+  return camx_band_stats(images, removal ? prev_frame : nullptr, nullptr,
+                         int64_t(n_batch) * per_frame, height, width, band_width, blocks, t_diff,
+                         stats, hist, stream);
+}
+
 static int stats_and_solve(const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch,
                            int32_t n_cams, int32_t wrap, int32_t height, int32_t width,
                            int32_t band_width, int32_t t_diff, const camx_solve_config *cfg,
@@ -880,23 +904,9 @@ static int stats_and_solve(const uint8_t *images, const uint8_t *prev_frame, int
   if (n_batch < 1 || n_cams < 2 || cfg->blocks < 1 || cfg->blocks > height) return CAMX_EINVAL;
   if (cfg->mode < CAMX_MODE_STANDARD || cfg->mode > CAMX_MODE_SMOOTHING) return CAMX_EINVAL;
   if (cfg->have_prev_maps && (prev_gain == nullptr || prev_offset == nullptr)) return CAMX_EINVAL;
-  const int64_t frame_bytes = static_cast<int64_t>(height) * width * 3 * n_cams;
-  const int64_t rec_frame = static_cast<int64_t>(n_cams) * 2 * cfg->blocks;
   const bool removal = cfg->mode == CAMX_MODE_OBJECT_REMOVAL;
-  int st;
-  // frames 1.. against their predecessors, frame 0 against prev_frame (OBJECT_REMOVAL)
-  if (removal && n_batch > 1) {
-    st = camx_band_stats(images + frame_bytes, images, nullptr, (n_batch - 1) * int64_t(n_cams),
-                         height, width, band_width, cfg->blocks, t_diff, stats + rec_frame,
-                         hist == nullptr ? nullptr : hist + rec_frame * 768, stream);
-    if (st != CAMX_OK) return st;
-    st = camx_band_stats(images, prev_frame, nullptr, n_cams, height, width, band_width,
-                         cfg->blocks, t_diff, stats, hist, stream);
-  } else {
-    st = camx_band_stats(images, removal ? prev_frame : nullptr, nullptr,
-                         int64_t(n_batch) * n_cams, height, width, band_width, cfg->blocks,
-                         t_diff, stats, hist, stream);
-  }
+  const int st = band_stats_frames(images, prev_frame, n_batch, n_cams, height, width, band_width,
+                                   cfg->blocks, t_diff, removal, stats, hist, stream);
   if (st != CAMX_OK) return st;
   return launch_seam_solve(stats, n_batch, n_cams, wrap, cfg, prev_gain, prev_offset, gain_out,
                            offset_out, fit_ok_out, as_stream(stream), true);
@@ -980,6 +990,140 @@ extern "C" int camx_correct_batch(const uint8_t *images, uint8_t *out, const uin
                                gain_out, offset_out);
   p.pdl = 1;  // K3 is a programmatic dependent of K2
   return launch_apply(p, as_stream(stream));
+}
+
+namespace camx {
+int comm_all_gather(const void *send, void *recv, size_t bytes, void *comm, cudaStream_t s);
+}
+constexpr int kMaxShardChunks = 8;
+
+// Library-owned side stream + fork/join events of the chunked sharded
+// pipeline (one set per device; capture-safe: only event record/wait).
+struct SidePipe {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[kMaxShardChunks + 2] = {};
+};
+static int side_pipe(SidePipe *&out) {
+  static std::mutex mu;
+  static SidePipe pipes[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  if (dev < 0 || dev >= 64) return CAMX_EINVAL;
+  std::lock_guard<std::mutex> lock(mu);
+  SidePipe &sp = pipes[dev];
+  if (sp.side == nullptr) {
+    e = cudaStreamCreateWithFlags(&sp.side, cudaStreamNonBlocking);
+    for (int i = 0; e == cudaSuccess && i < kMaxShardChunks + 2; ++i)
+      e = cudaEventCreateWithFlags(&sp.ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  out = &sp;
+  return CAMX_OK;
+}
+
+extern "C" int camx_correct_batch_sharded(
+    const uint8_t *images, uint8_t *out, const uint8_t *prev_frame, int32_t n_batch,
+    int32_t n_cams, int32_t cam_begin, int32_t cam_count, int32_t world, int32_t wrap,
+    int32_t height, int32_t width, int32_t band_width, int32_t t_diff, const camx_solve_config *cfg,
+    const double *prev_gain, const double *prev_offset, camx_band_stat *stats_local,
+    camx_band_stat *stats_all, uint32_t *hist, double *gain_out, double *offset_out,
+    uint8_t *fit_ok_out, int32_t n_chunks, void *comm, void *stream) {
+  if (!images || !out || !cfg || !stats_local || !stats_all || !gain_out || !offset_out)
+    return CAMX_EINVAL;
+  if (n_batch < 1 || n_cams < 2 || world < 1 || world > n_cams) return CAMX_EINVAL;
+  if (n_chunks < 1 || n_chunks > kMaxShardChunks) return CAMX_EINVAL;
+  if (cfg->blocks < 1 || cfg->blocks > height) return CAMX_EINVAL;
+  if (cfg->mode < CAMX_MODE_STANDARD || cfg->mode > CAMX_MODE_SMOOTHING) return CAMX_EINVAL;
+  if (cfg->have_prev_maps && (prev_gain == nullptr || prev_offset == nullptr)) return CAMX_EINVAL;
+  // this rank's group must be one of camera_partition(n_cams, world)
+  const int q = n_cams / world, r = n_cams % world;
+  int rank = -1;
+  for (int g = 0; g < world; ++g)
+    if (g * q + (g < r ? g : r) == cam_begin && q + (g < r ? 1 : 0) == cam_count) rank = g;
+  if (rank < 0) return CAMX_EINVAL;
+  if (world > 1 && comm == nullptr) return CAMX_EINVAL;
+  const int cmax = (n_cams + world - 1) / world;
+  const int S = wrap ? n_cams : n_cams - 1;
+  const bool removal = cfg->mode == CAMX_MODE_OBJECT_REMOVAL;
+  const int64_t img_bytes = static_cast<int64_t>(height) * width * 3;
+  const int64_t frame_bytes = img_bytes * cam_count;
+  const size_t rec = sizeof(camx_band_stat) * 2 * cfg->blocks;  // one camera-frame
+  const int64_t map_frame = static_cast<int64_t>(S) * 2 * cfg->blocks * 3;
+  n_chunks = n_chunks > n_batch ? n_batch : n_chunks;
+  cudaStream_t main = as_stream(stream);
+  SidePipe *sp = nullptr;
+  cudaStream_t side = main;
+  if (n_chunks > 1) {
+    int st = side_pipe(sp);
+    if (st != CAMX_OK) return st;
+    side = sp->side;
+    cudaError_t e = cudaEventRecord(sp->ev[0], main);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, sp->ev[0], 0);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  // Chunk c: K1 -> all-gather -> K2 on `side`, then K3 on `main`; K1/K2 of
+  // chunk c+1 overlap K3 of chunk c.  The tick-loop state flows between
+  // chunks through gain_out (previous frame's maps) and the raw frames.
+  for (int c = 0; c < n_chunks; ++c) {
+    const int lo = static_cast<int>(static_cast<int64_t>(n_batch) * c / n_chunks);
+    const int hi = static_cast<int>(static_cast<int64_t>(n_batch) * (c + 1) / n_chunks);
+    const int nb = hi - lo;
+    if (nb <= 0) continue;
+    const uint8_t *img = images + lo * frame_bytes;
+    const uint8_t *pf = lo == 0 ? prev_frame : img - frame_bytes;
+    camx_band_stat *sl = stats_local + static_cast<int64_t>(lo) * cam_count * 2 * cfg->blocks;
+    uint32_t *hl = hist == nullptr ? nullptr
+                                   : hist + static_cast<int64_t>(lo) * cam_count * 2 * cfg->blocks * 768;
+    uint8_t *sa = reinterpret_cast<uint8_t *>(stats_all) + rec * cmax * world * lo;
+    int st = band_stats_frames(img, pf, nb, cam_count, height, width, band_width, cfg->blocks,
+                               t_diff, removal, sl, hl, side);
+    if (st != CAMX_OK) return st;
+    const size_t block = rec * cmax * nb;  // one rank's block of this chunk
+    if (world > 1 || comm != nullptr) {     // (a one-rank comm still goes through NCCL)
+      const void *send = sl;
+      if (cam_count < cmax) {  // pad each frame to cmax cameras, in this rank's slot
+        uint8_t *slot = sa + block * rank;
+        cudaError_t e = cudaMemcpy2DAsync(slot, rec * cmax, sl, rec * cam_count, rec * cam_count,
+                                          nb, cudaMemcpyDeviceToDevice, side);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        send = slot;  // in-place all-gather
+      }
+      st = comm_all_gather(send, sa, block, comm, side);
+      if (st != CAMX_OK) return st;
+    } else if (reinterpret_cast<void *>(sa) != reinterpret_cast<void *>(sl)) {
+      cudaError_t e = cudaMemcpyAsync(sa, sl, block, cudaMemcpyDeviceToDevice, side);
+      if (e != cudaSuccess) return static_cast<int>(e);
+    }
+    camx_solve_config cc = *cfg;
+    const double *pg = prev_gain, *po = prev_offset;
+    if (lo > 0) {  // the previous chunk's last frame seeds this one
+      cc.have_prev_maps = 1;
+      cc.have_prev_frames = removal ? 1 : cc.have_prev_frames;
+      pg = gain_out + (lo - 1) * map_frame;
+      po = offset_out + (lo - 1) * map_frame;
+    }
+    st = launch_seam_solve(reinterpret_cast<const camx_band_stat *>(sa), nb, n_cams, wrap, &cc,
+                           pg, po, gain_out + lo * map_frame, offset_out + lo * map_frame,
+                           fit_ok_out == nullptr ? nullptr
+                                                 : fit_ok_out + static_cast<int64_t>(lo) * S * cfg->blocks,
+                           side, false, world, cmax);
+    if (st != CAMX_OK) return st;
+    if (side != main) {
+      cudaError_t e = cudaEventRecord(sp->ev[1 + c], side);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(main, sp->ev[1 + c], 0);
+      if (e != cudaSuccess) return static_cast<int>(e);
+    }
+    ApplyParams p = array_params(img, out + lo * frame_bytes, nb, cam_count, wrap, height, width,
+                                 cfg->blocks, gain_out + lo * map_frame, offset_out + lo * map_frame);
+    p.cam_begin = cam_begin;
+    p.n_cams = n_cams;
+    p.S = S;
+    p.pdl = side == main ? 1 : 0;  // K3 right behind K2 on one stream
+    st = launch_apply(p, main);
+    if (st != CAMX_OK) return st;
+  }
+  return CAMX_OK;
 }
 
 extern "C" int camx_correct_batch_tiles(

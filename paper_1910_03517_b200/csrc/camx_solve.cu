@@ -47,9 +47,12 @@ namespace camx {
 int launch_seam_solve(const camx_band_stat *stats, int32_t n_batch, int32_t n_cams, int32_t wrap,
                       const camx_solve_config *cfg, const double *prev_gain,
                       const double *prev_offset, double *gain_out, double *offset_out,
-                      uint8_t *fit_ok_out, cudaStream_t stream, bool pdl) {
+                      uint8_t *fit_ok_out, cudaStream_t stream, bool pdl, int32_t world,
+                      int32_t cmax) {
   SolveParams p{};
   p.stats = stats;
+  p.world = world;
+  p.cmax = cmax;
   p.B = n_batch;
   p.N = n_cams;
   p.S = wrap ? n_cams : n_cams - 1;
@@ -88,7 +91,24 @@ extern "C" int camx_seam_solve(const camx_band_stat *stats, int32_t n_batch, int
   if (cfg->mode < CAMX_MODE_STANDARD || cfg->mode > CAMX_MODE_SMOOTHING) return CAMX_EINVAL;
   if (cfg->have_prev_maps && (prev_gain == nullptr || prev_offset == nullptr)) return CAMX_EINVAL;
   return launch_seam_solve(stats, n_batch, n_cams, wrap, cfg, prev_gain, prev_offset, gain_out,
-                           offset_out, fit_ok_out, as_stream(stream), false);
+                           offset_out, fit_ok_out, as_stream(stream), false, 1, n_cams);
+}
+
+extern "C" int camx_seam_solve_sharded(const camx_band_stat *stats_all, int32_t n_batch,
+                                       int32_t n_cams, int32_t world, int32_t wrap,
+                                       const camx_solve_config *cfg, const double *prev_gain,
+                                       const double *prev_offset, double *gain_out,
+                                       double *offset_out, uint8_t *fit_ok_out, void *stream) {
+  if (cfg == nullptr || stats_all == nullptr || gain_out == nullptr || offset_out == nullptr)
+    return CAMX_EINVAL;
+  if (n_batch < 0 || n_cams < 1 || cfg->blocks < 1 || world < 1 || world > n_cams)
+    return CAMX_EINVAL;
+  if (wrap && n_cams < 2) return CAMX_EINVAL;
+  if (cfg->mode < CAMX_MODE_STANDARD || cfg->mode > CAMX_MODE_SMOOTHING) return CAMX_EINVAL;
+  if (cfg->have_prev_maps && (prev_gain == nullptr || prev_offset == nullptr)) return CAMX_EINVAL;
+  const int32_t cmax = (n_cams + world - 1) / world;
+  return launch_seam_solve(stats_all, n_batch, n_cams, wrap, cfg, prev_gain, prev_offset,
+                           gain_out, offset_out, fit_ok_out, as_stream(stream), false, world, cmax);
 }
 
 extern "C" int camx_fit_affine(const double *l_mean, const double *l_std, const int64_t *l_valid,

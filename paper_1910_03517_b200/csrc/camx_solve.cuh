@@ -78,8 +78,9 @@ __device__ __forceinline__ Pair blend_pair(const Pair &a, const Pair &b, double 
 }
 
 struct SolveParams {
-  const camx_band_stat *stats;  // [B][N][2][K]
+  const camx_band_stat *stats;  // [B][N][2][K], or rank-major (world > 1, see rec_index)
   int32_t B, N, S, K, wrap;
+  int32_t world, cmax;          // camera shards: world ranks, <= cmax cameras each
   camx_solve_config cfg;
   const double *prev_gain, *prev_offset;  // [S][2][K][3]
   double *gain, *offset;                  // [B][S][2][K][3]
@@ -111,6 +112,25 @@ __device__ __forceinline__ camx_band_stat load_rec(const camx_band_stat *r) {
   return o;
 }
 
+// Record of (frame b, camera cam, side, block k).  world <= 1: the dense
+// [B][N][2][K] layout.  world > 1: the NCCL all-gather of the camera shards
+// (dist.camera_partition: contiguous groups, sizes differing by <= 1), rank
+// g's block [B][cmax][2][K] at g * B * cmax records, camera cam at local
+// index cam - begin(g).
+__device__ __forceinline__ int64_t rec_index(const SolveParams &p, int b, int cam, int side,
+                                             int k) {
+  int64_t slot;
+  if (p.world <= 1) {
+    slot = static_cast<int64_t>(b) * p.N + cam;
+  } else {
+    const int q = p.N / p.world, r = p.N % p.world;
+    const int g = cam < (q + 1) * r ? cam / (q + 1) : r + (cam - (q + 1) * r) / q;
+    const int beg = g * q + min(g, r);
+    slot = (static_cast<int64_t>(g) * p.B + b) * p.cmax + (cam - beg);
+  }
+  return (slot * 2 + side) * p.K + k;
+}
+
 __device__ __forceinline__ void solve_seam_block(const SolveParams &p, int s, int k,
                                                  Cand (*cand)[3]) {
   const int camL = s;
@@ -135,10 +155,8 @@ __device__ __forceinline__ void solve_seam_block(const SolveParams &p, int s, in
       const int bl = idx / 3;
       const int ch = idx % 3;
       const int b = b0 + bl;
-      const camx_band_stat L = load_rec(
-          &p.stats[((static_cast<int64_t>(b) * p.N + camL) * 2 + CAMX_SIDE_LEFT) * p.K + k]);
-      const camx_band_stat R = load_rec(
-          &p.stats[((static_cast<int64_t>(b) * p.N + camR) * 2 + CAMX_SIDE_RIGHT) * p.K + k]);
+      const camx_band_stat L = load_rec(&p.stats[rec_index(p, b, camL, CAMX_SIDE_LEFT, k)]);
+      const camx_band_stat R = load_rec(&p.stats[rec_index(p, b, camR, CAMX_SIDE_RIGHT, k)]);
       Cand c;
       const Mom Lr = mom_of(L, ch, true), Rr = mom_of(R, ch, true);
       bool ok;

@@ -8,6 +8,10 @@ bound) over NCCL, runs the tiny K2 solve for all seams redundantly, and
 applies K3 to its own cameras only - so the corrected output is
 byte-identical to the 1-GPU result.  The reference has no
 parallelism; this is the one exchange step the path really has.
+
+With NCCL the exchange runs in C (NcclComm + camx_correct_batch_sharded:
+K1 -> ncclAllGather -> K2 -> K3 from one call, ~no host work per batch);
+make_stats_exchange is the backend-agnostic Python form (gloo tests).
 """
 
 from __future__ import annotations
@@ -61,18 +65,71 @@ def make_stats_exchange(n_cams: int, group=None):
     return exchange
 
 
+class NcclComm:
+    """camx's own NCCL communicator over the ranks of `group` (camx_comm_*):
+    the unique id is made on the group's first rank and broadcast with
+    torch.distributed; afterwards every batch's seam-stat all-gather is
+    issued from C inside camx_correct_batch_sharded (no Python, no
+    torch.distributed call on the per-batch path).  Call on every rank
+    (NCCL init is collective), with this rank's CUDA device current."""
+
+    def __init__(self, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+        t = _dev.require_cuda()
+        if not _lib.load().camx_comm_available():
+            raise RuntimeError("camx: libnccl.so.2 not loadable, cannot build an NCCL comm")
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = t.zeros(128, dtype=t.uint8)
+        if self.rank == 0:
+            _lib.call("camx_comm_unique_id", uid.data_ptr())
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        if dist.get_backend(group) == "nccl":
+            d = uid.cuda()
+            dist.broadcast(d, src=src, group=group)
+            uid = d.cpu()
+        else:
+            dist.broadcast(uid, src=src, group=group)
+        h = ctypes.c_void_p()
+        _lib.call("camx_comm_init", ctypes.byref(h), uid.data_ptr(), self.world, self.rank)
+        self.handle = h.value
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            from . import _lib
+            _lib.call("camx_comm_destroy", self.handle)
+            self.handle = None
+
+
 def sharded_corrector(n_cams: int, height: int, width: int,
                       cfg: ExposureConfig = ExposureConfig(),
                       mode: ExposureMode = ExposureMode.STANDARD, *, wrap: bool = False,
-                      histograms: bool = False, group=None) -> ArrayCorrector:
-    """ArrayCorrector for this rank's camera shard of an n_cams array."""
+                      histograms: bool = False, group=None, native: bool | None = None
+                      ) -> ArrayCorrector:
+    """ArrayCorrector for this rank's camera shard of an n_cams array.
+
+    native (default: the group's backend is NCCL): exchange the seam stats
+    with camx's own NCCL communicator inside one C call per batch
+    (camx_correct_batch_sharded); otherwise through torch.distributed
+    all-gathers in Python (make_stats_exchange; any backend)."""
     import torch.distributed as dist
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     begin, count = camera_partition(n_cams, world)[rank]
-    ex = make_stats_exchange(n_cams, group) if world > 1 else None
+    if world == 1:
+        return ArrayCorrector(n_cams, height, width, cfg, mode, wrap=wrap, histograms=histograms)
+    if native is None:
+        native = dist.get_backend(group) == "nccl"
+    if native:
+        return ArrayCorrector(n_cams, height, width, cfg, mode, wrap=wrap, histograms=histograms,
+                              cam_begin=begin, cam_count=count, comm=NcclComm(group))
     return ArrayCorrector(n_cams, height, width, cfg, mode, wrap=wrap, histograms=histograms,
-                          cam_begin=begin, cam_count=count, exchange=ex)
+                          cam_begin=begin, cam_count=count,
+                          exchange=make_stats_exchange(n_cams, group))
 
 
 def sharded_window_counts(origins, size: int, *, cur=None, prev=None, mask=None,

@@ -770,3 +770,105 @@ def test_correct_array_one_tick_with_previous_state(om):
         mask = O.mask_diff(cur[c], prev[c], 20) if om == O.OBJECT_REMOVAL else None
         for s, side in ((0, O.LEFT), (1, O.RIGHT)):
             np.testing.assert_array_equal(hist[c, s], O.band_histograms(cur[c], side, 32, K, mask))
+
+
+def _rank_major(recs, N, world):
+    """(B, N, 2, K, R) records -> the NCCL all-gather layout of camera
+    shards: (world, B, cmax, 2, K, R), each rank's block padded to cmax."""
+    from paper_1910_03517_b200.dist import camera_partition
+    B = recs.shape[0]
+    cmax = -(-N // world)
+    out = torch.full((world, B, cmax, *recs.shape[2:]), 0xAB, dtype=recs.dtype, device=recs.device)
+    for g, (b0, c) in enumerate(camera_partition(N, world)):
+        out[g, :, :c] = recs[:, b0:b0 + c]
+    return out
+
+
+@pytest.mark.parametrize("N,world,wrap", [(5, 2, False), (7, 3, True), (8, 8, False), (6, 4, True)])
+@pytest.mark.parametrize("mode", [xp.ExposureMode.STANDARD, xp.ExposureMode.OBJECT_REMOVAL,
+                                  xp.ExposureMode.SMOOTHING])
+def test_seam_solve_on_rank_major_records(N, world, wrap, mode):
+    """camx_seam_solve_sharded on the all-gathered (rank-major, padded)
+    records equals camx_seam_solve on the dense (B, N) records bit for bit,
+    for uneven partitions and wrap seams."""
+    import ctypes
+
+    from paper_1910_03517_b200 import _lib
+    H, W, B, K = 64, 96, 4, 4
+    frames = np.stack([O.synthetic_array(N, H, W, seed=7 + N, objects=2, frame_index=t)
+                       for t in range(B)])
+    cfg = xp.ExposureConfig(band_width=16, blocks=K)
+    ac = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap)
+    d = torch.from_numpy(frames).cuda()
+    ac.correct(d[:1])  # previous maps / frame for the second call
+    res = ac.correct(d[1:])
+    S = N if wrap else N - 1
+    removal = mode is xp.ExposureMode.OBJECT_REMOVAL
+    sc = _lib.SolveConfig(xp._MODE_CODE[mode], K, int(cfg.min_band_pixels), float(cfg.sigma_min),
+                          float(cfg.alpha), float(cfg.min_valid_fraction), 1, int(removal))
+    pg = torch.rand((S, 2, K, 3), dtype=torch.float64, device="cuda") + 0.5
+    po = torch.rand((S, 2, K, 3), dtype=torch.float64, device="cuda") * 10 - 5
+    Bn = B - 1
+    outs = []
+    for layout in ("dense", "sharded"):
+        g = torch.empty((Bn, S, 2, K, 3), dtype=torch.float64, device="cuda")
+        o = torch.empty_like(g)
+        ok = torch.empty((Bn, S, K), dtype=torch.uint8, device="cuda")
+        if layout == "dense":
+            _lib.call("camx_seam_solve", res.stats.data_ptr(), Bn, N, int(wrap), ctypes.byref(sc),
+                      pg.data_ptr(), po.data_ptr(), g.data_ptr(), o.data_ptr(), ok.data_ptr(), None)
+        else:
+            rm = _rank_major(res.stats, N, world).contiguous()
+            _lib.call("camx_seam_solve_sharded", rm.data_ptr(), Bn, N, world, int(wrap),
+                      ctypes.byref(sc), pg.data_ptr(), po.data_ptr(), g.data_ptr(), o.data_ptr(),
+                      ok.data_ptr(), None)
+        outs.append((g.cpu().numpy(), o.cpu().numpy(), ok.cpu().numpy()))
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+@pytest.mark.parametrize("use_comm", [False, True])
+@pytest.mark.parametrize("mode", [xp.ExposureMode.STANDARD, xp.ExposureMode.OBJECT_REMOVAL,
+                                  xp.ExposureMode.SMOOTHING])
+def test_correct_batch_sharded_one_rank_matches_array(use_comm, mode, chunks, monkeypatch):
+    """camx_correct_batch_sharded with world = 1 (optionally through a real
+    one-rank NCCL communicator: dlopen of the process's libnccl, unique id,
+    comm init, all-gather; optionally in 3 chunks on the side-stream
+    pipeline) reproduces ArrayCorrector.correct exactly, state carried
+    across two calls."""
+    import ctypes
+
+    from paper_1910_03517_b200 import _lib
+    monkeypatch.setenv("CAMX_SHARD_CHUNKS", str(chunks))
+    N, H, W, B, K = 4, 96, 128, 3, 4
+    frames = np.stack([O.synthetic_array(N, H, W, seed=77, objects=2, frame_index=t)
+                       for t in range(2 * B)])
+    cfg = xp.ExposureConfig(band_width=16, blocks=K)
+    d = torch.from_numpy(frames).cuda()
+    want_ac = ArrayCorrector(N, H, W, cfg, mode, histograms=True)
+    want = [want_ac.correct(d[:B]), want_ac.correct(d[B:])]
+
+    class OneRank:
+        world, rank = 1, 0
+
+        def __init__(self):
+            self.handle = None
+            if use_comm:
+                assert _lib.load().camx_comm_available() == 1
+                uid = torch.zeros(128, dtype=torch.uint8)
+                _lib.call("camx_comm_unique_id", uid.data_ptr())
+                h = ctypes.c_void_p()
+                _lib.call("camx_comm_init", ctypes.byref(h), uid.data_ptr(), 1, 0)
+                self.handle = h.value
+
+    comm = OneRank()
+    ac = ArrayCorrector(N, H, W, cfg, mode, histograms=True, comm=comm)
+    got = [ac.correct(d[:B]), ac.correct(d[B:])]
+    for g_, w_ in zip(got, want):
+        np.testing.assert_array_equal(g_.out.cpu().numpy(), w_.out.cpu().numpy())
+        np.testing.assert_array_equal(g_.gain.cpu().numpy(), w_.gain.cpu().numpy())
+        np.testing.assert_array_equal(g_.stats.cpu().numpy(), w_.stats.cpu().numpy())
+        np.testing.assert_array_equal(g_.hist.cpu().numpy(), w_.hist.cpu().numpy())
+    if comm.handle:
+        _lib.call("camx_comm_destroy", comm.handle)
