@@ -285,12 +285,18 @@ def run_camx(args):
         tiles_buf = torch.empty((n_tiles, 416, 416, 3), dtype=torch.uint8, device="cuda")
 
     use_graph = not args.no_graph and world == 1 and not tiles_mode
+    # N > 1 over NCCL: the front half (K1 -> all-gather -> K2) of batch k on a
+    # side stream under K3 of batch k-1 (ArrayCorrector.submit)
+    use_pipe = (world > 1 and getattr(ac, "comm", None) is not None and not tiles_mode
+                and os.environ.get("CAMX_SHARD_PIPE", "1") != "0")
 
     def step():
         if tiles_mode:
             return ac.correct_and_tile(frames, out=out, tiles=tiles_buf, stream=stream)[0]
         if use_graph:  # CUDA graph replay of K1 -> K2 -> K3 (+ state carry)
             return ac.correct_graphed(frames, out)
+        if use_pipe:
+            return ac.submit(frames, out, stream=stream)
         return ac.correct(frames, out, stream=stream)
 
     with torch.cuda.stream(stream):
@@ -309,6 +315,13 @@ def run_camx(args):
             # K1 (x2 for OBJECT_REMOVAL with B > 1) + K2 + K3 (+ tile fix-up)
             n_launch[0] += 3 if (mode is ExposureMode.OBJECT_REMOVAL and a[3] > 1) else 2
             n_launch[0] += 1 if fn == "camx_correct_batch" else 2
+        elif fn == "camx_correct_batch_sharded":  # K1 (x2) + K2 + K3 (+ NCCL, not ours)
+            n_launch[0] += 4 if (mode is ExposureMode.OBJECT_REMOVAL and a[3] > 1) else 3
+        elif fn == "camx_correct_batch_sharded_step":
+            if a[0] is not None:  # front half: K1 (x2) + K2
+                n_launch[0] += 3 if (mode is ExposureMode.OBJECT_REMOVAL and a[2] > 1) else 2
+            if a[21] is not None:  # back half: K3 of the previous batch
+                n_launch[0] += 1
         elif fn.startswith("camx_"):
             n_launch[0] += 1
         orig_call(fn, *a)
@@ -328,6 +341,10 @@ def run_camx(args):
             barrier()
     finally:
         _lib.call = orig_call
+    if use_pipe:  # drain the pipeline (outside the timed region)
+        with torch.cuda.stream(stream):
+            res = ac.flush(stream=stream) or res
+        torch.cuda.synchronize()
     if use_graph:  # replays do not pass through _lib.call: same kernels as an eager step
         per_step = 3 + (1 if (mode is ExposureMode.OBJECT_REMOVAL and B > 1) else 0)
         n_launch[0] = per_step * args.steps
@@ -479,7 +496,10 @@ def run_camx(args):
                        "step": "K1 band stats + K2 seam solve + K3 apply per array-frame",
                        "l2": "inputs larger than L2 (batch >> 126 MB)",
                        "parallelism": f"camera-shard{world}" if world > 1 else "single",
-                       "launch": "cuda-graph replay" if use_graph else "eager (PDL-chained)"},
+                       "launch": ("cuda-graph replay" if use_graph else
+                                  "software-pipelined: K1 -> NCCL all-gather -> K2 of batch k on "
+                                  "a side stream under K3 of batch k-1" if use_pipe else
+                                  "eager (PDL-chained)")},
             "roofline": {"bound": "hbm", "kernel": k3_name,
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,

@@ -247,6 +247,26 @@ int camx_correct_batch_sharded(const uint8_t *images, uint8_t *out,
                                uint8_t *fit_ok_out, int32_t n_chunks,
                                void *comm, void *stream);
 
+/* Software-pipelined step of the sharded path: the front half (K1 ->
+ * all-gather -> K2) of batch k runs on a library-owned side stream while K3
+ * of batch k-1 (apply_images / apply_out / apply_gain / apply_offset: the
+ * previous step's batch and maps) runs on `stream`; `stream` then joins the
+ * side stream, so work issued on it afterwards (refilling `images`, the next
+ * step) is ordered after both.  images == NULL: no front half (flush);
+ * apply_images == NULL: no back half (first step).  The caller double-buffers
+ * the maps / records between consecutive steps.  One pipelined sequence per
+ * device at a time. */
+int camx_correct_batch_sharded_step(
+    const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch,
+    int32_t n_cams, int32_t cam_begin, int32_t cam_count, int32_t world,
+    int32_t wrap, int32_t height, int32_t width, int32_t band_width,
+    int32_t t_diff, const camx_solve_config *cfg, const double *prev_gain,
+    const double *prev_offset, camx_band_stat *stats_local,
+    camx_band_stat *stats_all, uint32_t *hist, double *gain_out,
+    double *offset_out, uint8_t *fit_ok_out, const uint8_t *apply_images,
+    uint8_t *apply_out, int32_t apply_batch, const double *apply_gain,
+    const double *apply_offset, void *comm, void *stream);
+
 /* One map on n_images images (apply_exposure / apply_exposure_inplace):
  * gain/offset [K][3], side CAMX_SIDE_*. */
 int camx_apply_map(const uint8_t *images, uint8_t *out, int64_t n_images,

@@ -70,6 +70,8 @@ SIGNATURES = {
     "camx_comm_destroy": [P],
     "camx_correct_batch_sharded": [P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, I32,
                                    P, P, P, P, P, P, P, P, P, I32, P, P],
+    "camx_correct_batch_sharded_step": [P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, I32,
+                                        P, P, P, P, P, P, P, P, P, P, P, I32, P, P, P, P],
     "camx_band_stats_solve": [P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P,
                               P, P, P, P, P],
     "camx_correct_batch": [P, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P,

@@ -294,6 +294,139 @@ class ArrayCorrector:
                   buf["fit_ok"].data_ptr(), min(self.shard_chunks(world), B), self.comm.handle,
                   sh)
 
+    # ------------------------------------------------------------ pipelined stream
+    def submit(self, frames, out=None, *, stream=None) -> CorrectResult | None:
+        """Software-pipelined stream of batches for a camera shard (needs
+        `comm`): this call runs the front half (K1 -> NCCL all-gather -> K2)
+        of `frames` on a side stream while K3 of the previously submitted
+        batch runs on `stream`; returns the previous batch's CorrectResult
+        (complete in `stream` order), or None on the first call.  `flush()`
+        applies the last batch.  Keep each batch's frames/out alive until
+        its result is returned (the frames buffer may be refilled on
+        `stream` right after the call: the call's end is joined into it).
+        Maps and records are double-buffered: a returned result's gain /
+        offset / fit_ok / stats / hist stay valid until two more submits
+        (copy them to keep them).  The tick-loop state carries across
+        submits like correct()."""
+        t = _dev.require_cuda()
+        if self.comm is None or self.S == 0:
+            raise ValueError("submit() pipelines the sharded path: construct with comm=")
+        if frames.dim() == 4:
+            frames = frames[None]
+        B = frames.shape[0]
+        if tuple(frames.shape[1:]) != (self.cam_count, self.height, self.width, 3) or \
+                frames.dtype != t.uint8 or not frames.is_cuda or not frames.is_contiguous():
+            raise ValueError("frames must be a contiguous uint8 CUDA tensor "
+                             f"(B, {self.cam_count}, {self.height}, {self.width}, 3)")
+        if out is None:
+            out = t.empty_like(frames)
+        elif out.shape != frames.shape or not out.is_contiguous():
+            raise ValueError("out must match frames")
+        old = getattr(self, "_pipe", None)
+        if old is not None and old["pending"] is not None and old["B"] != B:
+            raise ValueError("submit() batches must keep one size (flush() first)")
+        pipe = self._pipe_state(B)
+        main = stream if stream is not None else t.cuda.current_stream()
+        k = pipe["k"]
+        cur = pipe["bufs"][k % 2]
+        removal = self.mode is ExposureMode.OBJECT_REMOVAL
+        pending = pipe["pending"]
+        if pending is not None and self.S > 0:  # maps of the previous batch's last frame
+            pg, po = pending[2]["gain"][-1], pending[2]["offset"][-1]
+        else:
+            pg, po = self._prev_maps if self._prev_maps is not None else (None, None)
+        pf = self._prev_frame if removal else None
+        self._step_call(frames, B, cur, pg, po, pf, pending, main)
+        res = self._pending_result(pending, main)
+        pipe["pending"] = (frames, out, cur)
+        pipe["k"] = k + 1
+        if removal:  # raw last frame for the next batch's motion mask
+            with t.cuda.stream(main):
+                if self._prev_frame is None:
+                    self._prev_frame = t.empty_like(frames[0])
+                self._prev_frame.copy_(frames[B - 1], non_blocking=True)
+        return res
+
+    def flush(self, *, stream=None) -> CorrectResult | None:
+        """K3 of the last submitted batch; returns its result.  The tick-loop
+        state (maps, previous frame) carries on to correct()/submit()."""
+        t = _dev.require_cuda()
+        pipe = getattr(self, "_pipe", None)
+        if pipe is None or pipe["pending"] is None:
+            return None
+        main = stream if stream is not None else t.cuda.current_stream()
+        pending = pipe["pending"]
+        self._step_call(None, 0, None, None, None, None, pending, main)
+        res = self._pending_result(pending, main)
+        buf = self._buffers(pending[0].shape[0])
+        with t.cuda.stream(main):
+            buf["prev_g"].copy_(pending[2]["gain"][-1], non_blocking=True)
+            buf["prev_o"].copy_(pending[2]["offset"][-1], non_blocking=True)
+        self._prev_maps = (buf["prev_g"], buf["prev_o"])
+        pipe["pending"] = None
+        return res
+
+    def _pipe_state(self, B):
+        pipe = getattr(self, "_pipe", None)
+        if pipe is None or pipe["B"] != B:
+            t = _dev.torch()
+            world = self.comm.world
+            cmax = -(-self.n_cams // world)
+            R, K, S = _lib.STAT_BYTES, self.K, self.S
+
+            def one():
+                return dict(
+                    stats_local=t.empty((B, cmax, 2, K, R), dtype=t.uint8, device="cuda"),
+                    stats_all=t.empty((world, B, cmax, 2, K, R), dtype=t.uint8, device="cuda"),
+                    hist=(t.empty((B, self.cam_count, 2, K, 3, 256), dtype=t.int32, device="cuda")
+                          if self.histograms else None),
+                    gain=t.empty((B, S, 2, K, 3), dtype=t.float64, device="cuda"),
+                    offset=t.empty((B, S, 2, K, 3), dtype=t.float64, device="cuda"),
+                    fit_ok=t.empty((B, S, K), dtype=t.uint8, device="cuda"))
+            from .dist import camera_partition
+            idx = [g * B * cmax + b * cmax + l for b in range(B)
+                   for g, (_, c) in enumerate(camera_partition(self.n_cams, world))
+                   for l in range(c)]
+            pipe = dict(B=B, k=0, pending=None, bufs=[one(), one()],
+                        index=t.as_tensor(idx, dtype=t.int64, device="cuda"))
+            self._pipe = pipe
+        return pipe
+
+    def _step_call(self, frames, B, cur, pg, po, pf, pending, main):
+        cfg = self.cfg
+        removal = self.mode is ExposureMode.OBJECT_REMOVAL
+        sc = _lib.SolveConfig(_MODE_CODE[self.mode], self.K, int(cfg.min_band_pixels),
+                              float(cfg.sigma_min), float(cfg.alpha),
+                              float(cfg.min_valid_fraction), int(pg is not None),
+                              int(removal and pf is not None))
+        front = () if frames is None else (
+            frames.data_ptr(), _dev.ptr(pf) if removal else None, B)
+        if not front:
+            front = (None, None, 0)
+        cb = cur if cur is not None else {}
+        ap = (None, None, 0, None, None) if pending is None else (
+            pending[0].data_ptr(), pending[1].data_ptr(), pending[0].shape[0],
+            pending[2]["gain"].data_ptr(), pending[2]["offset"].data_ptr())
+        _lib.call("camx_correct_batch_sharded_step", *front, self.n_cams, self.cam_begin,
+                  self.cam_count, self.comm.world, int(self.wrap), self.height, self.width,
+                  cfg.band_width, cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),
+                  _dev.ptr(cb.get("stats_local")), _dev.ptr(cb.get("stats_all")),
+                  _dev.ptr(cb.get("hist")), _dev.ptr(cb.get("gain")),
+                  _dev.ptr(cb.get("offset")), _dev.ptr(cb.get("fit_ok")), *ap,
+                  self.comm.handle, _dev.stream_handle(main))
+
+    def _pending_result(self, pending, main):
+        if pending is None:
+            return None
+        t = _dev.torch()
+        frames, out, b = pending
+        B = frames.shape[0]
+        R = _lib.STAT_BYTES
+        with t.cuda.stream(main):
+            full = b["stats_all"].view(-1, 2, self.K, R).index_select(
+                0, self._pipe["index"]).view(B, self.n_cams, 2, self.K, R)
+        return CorrectResult(out, b["gain"], b["offset"], b["fit_ok"], full, b["hist"])
+
     @staticmethod
     def shard_chunks(world: int) -> int:
         """Chunks of the sharded batch (K1 + all-gather + K2 of chunk c+1

@@ -50,3 +50,35 @@ for world, B, ch in [(1, 30, 1), (2, 30, 1), (2, 30, 2), (4, 30, 1), (4, 30, 2),
               f"(ideal {40300 * world:.0f})", flush=True)
         del frames, out, ac
         torch.cuda.empty_cache()
+
+print("-- pipelined (ArrayCorrector.submit: front half of batch k under K3 of batch k-1)")
+os.environ["CAMX_SHARD_CHUNKS"] = "1"
+for world, B in [(1, 30), (2, 30), (4, 30), (8, 30), (8, 60)]:
+    b0, c = camera_partition(N, world)[0]
+
+    class Comm:
+        rank = 0
+        handle = h.value
+    Comm.world = world
+    frames = synthetic_batch(B, c, H, W, seed=1)
+    out = torch.empty_like(frames)
+    ac = ArrayCorrector(N, H, W, cam_begin=b0, cam_count=c, comm=Comm())
+    for _ in range(5):
+        ac.submit(frames, out)
+    torch.cuda.synchronize()
+    steps = 40
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(steps):
+        ac.submit(frames, out)
+    e1.record()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    ac.flush()
+    ms = e0.elapsed_time(e1) / steps
+    print(f"world {world} B {B} pipelined: gpu {ms:.3f} ms/step, host enqueue "
+          f"{(t1 - t0) / steps * 1e3:.3f} ms/step, {B / (ms / 1e3):.0f} array-fps per rank "
+          f"(ideal {40300 * world:.0f})", flush=True)
+    del frames, out, ac
+    torch.cuda.empty_cache()
