@@ -400,12 +400,14 @@ def run_camx(args):
     tp = ROOT / "profiles" / "apply_traffic.json"
     if tp.exists():
         try:
-            d = json.loads(tp.read_text())
-            if d.get("workload") == name:
-                # DRAM bytes per algorithmic byte of the captured launch,
-                # scaled to this run's launch size (streaming kernel)
-                traffic = int(d["dram_bytes_per_launch"] / d["algorithmic_bytes_per_launch"]
-                              * k3_launch_bytes)
+            entries = json.loads(tp.read_text())
+            entries = entries.get("entries", [entries])
+            for d in entries:
+                if d.get("workload") == name:
+                    # DRAM bytes per algorithmic byte of the captured launch,
+                    # scaled to this run's launch size (streaming kernel)
+                    traffic = int(d["dram_bytes_per_launch"] / d["algorithmic_bytes_per_launch"]
+                                  * k3_launch_bytes)
         except Exception:
             pass
 
