@@ -141,6 +141,7 @@ __device__ __forceinline__ void solve_seam_block(const SolveParams &p, int s, in
   const int chB = threadIdx.x;
   bool have_prev = cfg.have_prev_maps != 0;
   Pair prev{1.0, 0.0, 1.0, 0.0};
+  __shared__ Pair prev_s[3], next_s[3];
   if (chB < 3 && have_prev) {
     const int64_t pb = static_cast<int64_t>(s) * 2 * K3 + k * 3 + chB;
     prev.gl = p.prev_gain[pb];
@@ -150,6 +151,7 @@ __device__ __forceinline__ void solve_seam_block(const SolveParams &p, int s, in
   }
   for (int b0 = 0; b0 < p.B; b0 += kSolveFrames) {
     const int nb = min(kSolveFrames, p.B - b0);
+    bool any_blend = false;
     // ---- phase A: independent per (frame, channel)
     for (int idx = threadIdx.x; idx < nb * 3; idx += blockDim.x) {
       const int bl = idx / 3;
@@ -177,10 +179,43 @@ __device__ __forceinline__ void solve_seam_block(const SolveParams &p, int s, in
         c.keep = (ok_m && (fmin(fl, fr) >= cfg.min_valid_fraction)) ? 1 : 2;  // 2: smooth
       }
       cand[bl][ch] = c;
+      any_blend |= (c.keep == 2);
     }
-    __syncthreads();
+    // Without a blend (SMOOTHING, or OBJECT_REMOVAL's smoothing fallback)
+    // the tick loop only carries the previous output through unfittable
+    // frames: out[b] = value of the last "defined" frame j <= b (masked fit
+    // kept, or raw fit ok), else the chunk's incoming maps - every frame is
+    // independent given that, so phase B runs in parallel.
+    const bool parallel =
+        !__syncthreads_or(any_blend) && cfg.mode != CAMX_MODE_SMOOTHING;
+    if (parallel) {
+      if (chB < 3) prev_s[chB] = have_prev ? prev : Pair{1.0, 0.0, 1.0, 0.0};
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < nb * 3; idx += blockDim.x) {
+        const int bl = idx / 3;
+        const int ch = idx % 3;
+        int j = bl;
+        while (j >= 0 && !(cand[j][ch].keep == 1 || cand[j][ch].ok_raw)) --j;
+        const Pair out = j < 0 ? prev_s[ch] : (cand[j][ch].keep == 1 ? cand[j][ch].masked
+                                                                       : cand[j][ch].raw);
+        const int b = b0 + bl;
+        const int64_t ob = (static_cast<int64_t>(b) * p.S + s) * 2 * K3 + k * 3 + ch;
+        p.gain[ob] = out.gl;
+        p.offset[ob] = out.ol;
+        p.gain[ob + K3] = out.gr;
+        p.offset[ob + K3] = out.orr;
+        if (p.fit_ok != nullptr && ch == 0)
+          p.fit_ok[(static_cast<int64_t>(b) * p.S + s) * p.K + k] = cand[bl][0].ok_raw ? 1 : 0;
+        if (bl == nb - 1) next_s[ch] = out;  // carried into the next chunk
+      }
+      __syncthreads();
+      if (chB < 3) {
+        prev = next_s[chB];
+        have_prev = true;
+      }
+    }
     // ---- phase B: the tick loop (exposure.py:295-342)
-    if (chB < 3) {
+    if (!parallel && chB < 3) {
       for (int bl = 0; bl < nb; ++bl) {
         const int b = b0 + bl;
         const Cand &c = cand[bl][chB];

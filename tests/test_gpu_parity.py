@@ -929,3 +929,31 @@ def test_pipelined_submit_matches_sequential_correct(mode):
         np.testing.assert_array_equal(g_.offset.cpu().numpy(), w_.offset.cpu().numpy())
         np.testing.assert_array_equal(g_.stats.cpu().numpy(), w_.stats.cpu().numpy())
     _lib.call("camx_comm_destroy", h.value)
+
+
+@pytest.mark.parametrize("with_prev", [False, True])
+def test_unfittable_batch_carries_previous_maps(with_prev):
+    """STANDARD with every block unfittable (min_band_pixels above the band
+    area): resolve() (exposure.py:275-293) returns the previous maps for
+    every frame - identity without them - through the parallel tick path."""
+    N, H, W, B, K = 3, 64, 96, 5, 4
+    frames = np.stack([O.synthetic_array(N, H, W, seed=5, objects=1, frame_index=t)
+                       for t in range(B)])
+    cfg = xp.ExposureConfig(band_width=16, blocks=K, min_band_pixels=10 ** 9)
+    ac = ArrayCorrector(N, H, W, cfg, xp.ExposureMode.STANDARD)
+    pm = None
+    if with_prev:
+        rng = np.random.default_rng(9)
+        pg = rng.uniform(0.7, 1.3, (N - 1, 2, K, 3))
+        po = rng.uniform(-9, 9, (N - 1, 2, K, 3))
+        ac.set_prev_maps([xp.SeamMaps(xp.ExposureMap((s, s + 1), xp.Side.LEFT, 16, pg[s, 0], po[s, 0]),
+                                      xp.ExposureMap((s, s + 1), xp.Side.RIGHT, 16, pg[s, 1], po[s, 1]))
+                          for s in range(N - 1)])
+        pm = (pg, po)
+    res = ac.correct(torch.from_numpy(frames).cuda())
+    want, wg, wo, wok = O.correct_sequence(frames, pm, O.STANDARD,
+                                           O.Cfg(band_width=16, blocks=K, min_band_pixels=10 ** 9))
+    assert not wok.any()
+    np.testing.assert_array_equal(res.gain.cpu().numpy(), wg)
+    np.testing.assert_array_equal(res.offset.cpu().numpy(), wo)
+    np.testing.assert_array_equal(res.out.cpu().numpy(), want)
