@@ -21,7 +21,6 @@
 //   min(., 255) on the 16-bit lanes (VIMNMX.U16x2), then byte pack.
 // Since clamp bounds are integers, clip(rint(y)) == rint(clip(y)).
 #include <cstdlib>
-#include <mutex>
 
 #include "camx_resize.cuh"
 
@@ -873,7 +872,7 @@ namespace camx {
 // K1 (+ K2 as a programmatic dependent) for a whole batch.
 // K1 over a batch: n_batch frames of `per_frame` images, frames 1.. against
 // their predecessors and frame 0 against prev_frame when `removal`.
-static int band_stats_frames(const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch,
+int band_stats_frames(const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch,
                              int32_t per_frame, int32_t height, int32_t width, int32_t band_width,
                              int32_t blocks, int32_t t_diff, bool removal, camx_band_stat *stats,
                              uint32_t *hist, void *stream) {
@@ -993,235 +992,19 @@ extern "C" int camx_correct_batch(const uint8_t *images, uint8_t *out, const uin
 }
 
 namespace camx {
-int comm_all_gather(const void *send, void *recv, size_t bytes, void *comm, cudaStream_t s);
-}
-constexpr int kMaxShardChunks = 8;
-
-// Library-owned side stream + events of the sharded pipelines (one set per
-// device; capture-safe: only event record / wait).  ev[0] fork, ev[1..]
-// per chunk, step[0] the join of camx_correct_batch_sharded_step.
-struct SidePipe {
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev[kMaxShardChunks + 1] = {};
-  cudaEvent_t step[1] = {};
-};
-static std::mutex g_pipe_mu;
-static int side_pipe(SidePipe *&out) {
-  static SidePipe pipes[64];
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return static_cast<int>(e);
-  if (dev < 0 || dev >= 64) return CAMX_EINVAL;
-  std::lock_guard<std::mutex> lock(g_pipe_mu);
-  SidePipe &sp = pipes[dev];
-  if (sp.side == nullptr) {
-    e = cudaStreamCreateWithFlags(&sp.side, cudaStreamNonBlocking);
-    for (int i = 0; e == cudaSuccess && i < kMaxShardChunks + 1; ++i)
-      e = cudaEventCreateWithFlags(&sp.ev[i], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sp.step[0], cudaEventDisableTiming);
-    if (e != cudaSuccess) return static_cast<int>(e);
-  }
-  out = &sp;
-  return CAMX_OK;
-}
-
-// Geometry of one rank's shard, validated against camera_partition.
-struct ShardGeom {
-  int n_cams, cam_begin, cam_count, world, rank, cmax, wrap, S, H, W, bw, t_diff;
-  bool removal;
-  int64_t frame_bytes;  // one frame of this rank's cameras
-  size_t rec;           // one camera-frame of records (2 sides x K)
-  int64_t map_frame;    // one frame of maps (S x 2 x K x 3 doubles)
-};
-static int shard_geom(ShardGeom &g, int32_t n_cams, int32_t cam_begin, int32_t cam_count,
-                      int32_t world, int32_t wrap, int32_t height, int32_t width,
-                      int32_t band_width, int32_t t_diff, const camx_solve_config *cfg,
-                      const double *prev_gain, const double *prev_offset, void *comm) {
-  if (cfg == nullptr || n_cams < 2 || world < 1 || world > n_cams) return CAMX_EINVAL;
-  if (cfg->blocks < 1 || cfg->blocks > height) return CAMX_EINVAL;
-  if (cfg->mode < CAMX_MODE_STANDARD || cfg->mode > CAMX_MODE_SMOOTHING) return CAMX_EINVAL;
-  if (cfg->have_prev_maps && (prev_gain == nullptr || prev_offset == nullptr)) return CAMX_EINVAL;
-  // this rank's group must be one of camera_partition(n_cams, world)
-  const int q = n_cams / world, r = n_cams % world;
-  g.rank = -1;
-  for (int k = 0; k < world; ++k)
-    if (k * q + (k < r ? k : r) == cam_begin && q + (k < r ? 1 : 0) == cam_count) g.rank = k;
-  if (g.rank < 0) return CAMX_EINVAL;
-  if (world > 1 && comm == nullptr) return CAMX_EINVAL;
-  g.n_cams = n_cams;
-  g.cam_begin = cam_begin;
-  g.cam_count = cam_count;
-  g.world = world;
-  g.cmax = (n_cams + world - 1) / world;
-  g.wrap = wrap;
-  g.S = wrap ? n_cams : n_cams - 1;
-  g.H = height;
-  g.W = width;
-  g.bw = band_width;
-  g.t_diff = t_diff;
-  g.removal = cfg->mode == CAMX_MODE_OBJECT_REMOVAL;
-  g.frame_bytes = static_cast<int64_t>(height) * width * 3 * cam_count;
-  g.rec = sizeof(camx_band_stat) * 2 * cfg->blocks;
-  g.map_frame = static_cast<int64_t>(g.S) * 2 * cfg->blocks * 3;
-  return CAMX_OK;
-}
-
-// Front half for nb frames on stream s: K1 on this rank's cameras -> pad +
-// ncclAllGather -> K2 (all seams, rank-major records).  stats_local is
-// dense [nb][cam_count], stats_all [world][nb][cmax].
-static int shard_front(const ShardGeom &g, const uint8_t *images, const uint8_t *prev_frame,
-                       int nb, const camx_solve_config *cfg, const double *prev_gain,
-                       const double *prev_offset, camx_band_stat *stats_local,
-                       camx_band_stat *stats_all, uint32_t *hist, double *gain, double *offset,
-                       uint8_t *fit_ok, void *comm, cudaStream_t s) {
-  int st = band_stats_frames(images, prev_frame, nb, g.cam_count, g.H, g.W, g.bw, cfg->blocks,
-                             g.t_diff, g.removal, stats_local, hist, s);
-  if (st != CAMX_OK) return st;
-  const size_t block = g.rec * g.cmax * nb;  // one rank's block
-  uint8_t *sa = reinterpret_cast<uint8_t *>(stats_all);
-  if (g.world > 1 || comm != nullptr) {  // (a one-rank comm still goes through NCCL)
-    const void *send = stats_local;
-    if (g.cam_count < g.cmax) {  // pad each frame to cmax cameras, in this rank's slot
-      uint8_t *slot = sa + block * g.rank;
-      cudaError_t e = cudaMemcpy2DAsync(slot, g.rec * g.cmax, stats_local, g.rec * g.cam_count,
-                                        g.rec * g.cam_count, nb, cudaMemcpyDeviceToDevice, s);
-      if (e != cudaSuccess) return static_cast<int>(e);
-      send = slot;  // in-place all-gather
-    }
-    st = comm_all_gather(send, sa, block, comm, s);
-    if (st != CAMX_OK) return st;
-  } else if (reinterpret_cast<void *>(sa) != reinterpret_cast<void *>(stats_local)) {
-    cudaError_t e = cudaMemcpyAsync(sa, stats_local, block, cudaMemcpyDeviceToDevice, s);
-    if (e != cudaSuccess) return static_cast<int>(e);
-  }
-  return launch_seam_solve(stats_all, nb, g.n_cams, g.wrap, cfg, prev_gain, prev_offset, gain,
-                           offset, fit_ok, s, false, g.world, g.cmax);
-}
-
-// Back half: K3 on this rank's cameras of nb frames.
-static int shard_apply(const ShardGeom &g, const uint8_t *images, uint8_t *out, int nb, int blocks,
+// K3 over this rank's cameras of nb frames (camx_shard.cu).
+int apply_camera_group(const uint8_t *images, uint8_t *out, int nb, int cam_begin, int cam_count,
+                       int n_cams, int wrap, int height, int width, int blocks,
                        const double *gain, const double *offset, bool pdl, cudaStream_t s) {
-  ApplyParams p = array_params(images, out, nb, g.cam_count, g.wrap, g.H, g.W, blocks, gain,
+  ApplyParams p = array_params(images, out, nb, cam_count, wrap, height, width, blocks, gain,
                                offset);
-  p.cam_begin = g.cam_begin;
-  p.n_cams = g.n_cams;
-  p.S = g.S;
+  p.cam_begin = cam_begin;
+  p.n_cams = n_cams;
+  p.S = wrap ? n_cams : n_cams - 1;
   p.pdl = pdl ? 1 : 0;
   return launch_apply(p, s);
 }
-
-extern "C" int camx_correct_batch_sharded(
-    const uint8_t *images, uint8_t *out, const uint8_t *prev_frame, int32_t n_batch,
-    int32_t n_cams, int32_t cam_begin, int32_t cam_count, int32_t world, int32_t wrap,
-    int32_t height, int32_t width, int32_t band_width, int32_t t_diff, const camx_solve_config *cfg,
-    const double *prev_gain, const double *prev_offset, camx_band_stat *stats_local,
-    camx_band_stat *stats_all, uint32_t *hist, double *gain_out, double *offset_out,
-    uint8_t *fit_ok_out, int32_t n_chunks, void *comm, void *stream) {
-  if (!images || !out || !stats_local || !stats_all || !gain_out || !offset_out || !fit_ok_out)
-    return CAMX_EINVAL;
-  if (n_batch < 1 || n_chunks < 1 || n_chunks > kMaxShardChunks) return CAMX_EINVAL;
-  ShardGeom g;
-  int st = shard_geom(g, n_cams, cam_begin, cam_count, world, wrap, height, width, band_width,
-                      t_diff, cfg, prev_gain, prev_offset, comm);
-  if (st != CAMX_OK) return st;
-  n_chunks = n_chunks > n_batch ? n_batch : n_chunks;
-  cudaStream_t main = as_stream(stream);
-  SidePipe *sp = nullptr;
-  cudaStream_t side = main;
-  if (n_chunks > 1) {
-    st = side_pipe(sp);
-    if (st != CAMX_OK) return st;
-    side = sp->side;
-    cudaError_t e = cudaEventRecord(sp->ev[0], main);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, sp->ev[0], 0);
-    if (e != cudaSuccess) return static_cast<int>(e);
-  }
-  // Chunk c: front half on `side`, K3 on `main`; the front half of chunk c+1
-  // overlaps K3 of chunk c.  The tick-loop state flows between chunks
-  // through gain_out (previous frame's maps) and the raw frames.
-  for (int c = 0; c < n_chunks; ++c) {
-    const int lo = static_cast<int>(static_cast<int64_t>(n_batch) * c / n_chunks);
-    const int hi = static_cast<int>(static_cast<int64_t>(n_batch) * (c + 1) / n_chunks);
-    const int nb = hi - lo;
-    if (nb <= 0) continue;
-    const uint8_t *img = images + lo * g.frame_bytes;
-    camx_solve_config cc = *cfg;
-    const double *pg = prev_gain, *po = prev_offset;
-    if (lo > 0) {  // the previous chunk's last frame seeds this one
-      cc.have_prev_maps = 1;
-      cc.have_prev_frames = g.removal ? 1 : cc.have_prev_frames;
-      pg = gain_out + (lo - 1) * g.map_frame;
-      po = offset_out + (lo - 1) * g.map_frame;
-    }
-    st = shard_front(g, img, lo == 0 ? prev_frame : img - g.frame_bytes, nb, &cc, pg, po,
-                     stats_local + static_cast<int64_t>(lo) * cam_count * 2 * cfg->blocks,
-                     reinterpret_cast<camx_band_stat *>(reinterpret_cast<uint8_t *>(stats_all) +
-                                                        g.rec * g.cmax * world * lo),
-                     hist == nullptr ? nullptr
-                                     : hist + static_cast<int64_t>(lo) * cam_count * 2 *
-                                                  cfg->blocks * 768,
-                     gain_out + lo * g.map_frame, offset_out + lo * g.map_frame,
-                     fit_ok_out + static_cast<int64_t>(lo) * g.S * cfg->blocks, comm, side);
-    if (st != CAMX_OK) return st;
-    if (side != main) {
-      cudaError_t e = cudaEventRecord(sp->ev[1 + c], side);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(main, sp->ev[1 + c], 0);
-      if (e != cudaSuccess) return static_cast<int>(e);
-    }
-    st = shard_apply(g, img, out + lo * g.frame_bytes, nb, cfg->blocks,
-                     gain_out + lo * g.map_frame, offset_out + lo * g.map_frame, side == main,
-                     main);
-    if (st != CAMX_OK) return st;
-  }
-  return CAMX_OK;
-}
-
-extern "C" int camx_correct_batch_sharded_step(
-    const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch, int32_t n_cams,
-    int32_t cam_begin, int32_t cam_count, int32_t world, int32_t wrap, int32_t height,
-    int32_t width, int32_t band_width, int32_t t_diff, const camx_solve_config *cfg,
-    const double *prev_gain, const double *prev_offset, camx_band_stat *stats_local,
-    camx_band_stat *stats_all, uint32_t *hist, double *gain_out, double *offset_out,
-    uint8_t *fit_ok_out, const uint8_t *apply_images, uint8_t *apply_out, int32_t apply_batch,
-    const double *apply_gain, const double *apply_offset, void *comm, void *stream) {
-  ShardGeom g;
-  int st = shard_geom(g, n_cams, cam_begin, cam_count, world, wrap, height, width, band_width,
-                      t_diff, cfg, prev_gain, prev_offset, comm);
-  if (st != CAMX_OK) return st;
-  const bool front = images != nullptr && n_batch > 0;
-  const bool back = apply_images != nullptr && apply_batch > 0;
-  if (front && (!stats_local || !stats_all || !gain_out || !offset_out || !fit_ok_out))
-    return CAMX_EINVAL;
-  if (back && (!apply_out || !apply_gain || !apply_offset)) return CAMX_EINVAL;
-  SidePipe *sp = nullptr;
-  st = side_pipe(sp);
-  if (st != CAMX_OK) return st;
-  cudaStream_t main = as_stream(stream);
-  cudaError_t e = cudaSuccess;
-  if (front) {
-    // the side stream sees everything issued on main so far: the frames,
-    // and K3 of two steps back (the last reader of the maps buffer K2 fills)
-    e = cudaEventRecord(sp->ev[0], main);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(sp->side, sp->ev[0], 0);
-    if (e != cudaSuccess) return static_cast<int>(e);
-    st = shard_front(g, images, prev_frame, n_batch, cfg, prev_gain, prev_offset, stats_local,
-                     stats_all, hist, gain_out, offset_out, fit_ok_out, comm, sp->side);
-    if (st != CAMX_OK) return st;
-  }
-  if (back) {  // K3 of the previous batch: its front half is already joined into main
-    st = shard_apply(g, apply_images, apply_out, apply_batch, cfg->blocks, apply_gain,
-                     apply_offset, false, main);
-    if (st != CAMX_OK) return st;
-  }
-  if (front) {
-    // join: work the caller issues on main after this call (refilling the
-    // frames, the next step's K3) runs after this front half
-    e = cudaEventRecord(sp->step[0], sp->side);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(main, sp->step[0], 0);
-    if (e != cudaSuccess) return static_cast<int>(e);
-  }
-  return CAMX_OK;
-}
+}  // namespace camx
 
 extern "C" int camx_correct_batch_tiles(
     const uint8_t *images, uint8_t *out, const uint8_t *prev_frame, int32_t n_batch,
