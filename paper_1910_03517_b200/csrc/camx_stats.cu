@@ -24,6 +24,8 @@
 // into per-lane registers by a SWAR (2 x 16-bit) column sum.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "camx_solve.cuh"
 
 namespace camx {
@@ -78,6 +80,11 @@ __device__ __noinline__ void fused_solve_tail(const StatsParams &p, int64_t unit
 constexpr int kStatsWarps = 4;  // warps per (image, side, block) unit = per CTA
 constexpr int kCounterWords = 3 * 64 * 32;  // per warp: 3 ch x 64 bin-quads x 32 lanes
 constexpr int kQuadBatch = 8;
+// Histograms: per-warp [3][256] uint32 bins in shared memory with atomics
+// (a unit is only 3072 pixels, so the per-lane private byte counters of the
+// alternative - conflict-free increments, but a 768-word flush and re-zero
+// per lane per unit - cost ~8x more; tools/k1_probe.py).
+constexpr bool kHistAtomic = true;
 // dp4a byte selectors of channel c in word k of a 12-byte pixel quad
 // (bytes r g b r | g b r g | b r g b)
 //   r: w0 b0,b3  w1 b2  w2 b1;  g: w0 b1  w1 b0,b3  w2 b2;  b: w0 b2  w1 b1  w2 b0,b3
@@ -115,7 +122,9 @@ __device__ __forceinline__ void add_pixel(Acc &a, uint32_t *cnt, int lane, uint3
     a.nvalid += 1;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      if (HIST) {
+      if (HIST && kHistAtomic) {
+        atomicAdd(cnt + c * 256 + v[c], 1u);
+      } else if (HIST) {
         uint32_t *wp = cnt + ((c * 64 + (v[c] >> 2)) << 5) + lane;
         *wp += 1u << ((v[c] & 3u) << 3);
       } else {
@@ -197,8 +206,11 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
   const uint8_t *pbase = (MASKMODE == 2) ? p.prev + img * p.img_bytes : nullptr;
   const uint8_t *mbase = (MASKMODE == 1) ? p.mask + img * p.mask_bytes : nullptr;
 
-  uint32_t *cnt = HIST ? smem + warp * kCounterWords : nullptr;
-  if (HIST) {
+  uint32_t *cnt = HIST ? smem + warp * (kHistAtomic ? 768 : kCounterWords) : nullptr;
+  if (HIST && kHistAtomic) {
+    for (int w = lane; w < 768; w += 32) cnt[w] = 0u;
+    __syncwarp();
+  } else if (HIST) {
     for (int w = 0; w < 3 * 64; ++w) cnt[(w << 5) + lane] = 0u;
     __syncwarp();
   }
@@ -312,7 +324,7 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
           add_pixel<HIST>(a, cnt, lane, (q[2] >> 8) & 0xFF, (q[2] >> 16) & 0xFF, q[2] >> 24, ex & 8);
         }
       }
-      if (HIST) {
+      if (HIST && !kHistAtomic) {
         since_flush += 4 * kQuadBatch;
         if (since_flush > 255 - 4 * kQuadBatch) {  // warp-uniform
           flush_counters(cnt, lane, bins);
@@ -346,7 +358,7 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
 #pragma unroll
       for (int u = 0; u < kQuadBatch; ++u)
         if (live[u]) add_pixel<HIST>(a, cnt, lane, v[u][0], v[u][1], v[u][2], ex[u]);
-      if (HIST) {
+      if (HIST && !kHistAtomic) {
         since_flush += kQuadBatch;
         if (since_flush > 255 - kQuadBatch) {
           flush_counters(cnt, lane, bins);
@@ -357,18 +369,20 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
   }
 
   if (HIST) {
-    if (since_flush > 0) flush_counters(cnt, lane, bins);
-    // combine the 4 warps' bins: stage them in (now unused) counter memory
-    __syncthreads();
     uint32_t *stage = smem;  // [warp][3][256]
+    if (!kHistAtomic) {
+      if (since_flush > 0) flush_counters(cnt, lane, bins);
+      // combine the 4 warps' bins: stage them in (now unused) counter memory
+      __syncthreads();
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      reinterpret_cast<uint4 *>(stage + (warp * 3 + c) * 256)[lane] =
-          make_uint4(bins[c][0], bins[c][1], bins[c][2], bins[c][3]);
-      reinterpret_cast<uint4 *>(stage + (warp * 3 + c) * 256 + 128)[lane] =
-          make_uint4(bins[c][4], bins[c][5], bins[c][6], bins[c][7]);
+      for (int c = 0; c < 3; ++c) {
+        reinterpret_cast<uint4 *>(stage + (warp * 3 + c) * 256)[lane] =
+            make_uint4(bins[c][0], bins[c][1], bins[c][2], bins[c][3]);
+        reinterpret_cast<uint4 *>(stage + (warp * 3 + c) * 256 + 128)[lane] =
+            make_uint4(bins[c][4], bins[c][5], bins[c][6], bins[c][7]);
+      }
     }
-    __syncthreads();
+    __syncthreads();  // every warp's bins complete
     // thread t owns bins t, t+128, ... of the 768 (channel, bin) pairs
 #pragma unroll
     for (int c = 0; c < 3; ++c) a.val_s[c] = a.val_q[c] = 0;
@@ -454,12 +468,20 @@ __global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const Stat
 template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
 static void launch_stats(const StatsParams &p, cudaStream_t s) {
   const int warps = kStatsWarps;
-  const size_t smem = HIST ? static_cast<size_t>(warps) * kCounterWords * sizeof(uint32_t) : 0;
+  const size_t smem = HIST ? static_cast<size_t>(warps) * (kHistAtomic ? 768 : kCounterWords) *
+                                 sizeof(uint32_t)
+                           : 0;
   if (HIST) {
     cudaFuncSetAttribute(band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   }
-  const int per_sm = HIST ? 2 : 8;
+  static const int env_per_sm = [] {  // experiment hook
+    const char *e = getenv("CAMX_K1_PER_SM");
+    return e != nullptr ? atoi(e) : 0;
+  }();
+  // 32 CTAs per SM for the plain path (8 resident): units are scheduled
+  // dynamically, ~6% faster than a one-wave persistent grid (tools/k1_probe.py)
+  const int per_sm = env_per_sm > 0 ? env_per_sm : (HIST && !kHistAtomic ? 2 : 32);
   const int64_t grid = std::min<int64_t>(p.n_units, static_cast<int64_t>(sm_count()) * per_sm);
   band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>
       <<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(p);
