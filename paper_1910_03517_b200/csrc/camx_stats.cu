@@ -85,6 +85,10 @@ constexpr int kQuadBatch = 8;
 // alternative - conflict-free increments, but a 768-word flush and re-zero
 // per lane per unit - cost ~8x more; tools/k1_probe.py).
 constexpr bool kHistAtomic = true;
+#ifndef CAMX_HIST_COPIES
+#define CAMX_HIST_COPIES 1
+#endif
+constexpr int kHistCopies = CAMX_HIST_COPIES;  // per-warp bin copies (by lane)
 // dp4a byte selectors of channel c in word k of a 12-byte pixel quad
 // (bytes r g b r | g b r g | b r g b)
 //   r: w0 b0,b3  w1 b2  w2 b1;  g: w0 b1  w1 b0,b3  w2 b2;  b: w0 b2  w1 b1  w2 b0,b3
@@ -123,7 +127,7 @@ __device__ __forceinline__ void add_pixel(Acc &a, uint32_t *cnt, int lane, uint3
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       if (HIST && kHistAtomic) {
-        atomicAdd(cnt + c * 256 + v[c], 1u);
+        atomicAdd(cnt + (lane & (kHistCopies - 1)) * 768 + c * 256 + v[c], 1u);
       } else if (HIST) {
         uint32_t *wp = cnt + ((c * 64 + (v[c] >> 2)) << 5) + lane;
         *wp += 1u << ((v[c] & 3u) << 3);
@@ -206,9 +210,9 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
   const uint8_t *pbase = (MASKMODE == 2) ? p.prev + img * p.img_bytes : nullptr;
   const uint8_t *mbase = (MASKMODE == 1) ? p.mask + img * p.mask_bytes : nullptr;
 
-  uint32_t *cnt = HIST ? smem + warp * (kHistAtomic ? 768 : kCounterWords) : nullptr;
+  uint32_t *cnt = HIST ? smem + warp * (kHistAtomic ? 768 * kHistCopies : kCounterWords) : nullptr;
   if (HIST && kHistAtomic) {
-    for (int w = lane; w < 768; w += 32) cnt[w] = 0u;
+    for (int w = lane; w < 768 * kHistCopies; w += 32) cnt[w] = 0u;
     __syncwarp();
   } else if (HIST) {
     for (int w = 0; w < 3 * 64; ++w) cnt[(w << 5) + lane] = 0u;
@@ -389,7 +393,8 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
     for (int e = threadIdx.x; e < 768; e += kStatsWarps * 32) {
       uint32_t tot = 0;
 #pragma unroll
-      for (int w2 = 0; w2 < kStatsWarps; ++w2) tot += stage[w2 * 768 + e];
+      for (int w2 = 0; w2 < kStatsWarps * (kHistAtomic ? kHistCopies : 1); ++w2)
+        tot += stage[w2 * 768 + e];
       const int c = e >> 8;
       const uint64_t bin = e & 255;
       if (p.hist != nullptr) p.hist[unit * 768 + e] = tot;
@@ -468,7 +473,8 @@ __global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const Stat
 template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
 static void launch_stats(const StatsParams &p, cudaStream_t s) {
   const int warps = kStatsWarps;
-  const size_t smem = HIST ? static_cast<size_t>(warps) * (kHistAtomic ? 768 : kCounterWords) *
+  const size_t smem = HIST ? static_cast<size_t>(warps) *
+                                 (kHistAtomic ? 768 * kHistCopies : kCounterWords) *
                                  sizeof(uint32_t)
                            : 0;
   if (HIST) {
