@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-batch", type=int, default=8)
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--no-hist", action="store_true",
+                    help="skip the seam-band histograms (K1 means/moments only)")
     return ap.parse_args()
 
 
@@ -261,10 +263,10 @@ def run_camx(args):
     cfg = ExposureConfig()
     wrap = name == "config4"
     if world > 1:
-        ac = sharded_corrector(n_cams, H, W, cfg, mode, wrap=wrap)
+        ac = sharded_corrector(n_cams, H, W, cfg, mode, wrap=wrap, histograms=not args.no_hist)
         begin, count = camera_partition(n_cams, world)[rank]
     else:
-        ac = ArrayCorrector(n_cams, H, W, cfg, mode, wrap=wrap)
+        ac = ArrayCorrector(n_cams, H, W, cfg, mode, wrap=wrap, histograms=not args.no_hist)
         begin, count = 0, n_cams
     full = synthetic_batch(B, n_cams, H, W, seed=100)
     frames = full[:, begin:begin + count].contiguous()
@@ -493,9 +495,11 @@ def run_camx(args):
             "data": "synthetic (on-device panorama + per-camera affine distortion + moving objects)",
             "array_frames_per_sec": round(afps, 2),
             "config": {"workload": f"{name}: {desc}", "batch": B, "mode": mode.value,
+                       "histograms": not args.no_hist,
                        "tiles_per_step": (tiles_buf.shape[0] if tiles_mode else 0),
                        "cameras_per_gpu": count, "frame": f"{W}x{H}",
-                       "step": "K1 band stats + K2 seam solve + K3 apply per array-frame",
+                       "step": ("K1 band stats" + ("" if args.no_hist else " + histograms") +
+                                " + K2 seam solve + K3 apply per array-frame"),
                        "l2": "inputs larger than L2 (batch >> 126 MB)",
                        "parallelism": f"camera-shard{world}" if world > 1 else "single",
                        "launch": ("cuda-graph replay" if use_graph else
