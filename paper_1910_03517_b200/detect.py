@@ -3,13 +3,18 @@ detect.py:60-72) and the batched tile crop/resize (the crop of
 ExternalDetector.detect, detect.py:297-300, plus the builder-defined
 resize to the detector input size) on the GPU (K5).
 
-The detectors themselves (nms, Oracle/Blob/External detectors) consume
-tiles and are out of scope ("tile consumer").
+Tile consumers: nms, the motion-blob detector (GPU connected
+components) and the external-detector wire adapter (`ExternalDetector`,
+plus `detect_tiles` feeding it whole device tile batches).  The
+ground-truth OracleDetector projects the scene generator's 3-D objects
+(world3d) and stays out of scope.
 """
 
 from __future__ import annotations
 
+import abc
 import enum
+import socket
 import threading
 from dataclasses import dataclass, replace
 
@@ -19,8 +24,8 @@ from . import _dev, _lib
 from .core import BBox, Category, Mosaic, iou
 
 __all__ = ["DetectorWindow", "crop_window", "tiles", "encode_ppm", "encode_ppm_tiles",
-           "detect_requests", "Detection", "DetectionSource", "BlobDetector", "nms",
-           "TOL_DETECT", "TOL_NMS"]
+           "detect_requests", "Detection", "DetectionSource", "Detector", "BlobDetector",
+           "ExternalDetector", "nms", "TOL_DETECT", "TOL_NMS"]
 
 
 @dataclass(frozen=True)
@@ -218,7 +223,15 @@ def blob_components(mask, window: DetectorWindow, n_cams: int = 1, max_comp: int
     return _dev.to_host(comp[:count])
 
 
-class BlobDetector:
+class Detector(abc.ABC):
+    """Detections in one window of one mosaic tick (detect.py:117-129)."""
+
+    @abc.abstractmethod
+    def detect(self, window: DetectorWindow, mosaic: Mosaic) -> list[Detection]:
+        ...
+
+
+class BlobDetector(Detector):
     """Motion-blob detector (detect.py:192-249): connected components of the
     frame-difference mask of consecutive mosaics, one detection per
     component of at least `min_area` on-pixels (counted over its box, as
@@ -281,3 +294,123 @@ class BlobDetector:
             dets.append(Detection(self.category, box, p, mosaic.frame_index,
                                   DetectionSource.BLOB))
         return _finalize(dets, mosaic.width, mosaic.height, self.tol_detect, self.tol_nms)
+
+
+class ExternalDetector(Detector):
+    """Adapter to an external detector process over a local socket, the
+    reference's wire protocol (detect.py:252-349): per request
+      -> "DETECT v1 <x> <y> <size> <w> <h>\n" + P6 bytes of the crop
+      <- "OK <n>\n" + n lines "<category> <x> <y> <w> <h> <p>" (crop-local
+         coordinates) or "ERR <message>\n".
+    A missed deadline or a broken connection gives an empty result and sets
+    `degraded` (the pipeline is never blocked).  `detect` sends the window's
+    crop of a host mosaic exactly as the reference; `detect_tiles` feeds a
+    whole device tile batch (K5 crops / resizes: one D2H copy, then one
+    request per tile) and maps the replies back to mosaic coordinates."""
+
+    def __init__(self, address, *, deadline_s: float = 0.1,
+                 tol_detect: float = TOL_DETECT, tol_nms: float = TOL_NMS):
+        self.address = address
+        self.deadline_s = deadline_s
+        self.tol_detect = tol_detect
+        self.tol_nms = tol_nms
+        self.degraded = False
+        self._sock = None
+        self._lock = threading.Lock()
+
+    def _connect(self):
+        fam = socket.AF_UNIX if isinstance(self.address, str) else socket.AF_INET
+        s = socket.socket(fam, socket.SOCK_STREAM)
+        s.settimeout(self.deadline_s)
+        s.connect(self.address)
+        return s
+
+    def close(self) -> None:
+        with self._lock:
+            self._drop()
+
+    def _drop(self) -> None:
+        if self._sock is not None:
+            try:
+                self._sock.close()
+            finally:
+                self._sock = None
+
+    @staticmethod
+    def _line(sock) -> str:
+        buf = bytearray()
+        while True:
+            c = sock.recv(1)
+            if not c:
+                raise OSError("connection closed")
+            if c == b"\n":
+                return buf.decode()
+            buf += c
+
+    def _exchange(self, payload: bytes):
+        """One request/reply; None on a missed deadline / broken peer."""
+        with self._lock:
+            try:
+                if self._sock is None:
+                    self._sock = self._connect()
+                self._sock.settimeout(self.deadline_s)
+                self._sock.sendall(payload)
+                status = self._line(self._sock)
+                if status.startswith("ERR"):
+                    raise ValueError(status)
+                if not status.startswith("OK "):
+                    raise ValueError(f"malformed reply {status!r}")
+                rows = []
+                for _ in range(int(status.split()[1])):
+                    f = self._line(self._sock).split()
+                    rows.append((f[0], *(float(v) for v in f[1:6])))
+            except (OSError, ValueError):
+                self._drop()
+                self.degraded = True
+                return None
+        self.degraded = False
+        return rows
+
+    def _to_dets(self, rows, ox, oy, scale, frame_index):
+        dets = []
+        for cat_s, bx, by, bw, bh, p in rows:
+            try:
+                cat = Category(cat_s)
+            except ValueError:
+                continue
+            box = BBox(ox + bx * scale, oy + by * scale, bw * scale, bh * scale)
+            dets.append(Detection(cat, box, min(max(p, 0.0), 1.0), frame_index,
+                                  DetectionSource.EXTERNAL))
+        return dets
+
+    def detect(self, window: DetectorWindow, mosaic: Mosaic) -> list[Detection]:
+        x0, y0 = max(window.x, 0), max(window.y, 0)
+        x1 = min(window.x + window.size, mosaic.width)
+        y1 = min(window.y + window.size, mosaic.height)
+        crop = np.ascontiguousarray(mosaic.pixels[y0:y1, x0:x1])
+        req = (b"DETECT v1 %d %d %d %d %d\n" % (window.x, window.y, window.size, crop.shape[1],
+                                                crop.shape[0]) + encode_ppm(crop))
+        rows = self._exchange(req)
+        if rows is None:
+            return []
+        return _finalize(self._to_dets(rows, x0, y0, 1.0, mosaic.frame_index), mosaic.width,
+                         mosaic.height, self.tol_detect, self.tol_nms)
+
+    def detect_tiles(self, windows, tile_batch, *, frame_index: int, mosaic_w: int,
+                     mosaic_h: int) -> list[list[Detection]]:
+        """Detections of every window from its K5 tile (T, S', S', 3) - a
+        crop resized to S' (or the exact crop when S' = size).  Reply
+        coordinates are tile-local and scaled by size / S' back to the
+        mosaic; per window: clip, confidence gate and NMS as `detect`."""
+        reqs = detect_requests(windows, tile_batch)
+        out = []
+        for w, req in zip(windows, reqs):
+            x, y, size = (w.x, w.y, w.size) if isinstance(w, DetectorWindow) else w
+            side = int(req.split(b"\n", 1)[0].split()[5])
+            rows = self._exchange(req)
+            if rows is None:
+                out.append([])
+                continue
+            dets = self._to_dets(rows, max(x, 0), max(y, 0), size / side, frame_index)
+            out.append(_finalize(dets, mosaic_w, mosaic_h, self.tol_detect, self.tol_nms))
+        return out
