@@ -957,3 +957,63 @@ def test_unfittable_batch_carries_previous_maps(with_prev):
     np.testing.assert_array_equal(res.gain.cpu().numpy(), wg)
     np.testing.assert_array_equal(res.offset.cpu().numpy(), wo)
     np.testing.assert_array_equal(res.out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("mode,om", [(xp.ExposureMode.STANDARD, O.STANDARD),
+                                     (xp.ExposureMode.OBJECT_REMOVAL, O.OBJECT_REMOVAL)])
+def test_full_size_config2_and_config5_vs_oracle(mode, om):
+    """BASELINE config 2 at full size (8 x 2048x1536, 2 array-frames) through
+    the production path with histograms: gains vs the oracle tick loop,
+    corrected pixels within +-1 LSB (bit-exact expected), histograms of a
+    sample of band blocks bit-exact and every histogram summing to its
+    block's (valid) pixel count; then config 5's fused tiles (36 per frame,
+    960 -> 416) against the oracle crop + resize of the oracle output."""
+    from paper_1910_03517_b200.synth import synthetic_batch
+    N, H, W, B, K = 8, 1536, 2048, 2, 16
+    d = synthetic_batch(B, N, H, W, seed=5)
+    frames = d.cpu().numpy()
+    cfg = xp.ExposureConfig()
+    ac = ArrayCorrector(N, H, W, cfg, mode, histograms=True)
+    res, tiles = ac.correct_and_tile(d, size=960, out_size=416)
+    want_out, wg, wo, wok = O.correct_sequence(frames, None, om, O.Cfg())
+    np.testing.assert_allclose(res.gain.cpu().numpy(), wg, rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    np.testing.assert_allclose(res.offset.cpu().numpy(), wo, rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    np.testing.assert_array_equal(res.fit_ok.cpu().numpy().astype(bool), wok)
+    out = res.out.cpu().numpy()
+    diff = np.abs(out.astype(int) - want_out.astype(int))
+    assert diff.max() <= 1 and (diff > 0).mean() < 1e-6
+    hist = res.hist.cpu().numpy().view(np.uint32)  # (B, N, 2, K, 3, 256)
+    from paper_1910_03517_b200 import _lib
+    stats = res.stats.cpu().numpy().view(_lib.STAT_DTYPE).reshape(B, N, 2, K)
+    assert (hist.sum(-1) == stats["valid"][..., None]).all()  # every block, every channel
+    rng = np.random.default_rng(0)
+    for _ in range(6):
+        b, c, s = int(rng.integers(B)), int(rng.integers(N)), int(rng.integers(2))
+        mask = None
+        if om == O.OBJECT_REMOVAL and b > 0:
+            mask = O.mask_diff(frames[b, c], frames[b - 1, c], 20)
+        side = O.LEFT if s == 0 else O.RIGHT
+        np.testing.assert_array_equal(hist[b, c, s], O.band_histograms(frames[b, c], side, 32, K,
+                                                                       mask))
+    wins = O.sliding_window_plan(N * W, H, 960)
+    assert len(wins) == 36
+    tiles = tiles.cpu().numpy()
+    for i in rng.choice(B * len(wins), 8, replace=False):
+        b, (x, y) = int(i) // len(wins), wins[int(i) % len(wins)]
+        mosaic = np.concatenate(list(out[b]), axis=1)
+        np.testing.assert_array_equal(tiles[i], O.resize_bilinear(O.crop(mosaic, x, y, 960), 416))
+
+
+def test_full_size_config4_wrap_vs_oracle():
+    """BASELINE config 4 at full size: 14 x 3840x2160 with the 13|0 wrap seam,
+    one array-frame: gains and corrected pixels vs the oracle."""
+    from paper_1910_03517_b200.synth import synthetic_batch
+    N, H, W = 14, 2160, 3840
+    d = synthetic_batch(1, N, H, W, seed=9)
+    frames = d.cpu().numpy()
+    ac = ArrayCorrector(N, H, W, xp.ExposureConfig(), wrap=True)
+    res = ac.correct(d)
+    want_out, wg, wo, _ = O.correct_sequence(frames, None, O.STANDARD, O.Cfg(), None, True)
+    np.testing.assert_allclose(res.gain.cpu().numpy(), wg, rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    diff = np.abs(res.out.cpu().numpy().astype(int) - want_out.astype(int))
+    assert diff.max() <= 1 and (diff > 0).mean() < 1e-6
