@@ -78,17 +78,12 @@ __device__ __noinline__ void fused_solve_tail(const StatsParams &p, int64_t unit
 }
 
 constexpr int kStatsWarps = 4;  // warps per (image, side, block) unit = per CTA
-constexpr int kCounterWords = 3 * 64 * 32;  // per warp: 3 ch x 64 bin-quads x 32 lanes
 constexpr int kQuadBatch = 8;
-// Histograms: per-warp [3][256] uint32 bins in shared memory with atomics
-// (a unit is only 3072 pixels, so the per-lane private byte counters of the
-// alternative - conflict-free increments, but a 768-word flush and re-zero
-// per lane per unit - cost ~8x more; tools/k1_probe.py).
-constexpr bool kHistAtomic = true;
-#ifndef CAMX_HIST_COPIES
-#define CAMX_HIST_COPIES 1
-#endif
-constexpr int kHistCopies = CAMX_HIST_COPIES;  // per-warp bin copies (by lane)
+// Histograms: per-warp [3][256] uint32 bins in shared memory, one atomic
+// per (kept pixel, channel).  (A band block is only 3,072 pixels: per-lane
+// private byte counters - conflict-free, but a 768-word flush and re-zero
+// per lane per block - measured ~4x slower; profiles/r01/SUMMARY.md.)
+constexpr int kHistWords = 3 * 256;
 // dp4a byte selectors of channel c in word k of a 12-byte pixel quad
 // (bytes r g b r | g b r g | b r g b)
 //   r: w0 b0,b3  w1 b2  w2 b1;  g: w0 b1  w1 b0,b3  w2 b2;  b: w0 b2  w1 b1  w2 b0,b3
@@ -126,11 +121,8 @@ __device__ __forceinline__ void add_pixel(Acc &a, uint32_t *cnt, int lane, uint3
     a.nvalid += 1;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      if (HIST && kHistAtomic) {
-        atomicAdd(cnt + (lane & (kHistCopies - 1)) * 768 + c * 256 + v[c], 1u);
-      } else if (HIST) {
-        uint32_t *wp = cnt + ((c * 64 + (v[c] >> 2)) << 5) + lane;
-        *wp += 1u << ((v[c] & 3u) << 3);
+      if (HIST) {
+        atomicAdd(cnt + c * 256 + v[c], 1u);
       } else {
         a.val_s[c] += v[c];
         a.val_q[c] += v[c] * v[c];
@@ -139,32 +131,6 @@ __device__ __forceinline__ void add_pixel(Acc &a, uint32_t *cnt, int lane, uint3
   }
 }
 
-// Column sums of the lane counters into this lane's 24 bins (3 channels x
-// bin-quads lane and lane+32), then clear the counters.
-__device__ __forceinline__ void flush_counters(uint32_t *cnt, int lane, uint32_t bins[3][8]) {
-  __syncwarp();
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int w = c * 64 + lane + 32 * h;
-      uint32_t lo = 0, hi = 0;
-#pragma unroll 8
-      for (int l = 0; l < 32; ++l) {
-        const uint32_t x = cnt[(w << 5) + ((l + lane) & 31)];
-        lo += x & 0x00FF00FFu;
-        hi += (x >> 8) & 0x00FF00FFu;
-      }
-      bins[c][4 * h + 0] += lo & 0xFFFFu;
-      bins[c][4 * h + 1] += hi & 0xFFFFu;
-      bins[c][4 * h + 2] += lo >> 16;
-      bins[c][4 * h + 3] += hi >> 16;
-    }
-  }
-  __syncwarp();
-  for (int w = 0; w < 3 * 64; ++w) cnt[(w << 5) + lane] = 0u;
-  __syncwarp();
-}
 
 // Excluded-pixel flags of a quad (bit e set = pixel e excluded).
 template <int MASKMODE>
@@ -210,26 +176,17 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
   const uint8_t *pbase = (MASKMODE == 2) ? p.prev + img * p.img_bytes : nullptr;
   const uint8_t *mbase = (MASKMODE == 1) ? p.mask + img * p.mask_bytes : nullptr;
 
-  uint32_t *cnt = HIST ? smem + warp * (kHistAtomic ? 768 * kHistCopies : kCounterWords) : nullptr;
-  if (HIST && kHistAtomic) {
-    for (int w = lane; w < 768 * kHistCopies; w += 32) cnt[w] = 0u;
-    __syncwarp();
-  } else if (HIST) {
-    for (int w = 0; w < 3 * 64; ++w) cnt[(w << 5) + lane] = 0u;
+  uint32_t *cnt = HIST ? smem + warp * kHistWords : nullptr;
+  if (HIST) {
+    for (int w = lane; w < kHistWords; w += 32) cnt[w] = 0u;
     __syncwarp();
   }
-  uint32_t bins[3][8];
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) bins[c][i] = 0u;
   Acc a;
 #pragma unroll
   for (int c = 0; c < 3; ++c) a.raw_s[c] = a.raw_q[c] = a.val_s[c] = a.val_q[c] = 0;
   a.nvalid = 0;
 
   const int rows = r1 - r0;
-  int since_flush = 0;  // pixels added per lane since the last counter flush
   if (QUAD) {
     const int qpr = p.bw >> 2;
     const int nq = rows * qpr;
@@ -260,11 +217,12 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
         if (MASKMODE == 1)
           mw[u] = __ldg(reinterpret_cast<const uint32_t *>(mbase + static_cast<int64_t>(row) * p.W + col));
       }
-      if (!HIST && MASKMODE != 1) {
+      if (MASKMODE != 1) {
         // Channel sums / sums of squares with dp4a: in a quad the byte
         // positions of each channel are fixed (r g b r | g b r g | b r g b),
         // so constant byte masks select them.  32-bit per batch (<= 32 px
-        // per lane), widened once per batch.
+        // per lane), widened once per batch.  HIST: plus one shared-memory
+        // atomic per kept (pixel, channel) - no per-pixel 64-bit moments.
         uint32_t rs[3] = {0, 0, 0}, rq[3] = {0, 0, 0}, vs[3] = {0, 0, 0}, vq[3] = {0, 0, 0};
         uint32_t nv = 0;
 #pragma unroll
@@ -280,8 +238,21 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
               rq[c] = __dp4a(m, m, rq[c]);
             }
           }
+          uint32_t ex = 0u;
+          if (MASKMODE == 2) ex = quad_exclusion<MASKMODE>(p, w[u], pw[u], mw[u]);
+          if (HIST) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if ((ex >> e) & 1u) continue;
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                const int byte = 3 * e + c;  // compile-time position in the 12-byte quad
+                const uint32_t val = (w[u][byte >> 2] >> ((byte & 3) * 8)) & 0xFFu;
+                atomicAdd(cnt + c * 256 + val, 1u);
+              }
+            }
+          }
           if (MASKMODE == 2) {
-            const uint32_t ex = quad_exclusion<MASKMODE>(p, w[u], pw[u], mw[u]);
             nv += 4 - __popc(ex);
             // keep-masks of the 12 bytes: pixel e kept -> its 3 bytes
             const uint32_t kp = (~ex) & 0xFu;
@@ -328,13 +299,6 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
           add_pixel<HIST>(a, cnt, lane, (q[2] >> 8) & 0xFF, (q[2] >> 16) & 0xFF, q[2] >> 24, ex & 8);
         }
       }
-      if (HIST && !kHistAtomic) {
-        since_flush += 4 * kQuadBatch;
-        if (since_flush > 255 - 4 * kQuadBatch) {  // warp-uniform
-          flush_counters(cnt, lane, bins);
-          since_flush = 0;
-        }
-      }
     }
   } else {
     const int npix = rows * p.bw;
@@ -362,49 +326,34 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
 #pragma unroll
       for (int u = 0; u < kQuadBatch; ++u)
         if (live[u]) add_pixel<HIST>(a, cnt, lane, v[u][0], v[u][1], v[u][2], ex[u]);
-      if (HIST && !kHistAtomic) {
-        since_flush += kQuadBatch;
-        if (since_flush > 255 - kQuadBatch) {
-          flush_counters(cnt, lane, bins);
-          since_flush = 0;
-        }
-      }
     }
   }
 
   if (HIST) {
     uint32_t *stage = smem;  // [warp][3][256]
-    if (!kHistAtomic) {
-      if (since_flush > 0) flush_counters(cnt, lane, bins);
-      // combine the 4 warps' bins: stage them in (now unused) counter memory
-      __syncthreads();
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        reinterpret_cast<uint4 *>(stage + (warp * 3 + c) * 256)[lane] =
-            make_uint4(bins[c][0], bins[c][1], bins[c][2], bins[c][3]);
-        reinterpret_cast<uint4 *>(stage + (warp * 3 + c) * 256 + 128)[lane] =
-            make_uint4(bins[c][4], bins[c][5], bins[c][6], bins[c][7]);
-      }
-    }
     __syncthreads();  // every warp's bins complete
     // thread t owns bins t, t+128, ... of the 768 (channel, bin) pairs
+    if (MASKMODE == 1 || !QUAD) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) a.val_s[c] = a.val_q[c] = 0;
+      for (int c = 0; c < 3; ++c) a.val_s[c] = a.val_q[c] = 0;
+    }
     for (int e = threadIdx.x; e < 768; e += kStatsWarps * 32) {
       uint32_t tot = 0;
 #pragma unroll
-      for (int w2 = 0; w2 < kStatsWarps * (kHistAtomic ? kHistCopies : 1); ++w2)
-        tot += stage[w2 * 768 + e];
+      for (int w2 = 0; w2 < kStatsWarps; ++w2) tot += stage[w2 * kHistWords + e];
       const int c = e >> 8;
       const uint64_t bin = e & 255;
       if (p.hist != nullptr) p.hist[unit * 768 + e] = tot;
       // c is warp-uniform for e in steps of 128 within one channel
-      const uint64_t s1 = bin * tot, s2 = bin * bin * tot;
-      if (c == 0) { a.val_s[0] += s1; a.val_q[0] += s2; }
-      if (c == 1) { a.val_s[1] += s1; a.val_q[1] += s2; }
-      if (c == 2) { a.val_s[2] += s1; a.val_q[2] += s2; }
+      if (MASKMODE == 1 || !QUAD) {  // the dp4a quad path already has the valid sums
+        const uint64_t s1 = bin * tot, s2 = bin * bin * tot;
+        if (c == 0) { a.val_s[0] += s1; a.val_q[0] += s2; }
+        if (c == 1) { a.val_s[1] += s1; a.val_q[1] += s2; }
+        if (c == 2) { a.val_s[2] += s1; a.val_q[2] += s2; }
+      }
     }
-  } else if (MASKMODE == 0) {
+  }
+  if (MASKMODE == 0 && (!HIST || QUAD)) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       a.val_s[c] = a.raw_s[c];
@@ -473,10 +422,7 @@ __global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const Stat
 template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
 static void launch_stats(const StatsParams &p, cudaStream_t s) {
   const int warps = kStatsWarps;
-  const size_t smem = HIST ? static_cast<size_t>(warps) *
-                                 (kHistAtomic ? 768 * kHistCopies : kCounterWords) *
-                                 sizeof(uint32_t)
-                           : 0;
+  const size_t smem = HIST ? static_cast<size_t>(warps) * kHistWords * sizeof(uint32_t) : 0;
   if (HIST) {
     cudaFuncSetAttribute(band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -487,7 +433,7 @@ static void launch_stats(const StatsParams &p, cudaStream_t s) {
   }();
   // 32 CTAs per SM for the plain path (8 resident): units are scheduled
   // dynamically, ~6% faster than a one-wave persistent grid (tools/k1_probe.py)
-  const int per_sm = env_per_sm > 0 ? env_per_sm : (HIST && !kHistAtomic ? 2 : 32);
+  const int per_sm = env_per_sm > 0 ? env_per_sm : 32;
   const int64_t grid = std::min<int64_t>(p.n_units, static_cast<int64_t>(sm_count()) * per_sm);
   band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>
       <<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(p);
