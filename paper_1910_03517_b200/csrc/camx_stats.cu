@@ -78,7 +78,13 @@ __device__ __noinline__ void fused_solve_tail(const StatsParams &p, int64_t unit
 }
 
 constexpr int kStatsWarps = 4;  // warps per (image, side, block) unit = per CTA
-constexpr int kQuadBatch = 8;
+#ifndef CAMX_K1_QB_REMOVAL
+#define CAMX_K1_QB_REMOVAL 3
+#endif
+#ifndef CAMX_K1_QB
+#define CAMX_K1_QB 6
+#endif
+constexpr int kQuadBatchMax = CAMX_K1_QB;
 // Histograms: per-warp [3][256] uint32 bins in shared memory, one atomic
 // per (kept pixel, channel).  (A band block is only 3,072 pixels: per-lane
 // private byte counters - conflict-free, but a 768-word flush and re-zero
@@ -161,6 +167,11 @@ __device__ __forceinline__ uint32_t quad_exclusion(const StatsParams &p, const u
 template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
 __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t unit,
                                            uint32_t *smem, uint64_t (*part)[13]) {
+  // quads per lane per step: 6 (18 loads in flight; a default 96-row x
+  // 32-px band block is 768 quads = exactly 6 per thread of the CTA); the
+  // motion-mask path also loads the previous frame's words: 3 (fewer
+  // registers, more CTAs per SM).  Measured: tools/k1_probe.py
+  constexpr int kQuadBatch = MASKMODE == 2 ? CAMX_K1_QB_REMOVAL : kQuadBatchMax;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   constexpr int kStride = 32 * kStatsWarps;  // quads (pixels) per CTA-wide step

@@ -25,3 +25,21 @@ for h in (None, hist):
     ts = sorted(ts[3:])
     print(os.environ.get("CAMX_LIB", "in-tree"), "hist" if h is not None else "plain",
           "K1 us", round(ts[len(ts) // 2], 2), flush=True)
+
+# OBJECT_REMOVAL: frames 1.. against their predecessors (fused in-band motion mask)
+fb = N * H * W * 3
+for h in (None, hist):
+    ts = []
+    for i in range(23):
+        frames[:2].add_(0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.call("camx_band_stats", frames.data_ptr() + fb, frames.data_ptr(), None,
+                  (B - 1) * N, H, W, 32, K, 20, stats.data_ptr(),
+                  None if h is None else h.data_ptr(), None)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    ts = sorted(ts[3:])
+    print(os.environ.get("CAMX_LIB", "in-tree"), "removal", "hist" if h is not None else "plain",
+          "K1 us", round(ts[len(ts) // 2], 2), flush=True)
