@@ -77,7 +77,14 @@ __device__ __noinline__ void fused_solve_tail(const StatsParams &p, int64_t unit
   solve_seam_block(p.solve, s, k, cand);
 }
 
-constexpr int kStatsWarps = 4;  // warps per (image, side, block) unit = per CTA
+#ifndef CAMX_K1_WARPS
+#define CAMX_K1_WARPS 1
+#endif
+// warps per (image, side, block) unit = per CTA.  One: every warp streams
+// its own band blocks with shuffle-only reductions and no CTA barrier
+// (K1 + histograms 49 -> 39 us, OBJECT_REMOVAL 53 -> 46 us per 30 config-2
+// frames vs four warps per block; tools/k1_probe.py)
+constexpr int kStatsWarps = CAMX_K1_WARPS;
 #ifndef CAMX_K1_QB_REMOVAL
 #define CAMX_K1_QB_REMOVAL 3
 #endif
@@ -444,7 +451,7 @@ static void launch_stats(const StatsParams &p, cudaStream_t s) {
   }();
   // 32 CTAs per SM for the plain path (8 resident): units are scheduled
   // dynamically, ~6% faster than a one-wave persistent grid (tools/k1_probe.py)
-  const int per_sm = env_per_sm > 0 ? env_per_sm : 32;
+  const int per_sm = env_per_sm > 0 ? env_per_sm : 128 / kStatsWarps;
   const int64_t grid = std::min<int64_t>(p.n_units, static_cast<int64_t>(sm_count()) * per_sm);
   band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>
       <<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(p);
