@@ -8,6 +8,8 @@
 // order, round-half-even (oracle/camarray_oracle.py: resize_bilinear).
 //
 // seam_cost: exposure.py:417-445 (box downsample, Eq. 1 of the paper).
+#include <cstdlib>
+
 #include "camx_resize.cuh"
 
 namespace camx {
@@ -215,6 +217,145 @@ __global__ void tiles_shard_kernel(const ShardTileParams p) {
   }
 }
 
+// Band-staged downscale kernel (out < size, size <= W, 16-byte aligned
+// rows): CTA = (tile, band of kBandRows output rows).  The 2 x kBandRows
+// source rows of the band (the two taps of each output row; a strict
+// downscale never shares them) are staged once - every window row as one
+// or two camera segments copied as 16-byte-aligned supersets with one
+// barrier - and a per-column tap table (byte offset of the first tap in a
+// staged row, dp2a weights) is built once per CTA.  Each output pixel is
+// then the fused kernel's fixed-point path (3 aligned words per row, funnel
+// shift, PRMT, dp2a, IMAD; camx_resize.cuh bilerp_fx arithmetic); the band's
+// output rows are assembled in shared memory and written with 16-byte stores
+// (they are contiguous in the tile).
+#ifndef CAMX_TILES_BAND_ROWS
+#define CAMX_TILES_BAND_ROWS 4
+#endif
+constexpr int kBandRows = CAMX_TILES_BAND_ROWS;
+constexpr int kBandThreads = 256;
+constexpr uint32_t kTapStraddle = 0x80000000u;  // taps in two camera segments
+
+struct BandSeg {
+  int x_begin, x_end;  // window-local pixel range of the segment
+  int cam;             // camera of the segment
+  int head;            // first wanted byte inside the staged 16-byte superset
+  int nvec;            // 16-byte vectors staged per row
+  int off;             // smem byte offset of the superset in a staged row
+};
+
+__device__ __forceinline__ int band_byte(const BandSeg &s0, const BandSeg &s1, int x) {
+  return x < s0.x_end ? s0.off + s0.head + 3 * x : s1.off + s1.head + 3 * (x - s1.x_begin);
+}
+
+__global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TileParams p, int pitch,
+                                                                   int nseg) {
+  extern __shared__ __align__(16) uint8_t bsm[];
+  const int t = blockIdx.y;
+  const int64_t b = p.wins[3 * t];
+  const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
+  const int out = p.out;
+  const int O3 = out * 3;
+  const int oy0 = blockIdx.x * kBandRows;
+  const int nr = min(kBandRows, out - oy0);
+  uint2 *tap = reinterpret_cast<uint2 *>(bsm);                       // [out]
+  uint8_t *rows = bsm + ((out * 8 + 15) & ~15);                      // [2 * kBandRows][pitch]
+  uint8_t *orow = rows + 2 * kBandRows * pitch;                      // [kBandRows][O3]
+  __shared__ uint32_t wy_s[kBandRows];
+  __shared__ int srow_s[2 * kBandRows];
+  // segments of the window's columns (CTA-uniform; <= 2 since size <= W)
+  BandSeg sg[2];
+  {
+    int x = x0, off = 0;
+    for (int i = 0; i < 2; ++i) {
+      const int cam = min(x / p.W, p.n_cams - 1);
+      const int xe = i < nseg ? min(x0 + p.size, (cam + 1) * p.W) : x;
+      sg[i].x_begin = x - x0;
+      sg[i].x_end = xe - x0;
+      sg[i].cam = cam;
+      sg[i].head = ((x - cam * p.W) * 3) & 15;
+      sg[i].nvec = xe > x ? (sg[i].head + (xe - x) * 3 + 15) >> 4 : 0;  // empty: none
+      sg[i].off = off;
+      off += sg[i].nvec * 16;
+      x = xe;
+    }
+  }
+  for (int ox = threadIdx.x; ox < out; ox += blockDim.x) {
+    int a, c, w1;
+    src_coord_w(ox, p.scale, p.size, a, c, w1);
+    uint32_t o = static_cast<uint32_t>(band_byte(sg[0], sg[1], a));
+    if (nseg > 1 && a < sg[0].x_end && c >= sg[0].x_end) o |= kTapStraddle;
+    tap[ox] = make_uint2(o, static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16));
+  }
+  if (threadIdx.x < nr) {
+    int a, c, w1;
+    src_coord_w(oy0 + threadIdx.x, p.scale, p.size, a, c, w1);
+    wy_s[threadIdx.x] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
+    srow_s[2 * threadIdx.x] = y0 + a;
+    srow_s[2 * threadIdx.x + 1] = y0 + c;
+  }
+  __syncthreads();
+  // stage the 2 * nr source rows (both segments) with 16-byte loads
+  {
+    const int nv = sg[0].nvec + sg[1].nvec;
+    const int total = 2 * nr * nv;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int r = i / nv;
+      int v = i - r * nv;
+      const int s = v < sg[0].nvec ? 0 : 1;
+      if (s) v -= sg[0].nvec;
+      const BandSeg &g = sg[s];
+      const uint8_t *src = p.img + (((b * p.n_cams + g.cam) * p.H + srow_s[r]) *
+                                        static_cast<int64_t>(p.W) +
+                                    (x0 + g.x_begin - g.cam * p.W)) * 3 - g.head;
+      reinterpret_cast<uint4 *>(rows + r * pitch + g.off)[v] =
+          __ldg(reinterpret_cast<const uint4 *>(src) + v);
+    }
+  }
+  __syncthreads();
+  for (int item = threadIdx.x; item < nr * out; item += blockDim.x) {
+    const int ol = item / out;
+    const int ox = item - ol * out;
+    const uint2 tv = tap[ox];
+    const uint32_t wyp = wy_s[ol];
+    const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
+    const uint8_t *ra = rows + (2 * ol) * pitch;
+    const uint8_t *rb = ra + pitch;
+    uint8_t *o = orow + ol * O3 + 3 * ox;
+    if (!(tv.x & kTapStraddle)) {
+      const uint32_t la = tv.x;
+      const uint32_t sh = la * 8u;
+      const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
+      const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
+      const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
+      const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
+        const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
+        const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
+        o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+      }
+    } else {  // first tap = last pixel of segment 0, second = first of segment 1
+      const int a0 = static_cast<int>(tv.x & ~kTapStraddle);
+      const int a1 = sg[1].off + sg[1].head;
+      const uint32_t w1 = tv.y >> 16;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch)
+        o[ch] = static_cast<uint8_t>(bilerp_fx(ra[a0 + ch], ra[a1 + ch], rb[a0 + ch], rb[a1 + ch],
+                                               w1, wy1));
+    }
+  }
+  __syncthreads();
+  uint8_t *dst = p.tiles + (static_cast<int64_t>(t) * out + oy0) * O3;
+  const int nbytes = nr * O3;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (nbytes & 15) == 0) {
+    for (int v = threadIdx.x; v < nbytes / 16; v += blockDim.x)
+      reinterpret_cast<uint4 *>(dst)[v] = reinterpret_cast<const uint4 *>(orow)[v];
+  } else {
+    for (int i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = orow[i];
+  }
+}
+
 // ---- seam cost ------------------------------------------------------------
 __device__ __forceinline__ void box_mean(const uint8_t *img, int W, int f, int row2, int col2,
                                          double out[3]) {
@@ -290,6 +431,31 @@ static int launch_tiles(const uint8_t *images, int32_t n_cams, int32_t height, i
     if (bx > 64) bx = 64;
     tiles_kernel<<<dim3(static_cast<unsigned>(bx), n_tiles), 256, 0, s>>>(p);
     return launch_status();
+  }
+  static const bool band_enabled = [] {
+    const char *e = getenv("CAMX_TILES_BAND");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  if (band_enabled && out_size < size && (width * 3) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(images) % 16 == 0) {
+    // segments: the window's columns cross at most one camera boundary
+    const int pitch = ((size * 3 + 15) & ~15) + 64;  // two supersets + word-read slack
+    const int O3 = out_size * 3;
+    const size_t smem = ((out_size * 8 + 15) & ~15) + 2 * kBandRows * pitch + kBandRows * O3;
+    if (smem <= 200 * 1024) {
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(tiles_band_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return static_cast<int>(e);
+      }
+      // one or two camera segments per window: decided per window on the
+      // device would diverge the staging; launch with nseg = 2 (a one-segment
+      // window gets an empty second segment)
+      dim3 grid((out_size + kBandRows - 1) / kBandRows, n_tiles);
+      tiles_band_kernel<<<grid, kBandThreads, smem, s>>>(p, pitch, 2);
+      return launch_status();
+    }
   }
   const int S3p = ((size * 3 + 15) & ~15) + 64;
   const int smem = 2 * S3p + ((out_size * 3 + 15) & ~15);
