@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TilePara
   BandSeg sg[2];
   {
     int x = x0, off = 0;
+#pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int cam = min(x / p.W, p.n_cams - 1);
       const int xe = i < nseg ? min(x0 + p.size, (cam + 1) * p.W) : x;
@@ -294,27 +295,43 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TilePara
     srow_s[2 * threadIdx.x + 1] = y0 + c;
   }
   __syncthreads();
-  // stage the 2 * nr source rows (both segments) with 16-byte loads
+  // stage the 2 * nr source rows (both segments) with 16-byte loads; the
+  // (row, vector) pair advances incrementally (no division per element)
   {
-    const int nv = sg[0].nvec + sg[1].nvec;
-    const int total = 2 * nr * nv;
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
-      const int r = i / nv;
-      int v = i - r * nv;
-      const int s = v < sg[0].nvec ? 0 : 1;
-      if (s) v -= sg[0].nvec;
-      const BandSeg &g = sg[s];
-      const uint8_t *src = p.img + (((b * p.n_cams + g.cam) * p.H + srow_s[r]) *
-                                        static_cast<int64_t>(p.W) +
-                                    (x0 + g.x_begin - g.cam * p.W)) * 3 - g.head;
-      reinterpret_cast<uint4 *>(rows + r * pitch + g.off)[v] =
-          __ldg(reinterpret_cast<const uint4 *>(src) + v);
+    const int nv0 = sg[0].nvec, nv = nv0 + sg[1].nvec;
+    const int64_t rowpix = static_cast<int64_t>(p.W);
+    const uint8_t *base0 = p.img + ((b * p.n_cams + sg[0].cam) * p.H) * rowpix * 3 +
+                           (x0 + sg[0].x_begin - sg[0].cam * p.W) * 3 - sg[0].head;
+    const uint8_t *base1 = p.img + ((b * p.n_cams + sg[1].cam) * p.H) * rowpix * 3 +
+                           (x0 + sg[1].x_begin - sg[1].cam * p.W) * 3 - sg[1].head;
+    const int off1 = sg[1].off;
+    int r = threadIdx.x / nv, v = threadIdx.x - r * nv;
+    const int step_r = blockDim.x / nv, step_v = blockDim.x - step_r * nv;
+    for (; r < 2 * nr;) {
+      const int64_t rowoff = static_cast<int64_t>(srow_s[r]) * rowpix * 3;
+      uint4 val;
+      int dsto;
+      if (v < nv0) {
+        val = __ldg(reinterpret_cast<const uint4 *>(base0 + rowoff) + v);
+        dsto = v * 16;
+      } else {
+        val = __ldg(reinterpret_cast<const uint4 *>(base1 + rowoff) + (v - nv0));
+        dsto = off1 + (v - nv0) * 16;
+      }
+      *reinterpret_cast<uint4 *>(rows + r * pitch + dsto) = val;
+      r += step_r;
+      v += step_v;
+      if (v >= nv) {
+        v -= nv;
+        ++r;
+      }
     }
   }
   __syncthreads();
-  for (int item = threadIdx.x; item < nr * out; item += blockDim.x) {
-    const int ol = item / out;
-    const int ox = item - ol * out;
+  const uint32_t a1_straddle = static_cast<uint32_t>(sg[1].off + sg[1].head);
+  int ol = threadIdx.x / out, ox = threadIdx.x - ol * out;
+  const int step_l = blockDim.x / out, step_x = blockDim.x - step_l * out;
+  for (; ol < nr;) {
     const uint2 tv = tap[ox];
     const uint32_t wyp = wy_s[ol];
     const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
@@ -336,13 +353,18 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TilePara
         o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
       }
     } else {  // first tap = last pixel of segment 0, second = first of segment 1
-      const int a0 = static_cast<int>(tv.x & ~kTapStraddle);
-      const int a1 = sg[1].off + sg[1].head;
+      const uint32_t a0 = tv.x & ~kTapStraddle;
       const uint32_t w1 = tv.y >> 16;
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch)
-        o[ch] = static_cast<uint8_t>(bilerp_fx(ra[a0 + ch], ra[a1 + ch], rb[a0 + ch], rb[a1 + ch],
-                                               w1, wy1));
+        o[ch] = static_cast<uint8_t>(bilerp_fx(ra[a0 + ch], ra[a1_straddle + ch], rb[a0 + ch],
+                                               rb[a1_straddle + ch], w1, wy1));
+    }
+    ol += step_l;
+    ox += step_x;
+    if (ox >= out) {
+      ox -= out;
+      ++ol;
     }
   }
   __syncthreads();
