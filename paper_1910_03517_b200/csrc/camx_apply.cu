@@ -655,23 +655,13 @@ __global__ void __launch_bounds__(256) tile_fixup_kernel(const ApplyParams p, co
   const int nc = ncol, nr = nrow;
   // work items: every ox of a bad row, then the bad columns of every row
   // (bad rows included twice would only rewrite identical bytes; skip them)
-  const int64_t n_items = static_cast<int64_t>(nr) * q.out + static_cast<int64_t>(q.out) * nc;
   const uint8_t *frame = p.dst + b * p.cam_count * p.img_bytes;
   auto px = [&](int row, int mx) -> const uint8_t * {
     const int camc = mx / p.W;
     return frame + camc * p.img_bytes + static_cast<int64_t>(row) * p.row_bytes +
            (mx - camc * p.W) * 3;
   };
-  for (int64_t it = threadIdx.x; it < n_items; it += blockDim.x) {
-    int oy, ox;
-    if (it < static_cast<int64_t>(nr) * q.out) {
-      oy = rowbad[it / q.out];
-      ox = static_cast<int>(it % q.out);
-    } else {
-      const int64_t u = it - static_cast<int64_t>(nr) * q.out;
-      oy = static_cast<int>(u / nc);
-      ox = colbad[u % nc];
-    }
+  auto emit = [&](int oy, int ox) {
     int ya, yb, xa, xb, wy, wx;
     src_coord_w(oy, q.scale, q.size, ya, yb, wy);
     src_coord_w(ox, q.scale, q.size, xa, xb, wx);
@@ -679,7 +669,23 @@ __global__ void __launch_bounds__(256) tile_fixup_kernel(const ApplyParams p, co
     const uint8_t *C = px(y0 + yb, x0 + xa), *D = px(y0 + yb, x0 + xb);
     uint8_t *o = q.tiles + ((static_cast<int64_t>(t) * q.out + oy) * q.out + ox) * 3;
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) o[ch] = static_cast<uint8_t>(bilerp_fx(A[ch], Bp[ch], C[ch], D[ch], wx, wy));
+    for (int ch = 0; ch < 3; ++ch)
+      o[ch] = static_cast<uint8_t>(bilerp_fx(A[ch], Bp[ch], C[ch], D[ch], wx, wy));
+  };
+  for (int j = 0; j < nr; ++j)  // whole bad rows
+    for (int ox = threadIdx.x; ox < q.out; ox += blockDim.x) emit(rowbad[j], ox);
+  if (nc > 0) {  // bad columns of every row: (row, column) stepped without divisions
+    int oy = threadIdx.x / nc, j = threadIdx.x - oy * nc;
+    const int step_y = blockDim.x / nc, step_j = blockDim.x - step_y * nc;
+    while (oy < q.out) {
+      emit(oy, colbad[j]);
+      oy += step_y;
+      j += step_j;
+      if (j >= nc) {
+        j -= nc;
+        ++oy;
+      }
+    }
   }
 }
 
