@@ -71,12 +71,14 @@ __global__ void __launch_bounds__(256) window_count_kernel(const CountParams p) 
   const int total_w = p.n_cams * p.W;
   const int64_t img_px = static_cast<int64_t>(p.H) * p.W;
   unsigned long long local = 0;
-  for (int y = ys; y < ye; ++y) {
-    for (int dx = threadIdx.x; dx < p.size; dx += blockDim.x) {
-      const int x = x0 + dx;
-      if (x < 0 || x >= total_w) continue;
-      const int cam = x / p.W;
-      const int col = x - cam * p.W;
+  // column-outer: one camera/column split per column, then the slab's rows
+  // (consecutive threads still read consecutive columns of a row)
+  for (int dx = threadIdx.x; dx < p.size; dx += blockDim.x) {
+    const int x = x0 + dx;
+    if (x < 0 || x >= total_w) continue;
+    const int cam = x / p.W;
+    const int col = x - cam * p.W;
+    for (int y = ys; y < ye; ++y) {
       const int64_t pix = cam * img_px + static_cast<int64_t>(y) * p.W + col;
       bool on;
       if (FUSED) {

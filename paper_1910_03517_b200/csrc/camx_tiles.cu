@@ -59,6 +59,28 @@ __global__ void tiles_kernel(const TileParams p) {
   }
 }
 
+// Exact crop (out == size <= W): each window row is at most two camera
+// segments; CTA = (tile, band of 8 rows), coalesced byte copies, no
+// per-pixel index arithmetic.
+__global__ void __launch_bounds__(256) tiles_crop_kernel(const TileParams p) {
+  const int t = blockIdx.y;
+  const int64_t b = p.wins[3 * t];
+  const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
+  const int S3 = p.size * 3;
+  const int cam0 = x0 / p.W;
+  const int n0 = min(p.size, (cam0 + 1) * p.W - x0) * 3;  // bytes from camera cam0
+  const int64_t img_bytes = static_cast<int64_t>(p.H) * p.W * 3;
+  const uint8_t *c0 = p.img + (b * p.n_cams + cam0) * img_bytes + static_cast<int64_t>(x0 - cam0 * p.W) * 3;
+  const uint8_t *c1 = p.img + (b * p.n_cams + min(cam0 + 1, p.n_cams - 1)) * img_bytes;
+  const int oy_end = min(p.size, (blockIdx.x + 1) * 8);
+  for (int oy = blockIdx.x * 8; oy < oy_end; ++oy) {
+    const int64_t roff = static_cast<int64_t>(y0 + oy) * p.W * 3;
+    uint8_t *dst = p.tiles + (static_cast<int64_t>(t) * p.size + oy) * S3;
+    for (int i = threadIdx.x; i < S3; i += blockDim.x)
+      dst[i] = i < n0 ? c0[roff + i] : c1[roff + (i - n0)];
+  }
+}
+
 // Row-staged version: CTA = (tile, band of kTileRowsPerCta output rows).  For
 // each output row the two source rows' window segments (one per camera the
 // window covers) are staged in shared memory as their 16-byte-aligned
@@ -440,7 +462,12 @@ static int launch_tiles(const uint8_t *images, int32_t n_cams, int32_t height, i
   p.tiles = tiles_out;
   // host SSE float division is IEEE round-to-nearest, = np.float32(S) / np.float32(out)
   p.scale = static_cast<float>(size) / static_cast<float>(out_size);
-  if (out_size == size) {  // exact crop: plain copy kernel
+  if (out_size == size && size <= width) {  // exact crop, <= 2 camera segments per row
+    dim3 grid((size + 7) / 8, n_tiles);
+    tiles_crop_kernel<<<grid, 256, 0, s>>>(p);
+    return launch_status();
+  }
+  if (out_size == size) {  // exact crop over > 2 cameras: per-pixel gather kernel
     const int64_t npx = static_cast<int64_t>(out_size) * out_size;
     int64_t bx = (npx + 255) / 256;
     if (bx > 64) bx = 64;
