@@ -105,6 +105,86 @@ __global__ void __launch_bounds__(256) window_count_kernel(const CountParams p) 
   }
 }
 
+// Quad-vectorised counts (W % 4 == 0, 4-byte aligned frames / mask): a
+// thread owns fixed 4-pixel column groups of the window (a group never
+// straddles a camera since W % 4 == 0; 12-byte RGB loads as 3 words, the
+// per-pixel max |diff| by SIMD byte ops) and walks the slab's rows; the
+// window's unaligned first / last pixels go through the scalar test.
+__device__ __forceinline__ uint32_t quad_on(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t p0,
+                                            uint32_t p1, uint32_t p2, uint32_t tq) {
+  const uint32_t d0 = __vabsdiffu4(c0, p0), d1 = __vabsdiffu4(c1, p1), d2 = __vabsdiffu4(c2, p2);
+  // channel c of pixels 0..3 (bytes r g b r | g b r g | b r g b)
+  const uint32_t x = __byte_perm(__byte_perm(d0, d1, 0x0630u), d2, 0x5210u);
+  const uint32_t y = __byte_perm(__byte_perm(d0, d1, 0x0741u), d2, 0x6210u);
+  const uint32_t z = __byte_perm(__byte_perm(d0, d1, 0x0052u), d2, 0x7410u);
+  const uint32_t m = __vmaxu4(__vmaxu4(x, y), z);
+  return __vcmpgtu4(m, tq);  // 0xFF per pixel on
+}
+
+template <bool FUSED>
+__global__ void __launch_bounds__(256) window_count_quad_kernel(const CountParams p) {
+  const int win = blockIdx.y;
+  const int x0 = p.windows[2 * win], y0 = p.windows[2 * win + 1];
+  const int ys = y0 + blockIdx.x * p.slab;
+  const int ye = min(min(y0 + p.size, ys + p.slab), p.H);
+  const int total_w = p.n_cams * p.W;
+  const int xa = max(x0, 0), xb = min(x0 + p.size, total_w);  // columns on this mosaic
+  const int qa = (xa + 3) & ~3, qb = xb & ~3;                  // whole quads [qa, qb)
+  const int64_t img_px = static_cast<int64_t>(p.H) * p.W;
+  const uint32_t tq = p.t_diff < 0 ? 0u : static_cast<uint32_t>(min(p.t_diff, 255)) * 0x01010101u;
+  unsigned long long local = 0;
+  if (ys < ye && xa < xb) {
+    const int nquads = qb > qa ? (qb - qa) >> 2 : 0;
+    for (int q = threadIdx.x; q < nquads; q += blockDim.x) {
+      const int x = qa + 4 * q;
+      const int cam = x / p.W;
+      const int64_t pix0 = cam * img_px + static_cast<int64_t>(ys) * p.W + (x - cam * p.W);
+      for (int y = ys; y < ye; ++y) {
+        const int64_t pix = pix0 + static_cast<int64_t>(y - ys) * p.W;
+        uint32_t on;
+        if (FUSED) {
+          const uint32_t *c = reinterpret_cast<const uint32_t *>(p.cur + 3 * pix);
+          const uint32_t *r = reinterpret_cast<const uint32_t *>(p.prev + 3 * pix);
+          on = p.t_diff < 0 ? 0xFFFFFFFFu : quad_on(c[0], c[1], c[2], r[0], r[1], r[2], tq);
+        } else {
+          on = __vcmpne4(*reinterpret_cast<const uint32_t *>(p.mask + pix), 0u);
+        }
+        local += __popc(on) >> 3;
+      }
+    }
+    // unaligned edge columns [xa, qa) and [max(qb, qa), xb): scalar
+    const int ne0 = min(qa, xb) - xa, ne1 = xb - max(qb, qa);
+    const int ne = max(ne0, 0) + max(ne1, 0);
+    for (int i = threadIdx.x; i < ne * (ye - ys); i += blockDim.x) {
+      const int e = i % ne, y = ys + i / ne;
+      const int x = e < ne0 ? xa + e : max(qb, qa) + (e - max(ne0, 0));
+      const int cam = x / p.W;
+      const int64_t pix = cam * img_px + static_cast<int64_t>(y) * p.W + (x - cam * p.W);
+      bool hit;
+      if (FUSED) {
+        int m = 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          m = max(m, abs(static_cast<int>(p.cur[3 * pix + c]) - p.prev[3 * pix + c]));
+        hit = m > p.t_diff;
+      } else {
+        hit = p.mask[pix] != 0;
+      }
+      local += hit ? 1 : 0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  __shared__ unsigned long long part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += part[w];
+    atomicAdd(reinterpret_cast<unsigned long long *>(p.counts + win), t);
+  }
+}
+
 }  // namespace camx
 
 using namespace camx;
@@ -167,6 +247,14 @@ extern "C" int camx_window_counts(const uint8_t *mask, const uint8_t *cur, const
   p.counts = counts_out;
   p.slab = 32;
   dim3 grid((size + p.slab - 1) / p.slab, n_windows);
+  auto al4 = [](const void *x) { return reinterpret_cast<uintptr_t>(x) % 4 == 0; };
+  if (width % 4 == 0 && (mask ? al4(mask) : (al4(cur) && al4(prev)))) {
+    if (mask)
+      window_count_quad_kernel<false><<<grid, 256, 0, s>>>(p);
+    else
+      window_count_quad_kernel<true><<<grid, 256, 0, s>>>(p);
+    return launch_status();
+  }
   if (mask) {
     window_count_kernel<false><<<grid, 256, 0, s>>>(p);
   } else {

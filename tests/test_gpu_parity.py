@@ -1017,3 +1017,27 @@ def test_full_size_config4_wrap_vs_oracle():
     np.testing.assert_allclose(res.gain.cpu().numpy(), wg, rtol=GAIN_RTOL, atol=GAIN_ATOL)
     diff = np.abs(res.out.cpu().numpy().astype(int) - want_out.astype(int))
     assert diff.max() <= 1 and (diff > 0).mean() < 1e-6
+
+
+@pytest.mark.parametrize("t_diff", [-1, 0, 20, 255])
+def test_window_counts_quad_path_vs_oracle(t_diff):
+    """The quad-vectorised K4 (W % 4 == 0): random windows at unaligned
+    origins (edge pixels through the scalar path), windows hanging off a
+    camera shard, both the fused frame difference and a given mask."""
+    rng = np.random.default_rng(31 + t_diff)
+    N, H, W, S = 3, 140, 96, 61
+    cur = rng.integers(0, 256, (N, H, W, 3), dtype=np.uint8)
+    prev = cur.copy()
+    sel = rng.random((N, H, W)) < 0.2
+    prev[sel] = rng.integers(0, 256, (int(sel.sum()), 3), dtype=np.uint8)
+    full = np.concatenate([O.mask_diff(cur[c], prev[c], t_diff) for c in range(N)], axis=1)
+    org = [(int(rng.integers(-40, N * W - S + 40)), int(rng.integers(0, H - S + 1)))
+           for _ in range(40)]
+    want = []
+    for (x, y) in org:
+        x0, x1 = max(x, 0), min(x + S, N * W)
+        want.append(int(full[y:y + S, x0:x1].sum()) if x1 > x0 else 0)
+    got = at.window_counts(org, S, cur=cur, prev=prev, t_diff=t_diff, n_cams=N)
+    np.testing.assert_array_equal(got, want)
+    got2 = at.window_counts(org, S, mask=np.stack(np.split(full, N, axis=1)), n_cams=N)
+    np.testing.assert_array_equal(got2, want)
