@@ -276,6 +276,10 @@ def run_camx(args):
     px_per_frame = n_cams * H * W                      # whole-job pixels per array-frame
 
     def barrier():
+        # drain this rank's GPU work first: the sharded path's own NCCL
+        # all-gathers (camx's communicator, side stream) must not be in
+        # flight while torch's communicator runs the barrier's collective
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
