@@ -31,7 +31,7 @@ WORKLOADS = {
     "config1": (2, 480, 640, 64, "2 cameras 640x480 (reference CPU oracle config)"),
     "config2": (8, 1536, 2048, 30, "8 cameras x 2048x1536 (25.17 MP array), 30-frame batch"),
     "config3": (8, 1536, 2048, 30, "8-camera 25 MP array sharded one camera group per GPU"),
-    "config4": (14, 2160, 3840, 16, "14-camera 360-degree 4K array (wrap seam)"),
+    "config4": (14, 2160, 3840, 64, "14-camera 360-degree 4K array (wrap seam), 64-frame batches"),
     "config5": (8, 1536, 2048, 30, "config 2 + 36 attention tiles/array-frame, 960 -> 416x416"),
 }
 FALLBACK_HBM_GBS = 6650.0
