@@ -12,16 +12,16 @@
 // channel) from which mean / population std follow; the optional 256-bin
 // histograms are an exact sufficient statistic of the same pixel sets.
 //
-// Decomposition: one CTA of 4 warps per (image, side, block) unit, warps
-// interleaved over the band's pixel quads.  When the band is
-// 4-pixel aligned (W % 4 == 0, bw % 4 == 0) a lane reads pixel quads as
-// three 32-bit words (12 bytes = r g b r g b r g b r g b, so the channel of
-// every byte is fixed), U quads per batch so U*3 loads are in flight per
-// lane; otherwise it falls back to per-pixel byte loads.  Histograms use
-// per-lane private 8-bit counters in shared memory (4 bins per 32-bit
-// word; word (channel, bin/4, lane) sits in bank `lane`, so increments
-// never conflict and need no atomics), flushed every <= 255 pixels per lane
-// into per-lane registers by a SWAR (2 x 16-bit) column sum.
+// Decomposition: one warp (a 32-thread CTA) per (image, side, block) unit,
+// scheduled dynamically (CAMX_K1_WARPS warps per unit is a build knob).
+// When the band is 4-pixel aligned (W % 4 == 0, bw % 4 == 0) a lane reads
+// pixel quads as three 32-bit words (12 bytes = r g b r g b r g b r g b,
+// so the channel of every byte is fixed), U quads per step so U*3 loads are
+// in flight per lane, and the channel sums / sums of squares come from
+// dp4a with constant byte masks; otherwise per-pixel byte loads.
+// Histograms: one shared-memory atomic per (kept pixel, channel) into the
+// warp's 3 x 256 bins.  Reductions: warp shuffles only (32-bit halves when
+// a unit cannot overflow them).
 #include <algorithm>
 
 #include <cstdlib>
