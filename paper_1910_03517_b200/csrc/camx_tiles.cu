@@ -4,8 +4,13 @@
 // mosaic.pixels[y:y+S, x:x+S] of the concatenated mosaic (core.py:102-119);
 // here the mosaic is virtual (column x -> camera x / W).  Resize to the
 // detector input size is builder-defined (the reference has none):
-// bilinear, half-pixel centres, float32 weights/blend in a fixed operation
-// order, round-half-even (oracle/camarray_oracle.py: resize_bilinear).
+// bilinear, half-pixel centres, source coordinate in float32, 8-bit
+// fixed-point weights and an exact integer blend rounded half up
+// (camx_resize.cuh; oracle/camarray_oracle.py: resize_bilinear).
+// Kernels: exact crop (two-segment row copies), band-staged downscale
+// (the default resize path), row-staged resize (any geometry with <= 2
+// cameras per window row), per-pixel gather (windows wider than a camera),
+// camera-sharded gather (multi-GPU).
 //
 // seam_cost: exposure.py:417-445 (box downsample, Eq. 1 of the paper).
 #include <cstdlib>
