@@ -260,6 +260,10 @@ __global__ void tiles_shard_kernel(const ShardTileParams p) {
 #endif
 constexpr int kBandRows = CAMX_TILES_BAND_ROWS;
 constexpr int kBandThreads = 256;
+#ifndef CAMX_TILES_BAND_CTAS
+#define CAMX_TILES_BAND_CTAS 16
+#endif
+constexpr int kBandCtasPerTile = CAMX_TILES_BAND_CTAS;  // CTAs sharing one tile's bands
 constexpr uint32_t kTapStraddle = 0x80000000u;  // taps in two camera segments
 
 struct BandSeg {
@@ -275,20 +279,18 @@ __device__ __forceinline__ int band_byte(const BandSeg &s0, const BandSeg &s1, i
 }
 
 __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TileParams p, int pitch,
-                                                                   int nseg) {
+                                                                   int nseg, int bands_per_cta) {
   extern __shared__ __align__(16) uint8_t bsm[];
   const int t = blockIdx.y;
   const int64_t b = p.wins[3 * t];
   const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
   const int out = p.out;
   const int O3 = out * 3;
-  const int oy0 = blockIdx.x * kBandRows;
-  const int nr = min(kBandRows, out - oy0);
   uint2 *tap = reinterpret_cast<uint2 *>(bsm);                       // [out]
   uint8_t *rows = bsm + ((out * 8 + 15) & ~15);                      // [2 * kBandRows][pitch]
   uint8_t *orow = rows + 2 * kBandRows * pitch;                      // [kBandRows][O3]
   __shared__ uint32_t wy_s[kBandRows];
-  __shared__ int srow_s[2 * kBandRows];
+  __shared__ const uint8_t *src0_s[2 * kBandRows], *src1_s[2 * kBandRows];
   // segments of the window's columns (CTA-uniform; <= 2 since size <= W)
   BandSeg sg[2];
   {
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TilePara
       x = xe;
     }
   }
+  // per-column taps: built once, used by every band of this CTA
   for (int ox = threadIdx.x; ox < out; ox += blockDim.x) {
     int a, c, w1;
     src_coord_w(ox, p.scale, p.size, a, c, w1);
@@ -314,94 +317,98 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TilePara
     if (nseg > 1 && a < sg[0].x_end && c >= sg[0].x_end) o |= kTapStraddle;
     tap[ox] = make_uint2(o, static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16));
   }
-  if (threadIdx.x < nr) {
-    int a, c, w1;
-    src_coord_w(oy0 + threadIdx.x, p.scale, p.size, a, c, w1);
-    wy_s[threadIdx.x] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
-    srow_s[2 * threadIdx.x] = y0 + a;
-    srow_s[2 * threadIdx.x + 1] = y0 + c;
-  }
-  __syncthreads();
-  // stage the 2 * nr source rows (both segments) with 16-byte loads; the
-  // (row, vector) pair advances incrementally (no division per element)
-  {
-    const int nv0 = sg[0].nvec, nv = nv0 + sg[1].nvec;
-    const int64_t rowpix = static_cast<int64_t>(p.W);
-    const uint8_t *base0 = p.img + ((b * p.n_cams + sg[0].cam) * p.H) * rowpix * 3 +
-                           (x0 + sg[0].x_begin - sg[0].cam * p.W) * 3 - sg[0].head;
-    const uint8_t *base1 = p.img + ((b * p.n_cams + sg[1].cam) * p.H) * rowpix * 3 +
-                           (x0 + sg[1].x_begin - sg[1].cam * p.W) * 3 - sg[1].head;
-    const int off1 = sg[1].off;
-    int r = threadIdx.x / nv, v = threadIdx.x - r * nv;
-    const int step_r = blockDim.x / nv, step_v = blockDim.x - step_r * nv;
-    for (; r < 2 * nr;) {
-      const int64_t rowoff = static_cast<int64_t>(srow_s[r]) * rowpix * 3;
-      uint4 val;
-      int dsto;
-      if (v < nv0) {
-        val = __ldg(reinterpret_cast<const uint4 *>(base0 + rowoff) + v);
-        dsto = v * 16;
-      } else {
-        val = __ldg(reinterpret_cast<const uint4 *>(base1 + rowoff) + (v - nv0));
-        dsto = off1 + (v - nv0) * 16;
-      }
-      *reinterpret_cast<uint4 *>(rows + r * pitch + dsto) = val;
-      r += step_r;
-      v += step_v;
-      if (v >= nv) {
-        v -= nv;
-        ++r;
-      }
-    }
-  }
-  __syncthreads();
+  const int64_t rowbytes = static_cast<int64_t>(p.W) * 3;
+  const int64_t img_bytes = static_cast<int64_t>(p.H) * rowbytes;
+  const uint8_t *seg0 = p.img + (b * p.n_cams + sg[0].cam) * img_bytes +
+                        (x0 + sg[0].x_begin - sg[0].cam * p.W) * 3 - sg[0].head;
+  const uint8_t *seg1 = p.img + (b * p.n_cams + sg[1].cam) * img_bytes +
+                        (x0 + sg[1].x_begin - sg[1].cam * p.W) * 3 - sg[1].head;
+  const int nv0 = sg[0].nvec, nv = nv0 + sg[1].nvec;
+  const int off1 = sg[1].off;
   const uint32_t a1_straddle = static_cast<uint32_t>(sg[1].off + sg[1].head);
-  int ol = threadIdx.x / out, ox = threadIdx.x - ol * out;
-  const int step_l = blockDim.x / out, step_x = blockDim.x - step_l * out;
-  for (; ol < nr;) {
-    const uint2 tv = tap[ox];
-    const uint32_t wyp = wy_s[ol];
-    const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
-    const uint8_t *ra = rows + (2 * ol) * pitch;
-    const uint8_t *rb = ra + pitch;
-    uint8_t *o = orow + ol * O3 + 3 * ox;
-    if (!(tv.x & kTapStraddle)) {
-      const uint32_t la = tv.x;
-      const uint32_t sh = la * 8u;
-      const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
-      const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
-      const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
-      const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
-        const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
-        const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
-        o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+  const int band0 = blockIdx.x * bands_per_cta;
+  for (int band = band0; band < band0 + bands_per_cta; ++band) {
+    const int oy0 = band * kBandRows;
+    if (oy0 >= out) break;  // CTA-uniform
+    const int nr = min(kBandRows, out - oy0);
+    __syncthreads();  // previous band: its rows consumed, its output rows stored
+    if (threadIdx.x < nr) {
+      int a, c, w1;
+      src_coord_w(oy0 + threadIdx.x, p.scale, p.size, a, c, w1);
+      wy_s[threadIdx.x] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
+      src0_s[2 * threadIdx.x] = seg0 + (y0 + a) * rowbytes;
+      src0_s[2 * threadIdx.x + 1] = seg0 + (y0 + c) * rowbytes;
+      src1_s[2 * threadIdx.x] = seg1 + (y0 + a) * rowbytes;
+      src1_s[2 * threadIdx.x + 1] = seg1 + (y0 + c) * rowbytes;
+    }
+    __syncthreads();
+    // stage the 2 * nr tap rows (both segments) with 16-byte loads; the
+    // (row, vector) pair advances incrementally (no division per element)
+    {
+      int r = threadIdx.x / nv, v = threadIdx.x - r * nv;
+      const int step_r = blockDim.x / nv, step_v = blockDim.x - step_r * nv;
+      while (r < 2 * nr) {
+        const bool first = v < nv0;
+        const uint4 *src = reinterpret_cast<const uint4 *>(first ? src0_s[r] : src1_s[r]) +
+                           (first ? v : v - nv0);
+        *reinterpret_cast<uint4 *>(rows + r * pitch + (first ? v * 16 : off1 + (v - nv0) * 16)) =
+            __ldg(src);
+        r += step_r;
+        v += step_v;
+        if (v >= nv) {
+          v -= nv;
+          ++r;
+        }
       }
-    } else {  // first tap = last pixel of segment 0, second = first of segment 1
-      const uint32_t a0 = tv.x & ~kTapStraddle;
-      const uint32_t w1 = tv.y >> 16;
+    }
+    __syncthreads();
+    int ol = threadIdx.x / out, ox = threadIdx.x - ol * out;
+    const int step_l = blockDim.x / out, step_x = blockDim.x - step_l * out;
+    while (ol < nr) {
+      const uint2 tv = tap[ox];
+      const uint32_t wyp = wy_s[ol];
+      const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
+      const uint8_t *ra = rows + (2 * ol) * pitch;
+      const uint8_t *rb = ra + pitch;
+      uint8_t *o = orow + ol * O3 + 3 * ox;
+      if (!(tv.x & kTapStraddle)) {
+        const uint32_t la = tv.x;
+        const uint32_t sh = la * 8u;
+        const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
+        const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
+        const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
+        const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch)
-        o[ch] = static_cast<uint8_t>(bilerp_fx(ra[a0 + ch], ra[a1_straddle + ch], rb[a0 + ch],
-                                               rb[a1_straddle + ch], w1, wy1));
+        for (int ch = 0; ch < 3; ++ch) {
+          const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
+          const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
+          const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
+          o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+        }
+      } else {  // first tap = last pixel of segment 0, second = first of segment 1
+        const uint32_t a0 = tv.x & ~kTapStraddle;
+        const uint32_t w1 = tv.y >> 16;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch)
+          o[ch] = static_cast<uint8_t>(bilerp_fx(ra[a0 + ch], ra[a1_straddle + ch], rb[a0 + ch],
+                                                 rb[a1_straddle + ch], w1, wy1));
+      }
+      ol += step_l;
+      ox += step_x;
+      if (ox >= out) {
+        ox -= out;
+        ++ol;
+      }
     }
-    ol += step_l;
-    ox += step_x;
-    if (ox >= out) {
-      ox -= out;
-      ++ol;
+    __syncthreads();
+    uint8_t *dst = p.tiles + (static_cast<int64_t>(t) * out + oy0) * O3;
+    const int nbytes = nr * O3;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (nbytes & 15) == 0) {
+      for (int v = threadIdx.x; v < nbytes / 16; v += blockDim.x)
+        reinterpret_cast<uint4 *>(dst)[v] = reinterpret_cast<const uint4 *>(orow)[v];
+    } else {
+      for (int i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = orow[i];
     }
-  }
-  __syncthreads();
-  uint8_t *dst = p.tiles + (static_cast<int64_t>(t) * out + oy0) * O3;
-  const int nbytes = nr * O3;
-  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (nbytes & 15) == 0) {
-    for (int v = threadIdx.x; v < nbytes / 16; v += blockDim.x)
-      reinterpret_cast<uint4 *>(dst)[v] = reinterpret_cast<const uint4 *>(orow)[v];
-  } else {
-    for (int i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = orow[i];
   }
 }
 
@@ -506,8 +513,11 @@ static int launch_tiles(const uint8_t *images, int32_t n_cams, int32_t height, i
       // one or two camera segments per window: decided per window on the
       // device would diverge the staging; launch with nseg = 2 (a one-segment
       // window gets an empty second segment)
-      dim3 grid((out_size + kBandRows - 1) / kBandRows, n_tiles);
-      tiles_band_kernel<<<grid, kBandThreads, smem, s>>>(p, pitch, 2);
+      // a CTA walks several bands of one tile: the tap table is built once
+      const int nbands = (out_size + kBandRows - 1) / kBandRows;
+      const int bpc = (nbands + kBandCtasPerTile - 1) / kBandCtasPerTile;
+      dim3 grid((nbands + bpc - 1) / bpc, n_tiles);
+      tiles_band_kernel<<<grid, kBandThreads, smem, s>>>(p, pitch, 2, bpc);
       return launch_status();
     }
   }
