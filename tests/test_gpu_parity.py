@@ -1041,3 +1041,25 @@ def test_window_counts_quad_path_vs_oracle(t_diff):
     np.testing.assert_array_equal(got, want)
     got2 = at.window_counts(org, S, mask=np.stack(np.split(full, N, axis=1)), n_cams=N)
     np.testing.assert_array_equal(got2, want)
+
+
+@pytest.mark.parametrize("mode,om", [(xp.ExposureMode.STANDARD, O.STANDARD),
+                                     (xp.ExposureMode.OBJECT_REMOVAL, O.OBJECT_REMOVAL),
+                                     (xp.ExposureMode.SMOOTHING, O.SMOOTHING)])
+def test_batch_longer_than_a_solve_chunk(mode, om):
+    """B = 70 > 64 frames per K2 shared-memory chunk: the tick-loop state is
+    carried from chunk to chunk (parallel and sequential phase B), and some
+    blocks are unfittable (tall blocks with few valid pixels)."""
+    N, H, W, B, K = 3, 40, 64, 70, 4
+    frames = np.stack([O.synthetic_array(N, H, W, seed=21, objects=2, frame_index=t)
+                       for t in range(B)])
+    cfg = xp.ExposureConfig(band_width=8, blocks=K, min_band_pixels=79)
+    ocfg = O.Cfg(band_width=8, blocks=K, min_band_pixels=79)
+    ac = ArrayCorrector(N, H, W, cfg, mode)
+    res = ac.correct(torch.from_numpy(frames).cuda())
+    want, wg, wo, wok = O.correct_sequence(frames, None, om, ocfg)
+    np.testing.assert_allclose(res.gain.cpu().numpy(), wg, rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    np.testing.assert_allclose(res.offset.cpu().numpy(), wo, rtol=GAIN_RTOL, atol=GAIN_ATOL)
+    np.testing.assert_array_equal(res.fit_ok.cpu().numpy().astype(bool), wok)
+    d = np.abs(res.out.cpu().numpy().astype(int) - want.astype(int))
+    assert d.max() <= 1 and (d > 0).mean() < 1e-5
