@@ -318,14 +318,18 @@ def run_camx(args):
 
     def traced_call(fn, *a):
         if fn in ("camx_correct_batch", "camx_correct_batch_tiles"):
-            # K1 (x2 for OBJECT_REMOVAL with B > 1) + K2 + K3 (+ tile fix-up)
-            n_launch[0] += 3 if (mode is ExposureMode.OBJECT_REMOVAL and a[3] > 1) else 2
+            # K1 (x2 for OBJECT_REMOVAL with B > 1 and no previous frame) + K2 + K3
+            # (+ tile fix-up)
+            two_k1 = mode is ExposureMode.OBJECT_REMOVAL and a[3] > 1 and a[2] is None
+            n_launch[0] += 3 if two_k1 else 2
             n_launch[0] += 1 if fn == "camx_correct_batch" else 2
         elif fn == "camx_correct_batch_sharded":  # K1 (x2) + K2 + K3 (+ NCCL, not ours)
-            n_launch[0] += 4 if (mode is ExposureMode.OBJECT_REMOVAL and a[3] > 1) else 3
+            two_k1 = mode is ExposureMode.OBJECT_REMOVAL and a[3] > 1 and a[2] is None
+            n_launch[0] += 4 if two_k1 else 3
         elif fn == "camx_correct_batch_sharded_step":
-            if a[0] is not None:  # front half: K1 (x2) + K2
-                n_launch[0] += 3 if (mode is ExposureMode.OBJECT_REMOVAL and a[2] > 1) else 2
+            if a[0] is not None:  # front half: K1 (x2 without a previous frame) + K2
+                two_k1 = mode is ExposureMode.OBJECT_REMOVAL and a[2] > 1 and a[1] is None
+                n_launch[0] += 3 if two_k1 else 2
             if a[21] is not None:  # back half: K3 of the previous batch
                 n_launch[0] += 1
         elif fn.startswith("camx_"):
@@ -352,7 +356,7 @@ def run_camx(args):
             res = ac.flush(stream=stream) or res
         torch.cuda.synchronize()
     if use_graph:  # replays do not pass through _lib.call: same kernels as an eager step
-        per_step = 3 + (1 if (mode is ExposureMode.OBJECT_REMOVAL and B > 1) else 0)
+        per_step = 3  # K1 (one launch: the captured tick has a previous frame), K2, K3
         n_launch[0] = per_step * args.steps
 
     # roofline leg: the dominant kernel (K3 apply) alone, same buffers and

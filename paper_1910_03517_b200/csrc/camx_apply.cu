@@ -876,6 +876,11 @@ extern "C" int camx_apply_map(const uint8_t *images, uint8_t *out, int64_t n_ima
 namespace camx {
 
 // K1 (+ K2 as a programmatic dependent) for a whole batch.
+int band_stats_seq(const uint8_t *images, const uint8_t *prev_images, const uint8_t *excl_masks,
+                   int64_t n_images, int64_t prev_seq, int32_t height, int32_t width,
+                   int32_t band_width, int32_t blocks, int32_t t_diff, camx_band_stat *stats_out,
+                   uint32_t *hist_out, void *stream);
+
 // K1 over a batch: n_batch frames of `per_frame` images, frames 1.. against
 // their predecessors and frame 0 against prev_frame when `removal`.
 int band_stats_frames(const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch,
@@ -885,7 +890,10 @@ int band_stats_frames(const uint8_t *images, const uint8_t *prev_frame, int32_t 
   const int64_t frame_bytes = static_cast<int64_t>(height) * width * 3 * per_frame;
   const int64_t rec_frame = static_cast<int64_t>(per_frame) * 2 * blocks;
   int st;
-  if (removal && n_batch > 1) {
+  if (removal && n_batch > 1 && prev_frame != nullptr)  // one launch for the whole batch
+    return band_stats_seq(images, prev_frame, nullptr, int64_t(n_batch) * per_frame, per_frame,
+                          height, width, band_width, blocks, t_diff, stats, hist, stream);
+  if (removal && n_batch > 1) {  // no previous frame: array-frame 0 unmasked
     st = camx_band_stats(images + frame_bytes, images, nullptr, (n_batch - 1) * int64_t(per_frame),
                          height, width, band_width, blocks, t_diff, stats + rec_frame,
                          hist == nullptr ? nullptr : hist + rec_frame * 768, stream);

@@ -33,6 +33,9 @@ namespace camx {
 struct StatsParams {
   const uint8_t *img;
   const uint8_t *prev;   // mode 2
+  int64_t prev_seq;      // mode 2 over a batch: images >= prev_seq diff against
+                         // image - prev_seq (the previous array-frame), the
+                         // first prev_seq against `prev`; 0 = always `prev`
   const uint8_t *mask;   // mode 1
   int64_t img_bytes;
   int64_t mask_bytes;    // H * W
@@ -191,7 +194,11 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
   const int col0 = (side == CAMX_SIDE_LEFT) ? p.W - p.bw : 0;
   const int64_t row_bytes = static_cast<int64_t>(p.W) * 3;
   const uint8_t *base = p.img + img * p.img_bytes;
-  const uint8_t *pbase = (MASKMODE == 2) ? p.prev + img * p.img_bytes : nullptr;
+  const uint8_t *pbase =
+      (MASKMODE == 2) ? (p.prev_seq > 0 && img >= p.prev_seq
+                             ? p.img + (img - p.prev_seq) * p.img_bytes
+                             : p.prev + img * p.img_bytes)
+                      : nullptr;
   const uint8_t *mbase = (MASKMODE == 1) ? p.mask + img * p.mask_bytes : nullptr;
 
   uint32_t *cnt = HIST ? smem + warp * kHistWords : nullptr;
@@ -507,10 +514,29 @@ __global__ void band_moments_kernel(const camx_band_stat *st, int64_t n, int raw
 
 using namespace camx;
 
+namespace camx {
+int band_stats_seq(const uint8_t *images, const uint8_t *prev_images, const uint8_t *excl_masks,
+                   int64_t n_images, int64_t prev_seq, int32_t height, int32_t width,
+                   int32_t band_width, int32_t blocks, int32_t t_diff, camx_band_stat *stats_out,
+                   uint32_t *hist_out, void *stream);
+}
+
 extern "C" int camx_band_stats(const uint8_t *images, const uint8_t *prev_images,
                                const uint8_t *excl_masks, int64_t n_images, int32_t height,
                                int32_t width, int32_t band_width, int32_t blocks, int32_t t_diff,
                                camx_band_stat *stats_out, uint32_t *hist_out, void *stream) {
+  return band_stats_seq(images, prev_images, excl_masks, n_images, 0, height, width, band_width,
+                        blocks, t_diff, stats_out, hist_out, stream);
+}
+
+// prev_seq > 0 (OBJECT_REMOVAL over a batch of array-frames of prev_seq
+// images): image i >= prev_seq is diffed against image i - prev_seq, the
+// first prev_seq against prev_images - one launch for the whole batch.
+int camx::band_stats_seq(const uint8_t *images, const uint8_t *prev_images,
+                         const uint8_t *excl_masks, int64_t n_images, int64_t prev_seq,
+                         int32_t height, int32_t width, int32_t band_width, int32_t blocks,
+                         int32_t t_diff, camx_band_stat *stats_out, uint32_t *hist_out,
+                         void *stream) {
   if (n_images < 0 || height < 1 || width < 1) return CAMX_EINVAL;
   if (band_width < 1 || band_width > width / 2) return CAMX_EINVAL;
   if (blocks < 1 || blocks > height) return CAMX_EINVAL;
@@ -521,6 +547,7 @@ extern "C" int camx_band_stats(const uint8_t *images, const uint8_t *prev_images
   StatsParams p{};
   p.img = images;
   p.prev = prev_images;
+  p.prev_seq = prev_images != nullptr ? prev_seq : 0;
   p.mask = excl_masks;
   p.H = height;
   p.W = width;
