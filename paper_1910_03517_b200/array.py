@@ -44,6 +44,12 @@ class CorrectResult:
     hist: object | None    # int32 (B, N, 2, K, 3, 256) (uint32 counts) or None
 
 
+class _LocalComm:
+    """The whole array on one GPU: no communicator (world 1)."""
+
+    world, rank, handle = 1, 0, None
+
+
 class ArrayCorrector:
     """Seam exposure correction of an N-camera array on one GPU."""
 
@@ -309,8 +315,10 @@ class ArrayCorrector:
         (copy them to keep them).  The tick-loop state carries across
         submits like correct()."""
         t = _dev.require_cuda()
-        if self.comm is None or self.S == 0:
-            raise ValueError("submit() pipelines the sharded path: construct with comm=")
+        if self.S == 0:
+            raise ValueError("submit() needs at least one seam")
+        if self.comm is None and self.cam_count != self.n_cams:
+            raise ValueError("a camera shard pipelines through its comm= (dist.NcclComm)")
         if frames.dim() == 4:
             frames = frames[None]
         B = frames.shape[0]
@@ -370,7 +378,7 @@ class ArrayCorrector:
         pipe = getattr(self, "_pipe", None)
         if pipe is None or pipe["B"] != B:
             t = _dev.torch()
-            world = self.comm.world
+            world = self._pipe_comm().world
             cmax = -(-self.n_cams // world)
             R, K, S = _lib.STAT_BYTES, self.K, self.S
 
@@ -407,13 +415,18 @@ class ArrayCorrector:
         ap = (None, None, 0, None, None) if pending is None else (
             pending[0].data_ptr(), pending[1].data_ptr(), pending[0].shape[0],
             pending[2]["gain"].data_ptr(), pending[2]["offset"].data_ptr())
+        comm = self._pipe_comm()
         _lib.call("camx_correct_batch_sharded_step", *front, self.n_cams, self.cam_begin,
-                  self.cam_count, self.comm.world, int(self.wrap), self.height, self.width,
+                  self.cam_count, comm.world, int(self.wrap), self.height, self.width,
                   cfg.band_width, cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),
                   _dev.ptr(cb.get("stats_local")), _dev.ptr(cb.get("stats_all")),
                   _dev.ptr(cb.get("hist")), _dev.ptr(cb.get("gain")),
                   _dev.ptr(cb.get("offset")), _dev.ptr(cb.get("fit_ok")), *ap,
-                  self.comm.handle, _dev.stream_handle(main))
+                  comm.handle, _dev.stream_handle(main))
+
+    def _pipe_comm(self):
+        """The shard's communicator, or a one-GPU stand-in (no collective)."""
+        return self.comm if self.comm is not None else _LocalComm
 
     def _pending_result(self, pending, main):
         if pending is None:

@@ -879,9 +879,10 @@ def test_correct_batch_sharded_one_rank_matches_array(use_comm, mode, chunks, mo
         _lib.call("camx_comm_destroy", comm.handle)
 
 
+@pytest.mark.parametrize("use_comm", [True, False])
 @pytest.mark.parametrize("mode", [xp.ExposureMode.STANDARD, xp.ExposureMode.OBJECT_REMOVAL,
                                   xp.ExposureMode.SMOOTHING])
-def test_pipelined_submit_matches_sequential_correct(mode):
+def test_pipelined_submit_matches_sequential_correct(mode, use_comm):
     """ArrayCorrector.submit/flush (front half of batch k on the side stream
     under K3 of batch k-1, through a one-rank NCCL comm) returns, one call
     late, exactly the results of sequential correct() calls, and the
@@ -911,7 +912,7 @@ def test_pipelined_submit_matches_sequential_correct(mode):
     class OneRank:
         world, rank, handle = 1, 0, h.value
 
-    ac = ArrayCorrector(N, H, W, cfg, mode, comm=OneRank())
+    ac = ArrayCorrector(N, H, W, cfg, mode, comm=OneRank() if use_comm else None)
     got = []
     outs = [torch.empty_like(x) for x in batches]
 

@@ -26,3 +26,17 @@ for _ in range(10):
 e1.record()
 torch.cuda.synchronize()
 print("camx_tiles ms", round(e0.elapsed_time(e1) / 10, 3))
+
+# the camera-sharded kernel on the whole array (one "rank", no halo)
+zero = torch.zeros_like(tiles)
+for _ in range(2):
+    _lib.call("camx_tiles_shard", out.data_ptr(), N, H, W, 0, None, wd.data_ptr(), len(wins), 960,
+              416, zero.data_ptr(), None)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(5):
+    _lib.call("camx_tiles_shard", out.data_ptr(), N, H, W, 0, None, wd.data_ptr(), len(wins), 960,
+              416, zero.data_ptr(), None)
+e1.record()
+torch.cuda.synchronize()
+print("camx_tiles_shard ms", round(e0.elapsed_time(e1) / 5, 3), "equal:", torch.equal(zero, tiles))
