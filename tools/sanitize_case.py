@@ -1,6 +1,6 @@
 """Small workload exercising the shared-memory kernels for compute-sanitizer:
-K1 with histograms (+ fused mask), K2, fused apply+tile (+ warp-specialised
-variant when CAMX_TILE_WS=1), fix-up, standalone tiles."""
+K1 with histograms (+ fused mask), K2, fused apply+tile, fix-up, standalone
+tiles (band-staged, exact crop), window counts, the one-GPU pipelined stream."""
 import os
 import sys
 
@@ -20,5 +20,13 @@ ac.correct(frames)
 ac.correct(frames)
 res, tiles = ac.correct_and_tile(frames, size=128, out_size=52)
 t2 = detect.tiles(res.out, [(0, 10, 5), (1, 900, 60)], 128, 52)
+t3 = detect.tiles(res.out, [(0, 10, 5), (1, 1000, 60)], 128, 128)   # exact crop
+from paper_1910_03517_b200 import attention  # noqa: E402
+cnt = attention.window_counts([(3, 0), (901, 50), (2900, 70)], 128, cur=frames[1], prev=frames[0],
+                              n_cams=N)
+pipe = ArrayCorrector(N, H, W, ExposureConfig(band_width=16, blocks=5), histograms=True)
+for _ in range(3):
+    pipe.submit(frames)
+pipe.flush()
 torch.cuda.synchronize()
-print("ok", tiles.shape, t2.shape)
+print("ok", tiles.shape, t2.shape, t3.shape, list(cnt))
