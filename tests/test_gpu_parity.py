@@ -1064,3 +1064,21 @@ def test_batch_longer_than_a_solve_chunk(mode, om):
     np.testing.assert_array_equal(res.fit_ok.cpu().numpy().astype(bool), wok)
     d = np.abs(res.out.cpu().numpy().astype(int) - want.astype(int))
     assert d.max() <= 1 and (d > 0).mean() < 1e-5
+
+
+@pytest.mark.parametrize("out_size", [31, 64, 95])
+def test_band_tile_kernel_edge_windows(out_size):
+    """The band-staged downscale kernel (3W % 16 == 0) at the awkward
+    windows: ending on the mosaic's last column, straddling a camera seam by
+    one pixel on either side, starting on a camera's last pixel, on row 0
+    and the last row."""
+    rng = np.random.default_rng(out_size)
+    N, H, W, S = 3, 150, 128, 96
+    arr = rng.integers(0, 256, (2, N, H, W, 3), dtype=np.uint8)
+    mosaic = [np.concatenate(list(arr[b]), axis=1) for b in range(2)]
+    wins = [(0, N * W - S, 0), (1, N * W - S, H - S), (0, W - S + 1, 7), (1, W - 1, 3),
+            (0, 2 * W - 1, H - S), (1, W, 0), (0, W - S, 11), (1, 0, H - S)]
+    got = detect.tiles(torch.from_numpy(arr).cuda(), wins, S, out_size).cpu().numpy()
+    for i, (b, x, y) in enumerate(wins):
+        np.testing.assert_array_equal(got[i], O.resize_bilinear(O.crop(mosaic[b], x, y, S),
+                                                                 out_size), err_msg=str(wins[i]))
