@@ -412,6 +412,180 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TilePara
   }
 }
 
+// Band-staged kernel for a camera shard (camx_tiles_shard): as
+// tiles_band_kernel, but only the window's columns on this shard are staged
+// and only the output columns this shard owns (first tap on the shard,
+// contiguous [ox_lo, ox_hi) since i0 increases) are computed and stored; a
+// second tap on the next shard's first column comes from the halo.
+constexpr uint32_t kTapSeam = 0x40000000u;  // second tap = first pixel of segment 1
+constexpr uint32_t kTapHalo = 0x20000000u;  // second tap = the halo column
+constexpr uint32_t kTapFlags = kTapSeam | kTapHalo;
+
+__global__ void __launch_bounds__(kBandThreads) tiles_band_shard_kernel(const ShardTileParams sp,
+                                                                         int pitch,
+                                                                         int bands_per_cta) {
+  const TileParams &p = sp.t;
+  extern __shared__ __align__(16) uint8_t bsm[];
+  const int t = blockIdx.y;
+  const int64_t b = p.wins[3 * t];
+  const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
+  const int out = p.out;
+  const int O3 = out * 3;
+  // the window's columns on this shard, in local mosaic columns
+  const int lx0 = max(x0, sp.col_begin) - sp.col_begin;
+  const int lx1 = min(x0 + p.size, sp.col_begin + sp.local_cols) - sp.col_begin;
+  if (lx1 <= lx0) return;  // CTA-uniform: nothing here
+  uint2 *tap = reinterpret_cast<uint2 *>(bsm);
+  uint8_t *rows = bsm + ((out * 8 + 15) & ~15);
+  uint8_t *orow = rows + 2 * kBandRows * pitch;
+  __shared__ uint32_t wy_s[kBandRows];
+  __shared__ int srow_s[2 * kBandRows];
+  __shared__ const uint8_t *src0_s[2 * kBandRows], *src1_s[2 * kBandRows];
+  __shared__ int ox_lo_s, ox_hi_s;
+  // segments of the staged span [lx0, lx1) over this shard's cameras
+  BandSeg sg[2];
+  {
+    int x = lx0, off = 0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int cam = min(x / p.W, p.n_cams - 1);
+      const int xe = min(lx1, (cam + 1) * p.W);
+      sg[i].x_begin = x - lx0;
+      sg[i].x_end = xe - lx0;
+      sg[i].cam = cam;
+      sg[i].head = ((x - cam * p.W) * 3) & 15;
+      sg[i].nvec = xe > x ? (sg[i].head + (xe - x) * 3 + 15) >> 4 : 0;
+      sg[i].off = off;
+      off += sg[i].nvec * 16;
+      x = xe;
+    }
+  }
+  if (threadIdx.x == 0) {
+    ox_lo_s = out;
+    ox_hi_s = 0;
+  }
+  __syncthreads();
+  const int span0 = x0 - sp.col_begin - lx0;  // window-local column a -> staged index a + span0
+  for (int ox = threadIdx.x; ox < out; ox += blockDim.x) {
+    int a, c, w1;
+    src_coord_w(ox, p.scale, p.size, a, c, w1);
+    const int sa = a + span0, sc = c + span0;  // indices in the staged span
+    uint32_t o = 0;
+    if (sa >= 0 && a + x0 - sp.col_begin < sp.local_cols) {  // first tap here: owned
+      o = static_cast<uint32_t>(band_byte(sg[0], sg[1], sa));
+      const bool halo = sc >= lx1 - lx0;  // second tap = the next shard's first column
+      if (halo) o |= kTapHalo;
+      else if (sa < sg[0].x_end && sc >= sg[0].x_end) o |= kTapSeam;
+      atomicMin(&ox_lo_s, ox);
+      atomicMax(&ox_hi_s, ox + 1);
+    }
+    tap[ox] = make_uint2(o, static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16));
+  }
+  __syncthreads();
+  const int ox_lo = ox_lo_s, ox_hi = ox_hi_s;
+  if (ox_hi <= ox_lo) return;  // CTA-uniform
+  const int width = ox_hi - ox_lo;
+  const int64_t rowbytes = static_cast<int64_t>(p.W) * 3;
+  const int64_t img_bytes = static_cast<int64_t>(p.H) * rowbytes;
+  const uint8_t *seg0 = p.img + (b * p.n_cams + sg[0].cam) * img_bytes +
+                        (lx0 + sg[0].x_begin - sg[0].cam * p.W) * 3 - sg[0].head;
+  const uint8_t *seg1 = p.img + (b * p.n_cams + sg[1].cam) * img_bytes +
+                        (lx0 + sg[1].x_begin - sg[1].cam * p.W) * 3 - sg[1].head;
+  const int nv0 = sg[0].nvec, nv = nv0 + sg[1].nvec;
+  const int off1 = sg[1].off;
+  const uint32_t a1_seg1 = static_cast<uint32_t>(sg[1].off + sg[1].head);
+  const int band0 = blockIdx.x * bands_per_cta;
+  for (int band = band0; band < band0 + bands_per_cta; ++band) {
+    const int oy0 = band * kBandRows;
+    if (oy0 >= out) break;
+    const int nr = min(kBandRows, out - oy0);
+    __syncthreads();
+    if (threadIdx.x < nr) {
+      int a, c, w1;
+      src_coord_w(oy0 + threadIdx.x, p.scale, p.size, a, c, w1);
+      wy_s[threadIdx.x] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
+      srow_s[2 * threadIdx.x] = y0 + a;
+      srow_s[2 * threadIdx.x + 1] = y0 + c;
+      src0_s[2 * threadIdx.x] = seg0 + (y0 + a) * rowbytes;
+      src0_s[2 * threadIdx.x + 1] = seg0 + (y0 + c) * rowbytes;
+      src1_s[2 * threadIdx.x] = seg1 + (y0 + a) * rowbytes;
+      src1_s[2 * threadIdx.x + 1] = seg1 + (y0 + c) * rowbytes;
+    }
+    __syncthreads();
+    {
+      int r = threadIdx.x / nv, v = threadIdx.x - r * nv;
+      const int step_r = blockDim.x / nv, step_v = blockDim.x - step_r * nv;
+      while (r < 2 * nr) {
+        const bool first = v < nv0;
+        const uint4 *src = reinterpret_cast<const uint4 *>(first ? src0_s[r] : src1_s[r]) +
+                           (first ? v : v - nv0);
+        *reinterpret_cast<uint4 *>(rows + r * pitch + (first ? v * 16 : off1 + (v - nv0) * 16)) =
+            __ldg(src);
+        r += step_r;
+        v += step_v;
+        if (v >= nv) {
+          v -= nv;
+          ++r;
+        }
+      }
+    }
+    __syncthreads();
+    int ol = threadIdx.x / width, ox = threadIdx.x - ol * width;
+    const int step_l = blockDim.x / width, step_x = blockDim.x - step_l * width;
+    while (ol < nr) {
+      const int gox = ox_lo + ox;
+      const uint2 tv = tap[gox];
+      const uint32_t wyp = wy_s[ol];
+      const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
+      const uint8_t *ra = rows + (2 * ol) * pitch;
+      const uint8_t *rb = ra + pitch;
+      uint8_t *o = orow + ol * O3 + 3 * gox;
+      if (!(tv.x & kTapFlags)) {
+        const uint32_t la = tv.x;
+        const uint32_t sh = la * 8u;
+        const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
+        const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
+        const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
+        const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const uint32_t sel = 0x0030u + 0x0011u * ch;
+          const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
+          const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
+          o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+        }
+      } else {
+        const uint32_t a0 = tv.x & ~kTapFlags;
+        const uint32_t w1 = tv.y >> 16;
+        const bool use_halo = (tv.x & kTapHalo) != 0;
+        const uint8_t *ha = sp.halo + (b * p.H + srow_s[2 * ol]) * 3;
+        const uint8_t *hb = sp.halo + (b * p.H + srow_s[2 * ol + 1]) * 3;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const uint32_t A = ra[a0 + ch], C = rb[a0 + ch];
+          const uint32_t Bv = use_halo ? ha[ch] : ra[a1_seg1 + ch];
+          const uint32_t D = use_halo ? hb[ch] : rb[a1_seg1 + ch];
+          o[ch] = static_cast<uint8_t>(bilerp_fx(A, Bv, C, D, w1, wy1));
+        }
+      }
+      ol += step_l;
+      ox += step_x;
+      if (ox >= width) {
+        ox -= width;
+        ++ol;
+      }
+    }
+    __syncthreads();
+    // store the owned byte range of every output row of the band
+    const int obytes = 3 * width;
+    for (int rr = 0; rr < nr; ++rr) {
+      uint8_t *drow = p.tiles + (static_cast<int64_t>(t) * out + oy0 + rr) * O3 + 3 * ox_lo;
+      const uint8_t *srow = orow + rr * O3 + 3 * ox_lo;
+      for (int c3 = threadIdx.x; c3 < obytes; c3 += blockDim.x) drow[c3] = srow[c3];
+    }
+  }
+}
+
 // ---- seam cost ------------------------------------------------------------
 __device__ __forceinline__ void box_mean(const uint8_t *img, int W, int f, int row2, int col2,
                                          double out[3]) {
@@ -589,6 +763,29 @@ extern "C" int camx_tiles_shard(const uint8_t *images, int32_t n_cams, int32_t h
   p.col_begin = col_begin;
   p.local_cols = n_cams * width;
   p.halo = halo;
+  static const bool band_enabled = [] {
+    const char *e = getenv("CAMX_TILES_BAND");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  if (band_enabled && out_size < size && size <= width && (width * 3) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(images) % 16 == 0) {
+    const int pitch = ((size * 3 + 15) & ~15) + 64;
+    const size_t smem = ((out_size * 8 + 15) & ~15) + 2 * kBandRows * pitch +
+                        static_cast<size_t>(kBandRows) * out_size * 3;
+    if (smem <= 200 * 1024) {
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(tiles_band_shard_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return static_cast<int>(e);
+      }
+      const int nbands = (out_size + kBandRows - 1) / kBandRows;
+      const int bpc = (nbands + kBandCtasPerTile - 1) / kBandCtasPerTile;
+      dim3 grid((nbands + bpc - 1) / bpc, n_tiles);
+      tiles_band_shard_kernel<<<grid, kBandThreads, smem, as_stream(stream)>>>(p, pitch, bpc);
+      return launch_status();
+    }
+  }
   const int64_t npx = static_cast<int64_t>(out_size) * out_size;
   int64_t bx = (npx + 255) / 256;
   if (bx > 128) bx = 128;

@@ -703,15 +703,17 @@ def test_window_counts_on_a_camera_shard():
     np.testing.assert_array_equal(total, want)
 
 
-@pytest.mark.parametrize("world,n_cams,size,out", [(2, 4, 96, 40), (3, 5, 96, 96), (4, 8, 150, 64)])
-def test_tiles_on_camera_shards_sum_to_array_tiles(world, n_cams, size, out):
+@pytest.mark.parametrize("W", [100, 128])  # 3W % 16 == 0: the band-staged shard kernel
+@pytest.mark.parametrize("world,n_cams,size,out", [(2, 4, 96, 40), (3, 5, 96, 96), (4, 8, 150, 64),
+                                                   (3, 6, 120, 77)])
+def test_tiles_on_camera_shards_sum_to_array_tiles(world, n_cams, size, out, W):
     """camx_tiles_shard on each rank's cameras (halo = next shard's first
     column) writes disjoint output columns whose sum is the whole-array
     camx_tiles result, for windows inside one shard and straddling ones."""
     from paper_1910_03517_b200 import _lib
     from paper_1910_03517_b200.dist import camera_partition
     rng = np.random.default_rng(23 + world)
-    B, H, W = 2, 160, 100
+    B, H = 2, 160
     full = torch.as_tensor(rng.integers(0, 256, (B, n_cams, H, W, 3), dtype=np.uint8),
                            device="cuda")
     wins = [(b, x, y) for b in range(B) for y in (0, H - size)
