@@ -10,7 +10,7 @@
 // Kernels: exact crop (two-segment row copies), band-staged downscale
 // (the default resize path), row-staged resize (any geometry with <= 2
 // cameras per window row), per-pixel gather (windows wider than a camera),
-// camera-sharded gather (multi-GPU).
+// camera-sharded band-staged kernel and gather fallback (multi-GPU).
 //
 // seam_cost: exposure.py:417-445 (box downsample, Eq. 1 of the paper).
 #include <cstdlib>
