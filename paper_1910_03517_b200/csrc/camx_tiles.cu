@@ -726,8 +726,16 @@ extern "C" int camx_tiles(const uint8_t *images, int32_t n_cams, int32_t height,
   if (!images || !tiles_args_ok(n_cams, height, width, windows, n_tiles, size, out_size, tiles_out))
     return CAMX_EINVAL;
   if (n_tiles == 0) return CAMX_OK;
-  return launch_tiles(images, n_cams, height, width, windows, n_tiles, size, out_size, tiles_out,
-                      as_stream(stream));
+  // tiles ride on gridDim.y (<= 65535): chunk larger batches
+  constexpr int32_t kChunk = 65535;
+  const int64_t tile_bytes = static_cast<int64_t>(out_size) * out_size * 3;
+  for (int32_t t0 = 0; t0 < n_tiles; t0 += kChunk) {
+    const int32_t n = n_tiles - t0 < kChunk ? n_tiles - t0 : kChunk;
+    const int st = launch_tiles(images, n_cams, height, width, windows + 3 * static_cast<int64_t>(t0),
+                                n, size, out_size, tiles_out + t0 * tile_bytes, as_stream(stream));
+    if (st != CAMX_OK) return st;
+  }
+  return CAMX_OK;
 }
 
 extern "C" int camx_seam_cost(const uint8_t *left, const uint8_t *right, int64_t n_pairs,
@@ -741,7 +749,7 @@ extern "C" int camx_seam_cost(const uint8_t *left, const uint8_t *right, int64_t
   return launch_status();
 }
 
-extern "C" int camx_tiles_shard(const uint8_t *images, int32_t n_cams, int32_t height,
+static int tiles_shard_launch(const uint8_t *images, int32_t n_cams, int32_t height,
                                 int32_t width, int32_t col_begin, const uint8_t *halo,
                                 const int32_t *windows, int32_t n_tiles, int32_t size,
                                 int32_t out_size, uint8_t *tiles_out, void *stream) {
@@ -792,4 +800,25 @@ extern "C" int camx_tiles_shard(const uint8_t *images, int32_t n_cams, int32_t h
   tiles_shard_kernel<<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(n_tiles)), 256, 0,
                        as_stream(stream)>>>(p);
   return launch_status();
+}
+
+
+extern "C" int camx_tiles_shard(const uint8_t *images, int32_t n_cams, int32_t height,
+                                int32_t width, int32_t col_begin, const uint8_t *halo,
+                                const int32_t *windows, int32_t n_tiles, int32_t size,
+                                int32_t out_size, uint8_t *tiles_out, void *stream) {
+  if (n_tiles < 0) return CAMX_EINVAL;
+  if (n_tiles == 0)
+    return tiles_shard_launch(images, n_cams, height, width, col_begin, halo, windows, 0, size,
+                              out_size, tiles_out, stream);
+  constexpr int32_t kChunk = 65535;  // tiles ride on gridDim.y
+  const int64_t tile_bytes = static_cast<int64_t>(out_size) * out_size * 3;
+  for (int32_t t0 = 0; t0 < n_tiles; t0 += kChunk) {
+    const int32_t n = n_tiles - t0 < kChunk ? n_tiles - t0 : kChunk;
+    const int st = tiles_shard_launch(images, n_cams, height, width, col_begin, halo,
+                                      windows + 3 * static_cast<int64_t>(t0), n, size, out_size,
+                                      tiles_out + t0 * tile_bytes, stream);
+    if (st != CAMX_OK) return st;
+  }
+  return CAMX_OK;
 }

@@ -1084,3 +1084,22 @@ def test_band_tile_kernel_edge_windows(out_size):
     for i, (b, x, y) in enumerate(wins):
         np.testing.assert_array_equal(got[i], O.resize_bilinear(O.crop(mosaic[b], x, y, S),
                                                                  out_size), err_msg=str(wins[i]))
+
+
+@pytest.mark.parametrize("out_size", [4, 2])
+def test_more_tiles_than_one_grid_dimension(out_size):
+    """70,000 windows (> 65,535, the gridDim.y limit the tile kernels use):
+    the launches are chunked; tiles on both sides of the chunk boundary and a
+    random sample equal the oracle."""
+    rng = np.random.default_rng(5)
+    N, H, W, S = 2, 32, 64, 4
+    arr = rng.integers(0, 256, (1, N, H, W, 3), dtype=np.uint8)
+    mosaic = np.concatenate(list(arr[0]), axis=1)
+    T = 70000
+    wins = [(0, int(x), int(y)) for x, y in zip(rng.integers(0, N * W - S + 1, T),
+                                                 rng.integers(0, H - S + 1, T))]
+    got = detect.tiles(torch.from_numpy(arr).cuda(), wins, S, out_size).cpu().numpy()
+    assert got.shape == (T, out_size, out_size, 3)
+    for i in [0, 65534, 65535, 65536, T - 1] + [int(v) for v in rng.integers(0, T, 200)]:
+        _, x, y = wins[i]
+        np.testing.assert_array_equal(got[i], O.resize_bilinear(O.crop(mosaic, x, y, S), out_size))
