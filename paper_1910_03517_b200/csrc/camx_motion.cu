@@ -246,19 +246,27 @@ extern "C" int camx_window_counts(const uint8_t *mask, const uint8_t *cur, const
   p.windows = windows;
   p.counts = counts_out;
   p.slab = 32;
-  dim3 grid((size + p.slab - 1) / p.slab, n_windows);
   auto al4 = [](const void *x) { return reinterpret_cast<uintptr_t>(x) % 4 == 0; };
-  if (width % 4 == 0 && (mask ? al4(mask) : (al4(cur) && al4(prev)))) {
-    if (mask)
-      window_count_quad_kernel<false><<<grid, 256, 0, s>>>(p);
-    else
-      window_count_quad_kernel<true><<<grid, 256, 0, s>>>(p);
-    return launch_status();
+  const bool quad = width % 4 == 0 && (mask ? al4(mask) : (al4(cur) && al4(prev)));
+  // windows ride on gridDim.y (<= 65535): chunk longer lists
+  for (int32_t w0 = 0; w0 < n_windows; w0 += 65535) {
+    CountParams pc = p;
+    pc.windows = windows + 2 * static_cast<int64_t>(w0);
+    pc.counts = counts_out + w0;
+    pc.n_windows = min(65535, n_windows - w0);
+    dim3 grid((size + p.slab - 1) / p.slab, pc.n_windows);
+    if (quad) {
+      if (mask)
+        window_count_quad_kernel<false><<<grid, 256, 0, s>>>(pc);
+      else
+        window_count_quad_kernel<true><<<grid, 256, 0, s>>>(pc);
+    } else if (mask) {
+      window_count_kernel<false><<<grid, 256, 0, s>>>(pc);
+    } else {
+      window_count_kernel<true><<<grid, 256, 0, s>>>(pc);
+    }
+    const int st = launch_status();
+    if (st != CAMX_OK) return st;
   }
-  if (mask) {
-    window_count_kernel<false><<<grid, 256, 0, s>>>(p);
-  } else {
-    window_count_kernel<true><<<grid, 256, 0, s>>>(p);
-  }
-  return launch_status();
+  return CAMX_OK;
 }
