@@ -396,6 +396,53 @@ def test_apply_array_bit_exact_given_maps():
             np.testing.assert_array_equal(got[b], want)
 
 
+@pytest.mark.parametrize("scale", ["tie", "wide"])
+def test_apply_extreme_and_tie_maps_bit_exact(scale):
+    """K3 and the fused K3+K5 kernel at extreme and tie-heavy maps, bit-exact.
+    'wide' maps (gains up to 1e3, offsets to +-3e4) clip most sub-pixels at
+    both ends; 'tie' maps (quarter gains, half offsets) put many products
+    exactly on .5 so the half-even rounding of every step is exercised (this
+    test caught ptxas contracting mul.rn.f32x2 + add.rn.f32x2 into one FFMA2
+    in an unsaturated-chain experiment; profiles/r01/SUMMARY.md)."""
+    rng = np.random.default_rng(17)
+    from paper_1910_03517_b200 import _lib
+    N, H, W, K, B = 3, 64, 1024, 4, 2
+    S = N - 1
+    frames = rng.integers(0, 256, (B, N, H, W, 3), dtype=np.uint8)
+    if scale == "wide":
+        gain = np.exp(rng.uniform(np.log(1e-3), np.log(1e3), (B, S, 2, K, 3)))
+        off = rng.uniform(-3e4, 3e4, (B, S, 2, K, 3))
+        off[:, :, :, ::2] = rng.uniform(-50, 50, (B, S, 2, (K + 1) // 2, 3))
+        gain[:, :, :, ::2] = rng.uniform(0.5, 2.0, (B, S, 2, (K + 1) // 2, 3))
+    else:
+        gain = rng.integers(1, 8, (B, S, 2, K, 3)) / 4.0
+        off = rng.integers(-64, 64, (B, S, 2, K, 3)) / 2.0
+    d_in = torch.from_numpy(frames).cuda()
+    d_out = torch.empty_like(d_in)
+    g = torch.from_numpy(gain).cuda()
+    o = torch.from_numpy(off).cuda()
+    stream = torch.cuda.current_stream().cuda_stream
+    _lib.call("camx_apply_array", d_in.data_ptr(), d_out.data_ptr(), B, 0, N, N, 0,
+              H, W, K, g.data_ptr(), o.data_ptr(), stream)
+    want = np.stack([O.apply_array(frames[b], gain[b], off[b], False) for b in range(B)])
+    np.testing.assert_array_equal(d_out.cpu().numpy(), want)
+    # fused correction + tiles with the same maps
+    size, out_size = 48, 20
+    wins = [(0, 10, 3), (0, 1000, 10), (1, 2000, 15), (1, 3 * W - size, H - size)]
+    win_t = torch.tensor([list(w) for w in wins], dtype=torch.int32).cuda()
+    frame_off = torch.tensor([0, 2, 4], dtype=torch.int32).cuda()
+    tiles = torch.empty((len(wins), out_size, out_size, 3), dtype=torch.uint8, device="cuda")
+    d_out2 = torch.empty_like(d_in)
+    _lib.call("camx_correct_and_tile", d_in.data_ptr(), d_out2.data_ptr(), B, N, 0, H, W, K,
+              g.data_ptr(), o.data_ptr(), win_t.data_ptr(), frame_off.data_ptr(), len(wins), 2,
+              size, out_size, tiles.data_ptr(), stream)
+    np.testing.assert_array_equal(d_out2.cpu().numpy(), want)
+    tiles = tiles.cpu().numpy()
+    for i, (b, x, y) in enumerate(wins):
+        mosaic = np.concatenate(list(want[b]), axis=1)
+        np.testing.assert_array_equal(tiles[i], O.resize_bilinear(O.crop(mosaic, x, y, size), out_size))
+
+
 def test_correct_host_matches_device():
     N, H, W, B = 3, 96, 128, 4
     frames = np.stack([O.synthetic_array(N, H, W, seed=2, frame_index=t) for t in range(B)])
