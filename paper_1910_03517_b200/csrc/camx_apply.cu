@@ -340,8 +340,17 @@ constexpr int kFuseMaxWin = 48;  // windows per array-frame the fused path accep
 // window (orow[] is well defined)
 // ring of the fused kernel: 4-row stages (one CTA barrier and one hit
 // enumeration per stage); refill lags two stages (previous row resident)
-constexpr int kFuseRows = 4;
-constexpr int kFuseStages = 4;
+#ifndef CAMX_FUSE_ROWS
+#define CAMX_FUSE_ROWS 4
+#endif
+#ifndef CAMX_FUSE_STAGES
+#define CAMX_FUSE_STAGES 4
+#endif
+#ifndef CAMX_FUSE_MINB
+#define CAMX_FUSE_MINB 5  // CTAs per SM the register budget is sized for
+#endif
+constexpr int kFuseRows = CAMX_FUSE_ROWS;
+constexpr int kFuseStages = CAMX_FUSE_STAGES;
 static_assert(kFuseRows == 4, "hit enumeration uses e >> 2 / e & 3");
 
 struct FuseSmem {  // carved from dynamic shared memory after the ring
@@ -412,7 +421,7 @@ __device__ __forceinline__ void resample_hit(const uint8_t *ringb, uint32_t offa
 }
 
 template <bool TILES, int ROWS, int STAGES>
-__global__ void __launch_bounds__(kApplyThreads, TILES ? 5 : 4)
+__global__ void __launch_bounds__(kApplyThreads, TILES ? CAMX_FUSE_MINB : 4)
     apply_tma_kernel(const ApplyParams p, const TileFuse q) {
   extern __shared__ __align__(128) uint4 ring[];  // [STAGES][ROWS][kApplyThreads]
   __shared__ __align__(8) uint64_t full[STAGES];
