@@ -642,10 +642,33 @@ __device__ __forceinline__ int col_cta(const ApplyParams &p, int mx) {
   return g0 == g1 ? camc * p.col_groups + g0 : -1 - camc;
 }
 
+// Per-tile tables (dynamic shared memory, fixup_smem_bytes()): for every
+// output column the byte offsets of its two column taps inside an image row
+// (camera image + pixel) and its weight; for every output row the byte
+// offsets of its two tap rows and its weight; then the bad-column / bad-row
+// lists.  Source bytes come through the read-only path (the corrected frame
+// is not written by this kernel), so the loads of several outputs overlap.
+struct FixupSmem {
+  int64_t *cola, *colb;  // [out] image-relative byte offset of column taps a, b
+  int32_t *rowa, *rowb;  // [out] row byte offset of row taps a, b
+  int32_t *colw, *roww;  // [out] fixed-point weights
+  int32_t *colbad, *rowbad;
+};
+__host__ __device__ __forceinline__ size_t fixup_smem_bytes(int out) {
+  return static_cast<size_t>(out) * (2 * sizeof(int64_t) + 6 * sizeof(int32_t));
+}
+
 __global__ void __launch_bounds__(256) tile_fixup_kernel(const ApplyParams p, const TileFuse q) {
-  extern __shared__ int32_t fx_smem[];
-  int32_t *colbad = fx_smem;          // [out] ox whose column taps are not one CTA's
-  int32_t *rowbad = fx_smem + q.out;  // [out] oy whose row taps are not one CTA's
+  extern __shared__ __align__(16) uint8_t fx_raw[];
+  FixupSmem fs;
+  fs.cola = reinterpret_cast<int64_t *>(fx_raw);
+  fs.colb = fs.cola + q.out;
+  fs.rowa = reinterpret_cast<int32_t *>(fs.colb + q.out);
+  fs.rowb = fs.rowa + q.out;
+  fs.colw = fs.rowb + q.out;
+  fs.roww = fs.colw + q.out;
+  fs.colbad = fs.roww + q.out;
+  fs.rowbad = fs.colbad + q.out;
   __shared__ int ncol, nrow;
   const int t = blockIdx.x;
   const int64_t b = q.wins[3 * t];
@@ -653,41 +676,55 @@ __global__ void __launch_bounds__(256) tile_fixup_kernel(const ApplyParams p, co
   if (threadIdx.x == 0) ncol = nrow = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < q.out; i += blockDim.x) {
-    int a, c;
-    float f;
-    src_coord(i, q.scale, q.size, a, c, f);
+    int a, c, w;
+    src_coord_w(i, q.scale, q.size, a, c, w);
     const int ga = col_cta(p, x0 + a), gb = col_cta(p, x0 + c);
-    if (ga < 0 || ga != gb) colbad[atomicAdd(&ncol, 1)] = i;
-    if (row_cta(p, y0 + a) != row_cta(p, y0 + c)) rowbad[atomicAdd(&nrow, 1)] = i;
+    if (ga < 0 || ga != gb) fs.colbad[atomicAdd(&ncol, 1)] = i;
+    if (row_cta(p, y0 + a) != row_cta(p, y0 + c)) fs.rowbad[atomicAdd(&nrow, 1)] = i;
+    const int ma = x0 + a, mc = x0 + c;
+    const int ca = ma / p.W, cc = mc / p.W;
+    fs.cola[i] = ca * p.img_bytes + static_cast<int64_t>(ma - ca * p.W) * 3;
+    fs.colb[i] = cc * p.img_bytes + static_cast<int64_t>(mc - cc * p.W) * 3;
+    fs.colw[i] = w;
+    fs.rowa[i] = (y0 + a) * p.row_bytes;
+    fs.rowb[i] = (y0 + c) * p.row_bytes;
+    fs.roww[i] = w;
   }
   __syncthreads();
   const int nc = ncol, nr = nrow;
   // work items: every ox of a bad row, then the bad columns of every row
   // (bad rows included twice would only rewrite identical bytes; skip them)
   const uint8_t *frame = p.dst + b * p.cam_count * p.img_bytes;
-  auto px = [&](int row, int mx) -> const uint8_t * {
-    const int camc = mx / p.W;
-    return frame + camc * p.img_bytes + static_cast<int64_t>(row) * p.row_bytes +
-           (mx - camc * p.W) * 3;
-  };
+  uint8_t *tile = q.tiles + static_cast<int64_t>(t) * q.out * q.out * 3;
   auto emit = [&](int oy, int ox) {
-    int ya, yb, xa, xb, wy, wx;
-    src_coord_w(oy, q.scale, q.size, ya, yb, wy);
-    src_coord_w(ox, q.scale, q.size, xa, xb, wx);
-    const uint8_t *A = px(y0 + ya, x0 + xa), *Bp = px(y0 + ya, x0 + xb);
-    const uint8_t *C = px(y0 + yb, x0 + xa), *D = px(y0 + yb, x0 + xb);
-    uint8_t *o = q.tiles + ((static_cast<int64_t>(t) * q.out + oy) * q.out + ox) * 3;
+    const uint8_t *ra = frame + fs.rowa[oy], *rb = frame + fs.rowb[oy];
+    const int64_t xa = fs.cola[ox], xb = fs.colb[ox];
+    const uint32_t wx = static_cast<uint32_t>(fs.colw[ox]), wy = static_cast<uint32_t>(fs.roww[oy]);
+    uint32_t A[3], B[3], C[3], D[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      A[ch] = __ldg(ra + xa + ch);
+      B[ch] = __ldg(ra + xb + ch);
+      C[ch] = __ldg(rb + xa + ch);
+      D[ch] = __ldg(rb + xb + ch);
+    }
+    uint8_t *o = tile + (static_cast<int64_t>(oy) * q.out + ox) * 3;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
-      o[ch] = static_cast<uint8_t>(bilerp_fx(A[ch], Bp[ch], C[ch], D[ch], wx, wy));
+      o[ch] = static_cast<uint8_t>(bilerp_fx(A[ch], B[ch], C[ch], D[ch], wx, wy));
   };
-  for (int j = 0; j < nr; ++j)  // whole bad rows
-    for (int ox = threadIdx.x; ox < q.out; ox += blockDim.x) emit(rowbad[j], ox);
+  const int nrow_items = nr * q.out;  // (bad row j, ox), ox fastest
+#pragma unroll 4
+  for (int it = threadIdx.x; it < nrow_items; it += blockDim.x) {
+    const int j = it / q.out;
+    emit(fs.rowbad[j], it - j * q.out);
+  }
   if (nc > 0) {  // bad columns of every row: (row, column) stepped without divisions
     int oy = threadIdx.x / nc, j = threadIdx.x - oy * nc;
     const int step_y = blockDim.x / nc, step_j = blockDim.x - step_y * nc;
+#pragma unroll 4
     while (oy < q.out) {
-      emit(oy, colbad[j]);
+      emit(oy, fs.colbad[j]);
       oy += step_y;
       j += step_j;
       if (j >= nc) {
@@ -801,7 +838,7 @@ static int launch_apply_tiles(ApplyParams &p, TileFuse &q, int32_t n_tiles,
   if (max_tiles_per_frame > kFuseMaxWin || q.out >= q.size || q.size > 4096) return CAMX_EINVAL;
   int st = launch_tma<true, kFuseRows, kFuseStages>(p, q, stream);
   if (st != CAMX_OK || n_tiles == 0) return st;
-  const size_t smem = 2 * sizeof(int32_t) * q.out;
+  const size_t smem = fixup_smem_bytes(q.out);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(tile_fixup_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
