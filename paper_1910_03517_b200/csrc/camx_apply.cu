@@ -346,6 +346,9 @@ constexpr int kFuseMaxWin = 48;  // windows per array-frame the fused path accep
 #ifndef CAMX_FUSE_STAGES
 #define CAMX_FUSE_STAGES 4
 #endif
+#ifndef CAMX_FUSE_SPLIT
+#define CAMX_FUSE_SPLIT 1  // resample work unit: 0 hit per CTA, 1 hit per warp, 2 half hit per warp
+#endif
 #ifndef CAMX_FUSE_MINB
 #define CAMX_FUSE_MINB 5  // CTAs per SM the register budget is sized for
 #endif
@@ -576,6 +579,10 @@ __global__ void __launch_bounds__(kApplyThreads, TILES ? CAMX_FUSE_MINB : 4)
       // with no shared hit list and no second barrier.
       const uint8_t *ringb = reinterpret_cast<const uint8_t *>(ring);
       const int lane = threadIdx.x & 31;
+#if CAMX_FUSE_SPLIT != 0
+      const int warp = threadIdx.x >> 5;
+      int hit_seq = st;  // rotates which warp takes a stage's first hit
+#endif
       const int rs0 = st * ROWS;  // CTA-relative first row of the stage
       for (int e0 = 0; e0 < 4 * nwin; e0 += 32) {
         const int e = e0 + lane;
@@ -611,15 +618,36 @@ __global__ void __launch_bounds__(kApplyThreads, TILES ? CAMX_FUSE_MINB : 4)
         while (bal) {
           const int src = __ffs(bal) - 1;
           bal &= bal - 1u;
+#if CAMX_FUSE_SPLIT == 0
+          // every hit split over the CTA's 128 threads
+          const int t0 = threadIdx.x, nt = kApplyThreads;
+#else
+          // hits (CAMX_FUSE_SPLIT 1) or half hits (2) dealt round-robin to the
+          // warps: the per-hit broadcast and set-up run once per hit instead
+          // of once per warp; the sequence is identical in every warp
+          const int j = hit_seq++;
+          const int t0 = lane, nt = 32;
+#if CAMX_FUSE_SPLIT == 1
+          if ((j & 3) != warp) continue;
+#else
+          const int half = (warp - 2 * j) & 3;
+          if (half > 1) continue;
+#endif
+#endif
           const uint32_t o = __shfl_sync(0xffffffffu, offs, src);
           const uint32_t wp = __shfl_sync(0xffffffffu, wpk, src);
           const int x3 = __shfl_sync(0xffffffffu, xc3, src);
           const int lh = __shfl_sync(0xffffffffu, lohi, src);
           const uint32_t tl = __shfl_sync(0xffffffffu, static_cast<uint32_t>(trow), src);
           const uint32_t th = __shfl_sync(0xffffffffu, static_cast<uint32_t>(trow >> 32), src);
+          int hlo = lh & 0xFFFF, hhi = lh >> 16;
+#if CAMX_FUSE_SPLIT == 2
+          const int mid = hlo + ((hhi - hlo + 1) >> 1);
+          if (half == 0) hhi = mid; else hlo = mid;
+#endif
           resample_hit(ringb, o & 0xFFFFu, o >> 16, wp, x3,
                           reinterpret_cast<uint8_t *>((static_cast<uint64_t>(th) << 32) | tl),
-                          lh & 0xFFFF, lh >> 16, threadIdx.x, kApplyThreads, fs);
+                          hlo, hhi, t0, nt, fs);
         }
       }
     } else {
