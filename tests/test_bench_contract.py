@@ -48,3 +48,25 @@ def test_camx_arm_needs_a_gpu():
     r = _run(["--steps", "1", "--warmup", "0", "--no-e2e", "--no-cpu-baseline"])
     assert r.returncode != 0
     assert "CUDA" in (r.stderr + r.stdout) or "cuda" in (r.stderr + r.stdout)
+
+
+@pytest.mark.gpu
+def test_camx_arm_json_line_on_gpu():
+    """The camx arm's line carries the contract keys: roofline (measured K3
+    launches), clocks sampled in the timed region, e2e through the host path,
+    and a non-zero count of our own kernel launches."""
+    r = _run(["--steps", "3", "--warmup", "3", "--batch", "4", "--e2e-batch", "2",
+              "--no-cpu-baseline"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip()][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "clocks", "e2e", "gpu_launches"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and 0 < rf["achieved"] <= 1.2 * rf["peak"]
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 3 * d["steps"]
+    assert "workload" in d["config"]
