@@ -1070,19 +1070,22 @@ def test_full_size_config4_wrap_vs_oracle():
 
 
 @pytest.mark.parametrize("t_diff", [-1, 0, 20, 255])
-def test_window_counts_quad_path_vs_oracle(t_diff):
-    """The quad-vectorised K4 (W % 4 == 0): random windows at unaligned
-    origins (edge pixels through the scalar path), windows hanging off a
-    camera shard, both the fused frame difference and a given mask."""
-    rng = np.random.default_rng(31 + t_diff)
-    N, H, W, S = 3, 140, 96, 61
+@pytest.mark.parametrize("W,n_win", [(96, 40), (100, 40), (96, 300)])
+def test_window_counts_quad_path_vs_oracle(t_diff, W, n_win):
+    """The vectorised K4 paths: W % 16 == 0 -> one-pass tile kernel (300
+    windows: several chunks of the CTA's window scan and more than 8
+    windows per tile), W % 4 == 0 -> per-window quad kernel.  Random
+    windows at unaligned origins, windows hanging off a camera shard, both
+    the fused frame difference and a given mask."""
+    rng = np.random.default_rng(31 + t_diff + W + n_win)
+    N, H, S = 3, 140, 61
     cur = rng.integers(0, 256, (N, H, W, 3), dtype=np.uint8)
     prev = cur.copy()
     sel = rng.random((N, H, W)) < 0.2
     prev[sel] = rng.integers(0, 256, (int(sel.sum()), 3), dtype=np.uint8)
     full = np.concatenate([O.mask_diff(cur[c], prev[c], t_diff) for c in range(N)], axis=1)
     org = [(int(rng.integers(-40, N * W - S + 40)), int(rng.integers(0, H - S + 1)))
-           for _ in range(40)]
+           for _ in range(n_win)]
     want = []
     for (x, y) in org:
         x0, x1 = max(x, 0), min(x + S, N * W)
