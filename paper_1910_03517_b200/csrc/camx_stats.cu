@@ -95,6 +95,13 @@ constexpr int kStatsWarps = CAMX_K1_WARPS;
 #define CAMX_K1_QB 6
 #endif
 constexpr int kQuadBatchMax = CAMX_K1_QB;
+#ifndef CAMX_K1_G16
+#define CAMX_K1_G16 2
+#endif
+#ifndef CAMX_K1_G16_REMOVAL
+#define CAMX_K1_G16_REMOVAL 1
+#endif
+constexpr int kG16Groups = CAMX_K1_G16, kG16GroupsRemoval = CAMX_K1_G16_REMOVAL;
 // Histograms: per-warp [3][256] uint32 bins in shared memory, one atomic
 // per (kept pixel, channel).  (A band block is only 3,072 pixels: per-lane
 // private byte counters - conflict-free, but a 768-word flush and re-zero
@@ -174,14 +181,17 @@ __device__ __forceinline__ uint32_t quad_exclusion(const StatsParams &p, const u
   return 0u;
 }
 
-template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
+template <bool HIST, int MASKMODE, int QUAD, bool FUSE>
 __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t unit,
                                            uint32_t *smem, uint64_t (*part)[13]) {
   // quads per lane per step: 6 (18 loads in flight; a default 96-row x
   // 32-px band block is 768 quads = exactly 6 per thread of the CTA); the
   // motion-mask path also loads the previous frame's words: 3 (fewer
   // registers, more CTAs per SM).  Measured: tools/k1_probe.py
-  constexpr int kQuadBatch = MASKMODE == 2 ? CAMX_K1_QB_REMOVAL : kQuadBatchMax;
+  // QUAD 2: 16-pixel groups (48 bytes = 3 x 16-byte loads) of 4 quads,
+  // kG16Groups per lane per step - 2.7x the bytes in flight per load slot
+  constexpr int kQuadBatch = QUAD == 2 ? 4 * (MASKMODE == 2 ? kG16GroupsRemoval : kG16Groups)
+                             : MASKMODE == 2 ? CAMX_K1_QB_REMOVAL : kQuadBatchMax;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   constexpr int kStride = 32 * kStatsWarps;  // quads (pixels) per CTA-wide step
@@ -217,9 +227,46 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
     const int nq = rows * qpr;
     const bool pow2 = (qpr & (qpr - 1)) == 0;
     const int qsh = __ffs(qpr) - 1;
-    for (int i0 = warp * 32; i0 < nq; i0 += kStride * kQuadBatch) {
+    const int gpr = p.bw >> 4;  // QUAD 2: groups per row
+    const bool gpow2 = (gpr & (gpr - 1)) == 0;
+    const int gsh = __ffs(gpr) - 1;
+    const int n_items = QUAD == 2 ? rows * gpr : nq;
+    constexpr int kItemBatch = QUAD == 2 ? kQuadBatch / 4 : kQuadBatch;
+    for (int i0 = warp * 32; i0 < n_items; i0 += kStride * kItemBatch) {
       uint32_t w[kQuadBatch][3], pw[kQuadBatch][3], mw[kQuadBatch];
       bool live[kQuadBatch];
+      if (QUAD == 2) {
+#pragma unroll
+        for (int ug = 0; ug < kItemBatch; ++ug) {
+          const int gi = i0 + ug * kStride + lane;
+          const bool lv = gi < n_items;
+          const int ii = lv ? gi : 0;
+          const int rq = gpow2 ? (ii >> gsh) : ii / gpr;
+          const int64_t off = (r0 + rq) * row_bytes +
+                              static_cast<int64_t>(col0 + (ii - rq * gpr) * 16) * 3;
+          const uint4 *vp = reinterpret_cast<const uint4 *>(base + off);
+          const uint4 v0 = __ldg(vp), v1 = __ldg(vp + 1), v2 = __ldg(vp + 2);
+          const uint32_t g[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y,
+                                  v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+          uint32_t h[12];
+          if (MASKMODE == 2) {
+            const uint4 *pp = reinterpret_cast<const uint4 *>(pbase + off);
+            const uint4 q0 = __ldg(pp), q1 = __ldg(pp + 1), q2 = __ldg(pp + 2);
+            h[0] = q0.x; h[1] = q0.y; h[2] = q0.z; h[3] = q0.w;
+            h[4] = q1.x; h[5] = q1.y; h[6] = q1.z; h[7] = q1.w;
+            h[8] = q2.x; h[9] = q2.y; h[10] = q2.z; h[11] = q2.w;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            live[4 * ug + t] = lv;
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk) {
+              w[4 * ug + t][kk] = g[3 * t + kk];
+              if (MASKMODE == 2) pw[4 * ug + t][kk] = h[3 * t + kk];
+            }
+          }
+        }
+      } else {
 #pragma unroll
       for (int u = 0; u < kQuadBatch; ++u) {
         const int i = i0 + u * kStride + lane;
@@ -241,6 +288,7 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
         }
         if (MASKMODE == 1)
           mw[u] = __ldg(reinterpret_cast<const uint32_t *>(mbase + static_cast<int64_t>(row) * p.W + col));
+      }
       }
       if (MASKMODE != 1) {
         // Channel sums / sums of squares with dp4a: in a quad the byte
@@ -431,7 +479,7 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
 // Persistent: a grid of a few CTAs per SM loops over the (image, side,
 // block) units, so the short per-unit load -> reduce phases of resident
 // CTAs overlap instead of running as many launch waves.
-template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
+template <bool HIST, int MASKMODE, int QUAD, bool FUSE>
 __global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const StatsParams p) {
   extern __shared__ uint32_t smem[];
   __shared__ uint64_t part[kStatsWarps][13];
@@ -444,7 +492,7 @@ __global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const Stat
   }
 }
 
-template <bool HIST, int MASKMODE, bool QUAD, bool FUSE>
+template <bool HIST, int MASKMODE, int QUAD, bool FUSE>
 static void launch_stats(const StatsParams &p, cudaStream_t s) {
   const int warps = kStatsWarps;
   const size_t smem = HIST ? static_cast<size_t>(warps) * kHistWords * sizeof(uint32_t) : 0;
@@ -464,12 +512,25 @@ static void launch_stats(const StatsParams &p, cudaStream_t s) {
       <<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(p);
 }
 
+// 16-pixel groups: whole 16-byte-aligned 48-byte runs in every band row
+static bool k1_g16(const StatsParams &p) {
+  static const bool enabled = [] {
+    const char *e = getenv("CAMX_K1_G16");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  auto al16 = [](const void *x) { return reinterpret_cast<uintptr_t>(x) % 16 == 0; };
+  return enabled && p.bw % 16 == 0 && (3 * p.W) % 16 == 0 && (3 * (p.W - p.bw)) % 16 == 0 &&
+         al16(p.img) && (p.prev == nullptr || al16(p.prev)) && p.mask == nullptr;
+}
+
 template <bool HIST, int MASKMODE, bool FUSE = false>
 static void launch_stats_q(const StatsParams &p, bool quad, cudaStream_t s) {
-  if (quad)
-    launch_stats<HIST, MASKMODE, true, FUSE>(p, s);
+  if (quad && MASKMODE != 1 && k1_g16(p))
+    launch_stats<HIST, MASKMODE, 2, FUSE>(p, s);
+  else if (quad)
+    launch_stats<HIST, MASKMODE, 1, FUSE>(p, s);
   else
-    launch_stats<HIST, MASKMODE, false, FUSE>(p, s);
+    launch_stats<HIST, MASKMODE, 0, FUSE>(p, s);
 }
 
 // ---- moments --------------------------------------------------------------
