@@ -15,6 +15,8 @@
 // seam_cost: exposure.py:417-445 (box downsample, Eq. 1 of the paper).
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "camx_resize.cuh"
 
 namespace camx {
@@ -599,33 +601,84 @@ __device__ __forceinline__ void box_mean(const uint8_t *img, int W, int f, int r
   for (int ch = 0; ch < 3; ++ch) out[ch] = __ddiv_rn(static_cast<double>(s[ch]), n);
 }
 
-__global__ void seam_cost_kernel(const uint8_t *left, const uint8_t *right, int H, int WL, int WR,
-                                 int f, double *cost) {
+// One CTA per pair; thread = one (downsampled row, box) of the four boxes a
+// row needs (left columns w2-2, w2-1; right columns 0, 1), so all the box
+// loads of a pair are in flight at once (the four boxes of a row sit in four
+// consecutive lanes and meet by shuffles).  Row costs are summed in a fixed
+// order (lane tree, then warps in order, then passes): deterministic.
+// f == 8 with 8-byte aligned rows: a box row is 24 bytes = 3 x 8-byte loads
+// = 6 words whose channel pattern repeats every 3 words (r g b r | g b r g |
+// b r g b), so per-channel byte sums are dp4a with constant masks.
+__device__ __forceinline__ void box_mean8(const uint8_t *img, int W, int row2, int col2,
+                                          double out[3]) {
+  uint32_t s[3] = {0, 0, 0};
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const uint2 *q = reinterpret_cast<const uint2 *>(
+        img + (static_cast<int64_t>(row2 * 8 + r) * W + col2 * 8) * 3);
+    const uint2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    const uint32_t w[6] = {a.x, a.y, b.x, b.y, c.x, c.y};
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const int sh = (ch + 3 - k % 3) % 3;  // byte positions of channel ch in word k
+        const uint32_t sel = sh == 0 ? 0x01000001u : sh == 1 ? 0x00000100u : 0x00010000u;
+        s[ch] = __dp4a(w[k], sel, s[ch]);
+      }
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) out[ch] = __ddiv_rn(static_cast<double>(s[ch]), 64.0);
+}
+
+__global__ void __launch_bounds__(1024) seam_cost_kernel(const uint8_t *left, const uint8_t *right,
+                                                         int H, int WL, int WR, int f,
+                                                         double *cost) {
+  const bool vec8 = f == 8 && (3 * WL) % 8 == 0 && (3 * WR) % 8 == 0 &&
+                    reinterpret_cast<uintptr_t>(left) % 8 == 0 &&
+                    reinterpret_cast<uintptr_t>(right) % 8 == 0;
   const int64_t pair = blockIdx.x;
   const uint8_t *L = left + pair * static_cast<int64_t>(H) * WL * 3;
   const uint8_t *R = right + pair * static_cast<int64_t>(H) * WR * 3;
   const int h2 = H / f, wl2 = WL / f;
+  const int lane = threadIdx.x & 31;
   double acc = 0.0;
-  for (int r = threadIdx.x; r < h2; r += blockDim.x) {
-    double lm1[3], l0[3], r0[3], r1[3];
-    box_mean(L, WL, f, r, wl2 - 2, lm1);
-    box_mean(L, WL, f, r, wl2 - 1, l0);
-    box_mean(R, WR, f, r, 0, r0);
-    box_mean(R, WR, f, r, 1, r1);
-    double dp = 0.0, dm = 0.0;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      const double a = __dsub_rn(__dsub_rn(r1[ch], r0[ch]), __dsub_rn(r0[ch], l0[ch]));
-      const double b = __dsub_rn(__dsub_rn(lm1[ch], l0[ch]), __dsub_rn(l0[ch], r0[ch]));
-      dp = __dadd_rn(dp, __dmul_rn(a, a));
-      dm = __dadd_rn(dm, __dmul_rn(b, b));
+  for (int i0 = 0; i0 < 4 * h2; i0 += blockDim.x) {  // CTA-uniform trip count
+    const int i = i0 + threadIdx.x;
+    const int row = i >> 2, box = i & 3;
+    double m[3] = {0.0, 0.0, 0.0};
+    if (row < h2) {
+      const uint8_t *img = box < 2 ? L : R;
+      const int W = box < 2 ? WL : WR;
+      const int col2 = box == 0 ? wl2 - 2 : box == 1 ? wl2 - 1 : box - 2;
+      if (vec8) {
+        box_mean8(img, W, row, col2, m);
+      } else {
+        box_mean(img, W, f, row, col2, m);
+      }
     }
-    acc += __ddiv_rn(__dadd_rn(sqrt(dp), sqrt(dm)), 2.0);
+    // lanes 4q .. 4q+3: lm1, l0, r0, r1 of one row
+    double v[4][3];
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) v[b][ch] = __shfl_sync(0xffffffffu, m[ch], (lane & ~3) | b);
+    if (box == 0 && row < h2) {
+      double dp = 0.0, dm = 0.0;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const double a = __dsub_rn(__dsub_rn(v[3][ch], v[2][ch]), __dsub_rn(v[2][ch], v[1][ch]));
+        const double b = __dsub_rn(__dsub_rn(v[0][ch], v[1][ch]), __dsub_rn(v[1][ch], v[2][ch]));
+        dp = __dadd_rn(dp, __dmul_rn(a, a));
+        dm = __dadd_rn(dm, __dmul_rn(b, b));
+      }
+      acc += __ddiv_rn(__dadd_rn(sqrt(dp), sqrt(dm)), 2.0);
+    }
   }
   __shared__ double part[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  if (lane == 0) part[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
@@ -744,7 +797,9 @@ extern "C" int camx_seam_cost(const uint8_t *left, const uint8_t *right, int64_t
   if (n_pairs < 0 || !left || !right || !cost_out || factor < 1) return CAMX_EINVAL;
   if (height / factor < 1 || left_width / factor < 2 || right_width / factor < 2) return CAMX_EINVAL;
   if (n_pairs == 0) return CAMX_OK;
-  seam_cost_kernel<<<static_cast<unsigned>(n_pairs), 128, 0, as_stream(stream)>>>(
+  const int items = 4 * (height / factor);
+  const int threads = std::min(1024, (items + 31) & ~31);
+  seam_cost_kernel<<<static_cast<unsigned>(n_pairs), threads, 0, as_stream(stream)>>>(
       left, right, height, left_width, right_width, factor, cost_out);
   return launch_status();
 }

@@ -96,6 +96,26 @@ def test_seam_cost_golden():
                                                                           rel=1e-12)
 
 
+@pytest.mark.parametrize("H,WL,WR,f", [(1536, 2048, 2048, 8), (100, 128, 96, 8), (64, 100, 64, 4),
+                                      (61, 37, 45, 3)])
+def test_seam_cost_vector_and_scalar_paths(H, WL, WR, f):
+    """camx_seam_cost: the 8-byte-load path (f = 8, rows 8-byte aligned) and
+    the per-byte path, against the oracle restatement of exposure.py:417-445;
+    several pairs in one call (the C API's batch)."""
+    rng = np.random.default_rng(H + WL + f)
+    from paper_1910_03517_b200 import _lib
+    n = 3
+    L = rng.integers(0, 256, (n, H, WL, 3), dtype=np.uint8)
+    R = rng.integers(0, 256, (n, H, WR, 3), dtype=np.uint8)
+    dl, dr = torch.from_numpy(L).cuda(), torch.from_numpy(R).cuda()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.call("camx_seam_cost", dl.data_ptr(), dr.data_ptr(), n, H, WL, WR, f, out.data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    got = out.cpu().numpy()
+    for i in range(n):
+        assert got[i] == pytest.approx(O.seam_cost(L[i], R[i], f), rel=1e-12)
+
+
 MODES = [("standard", xp.ExposureMode.STANDARD, O.STANDARD),
          ("object_removal", xp.ExposureMode.OBJECT_REMOVAL, O.OBJECT_REMOVAL),
          ("smoothing", xp.ExposureMode.SMOOTHING, O.SMOOTHING)]
