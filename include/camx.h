@@ -361,7 +361,8 @@ int camx_correct_batch_tiles(
  * component's first pixel, xmin, ymin, xmax, ymax (window coordinates,
  * inclusive), on-pixels of ANY component inside that box (detect.py:241)),
  * in scipy label order; *n_comp_out = number of components (may exceed
- * max_comp).  scratch: 16-byte aligned int32 [6 * size * size + 2 * size + 1]
+ * max_comp).  scratch: 16-byte aligned int32 [6 * size * size + 2 * size + 1 +
+ * (size * size + 1023) / 1024]
  * device memory. */
 int camx_blob_components(const uint8_t *mask, int32_t n_cams, int32_t height,
                          int32_t width, int32_t x0, int32_t y0, int32_t size,

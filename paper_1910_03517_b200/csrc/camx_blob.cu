@@ -13,7 +13,7 @@
 //   3. flatten  parent[i] = root(i); the root is the component's raster-first
 //               pixel, so sorting roots reproduces scipy's label order
 //   4. boxes    per-root atomic min/max of (x, y); roots compacted in
-//               raster order by a single-CTA ballot scan
+//               raster order (per-block counts, one scan, ballot ranks)
 //   5. counts   summed-area table of the window mask (row scan + column
 //               scan), 4 lookups per box
 #include <algorithm>
@@ -119,7 +119,44 @@ __global__ void blob_sat_rows_kernel(const BlobParams p) {
   }
 }
 
-__global__ void blob_sat_cols_kernel(const BlobParams p) {
+// Column prefix of the row-scanned table: CTA = 32 columns x 32 row chunks;
+// thread (column, chunk) keeps its chunk's values in registers, the 32 chunk
+// sums of a column are scanned in shared memory, then the chunk is written
+// back with its offset (31 CTAs x 1024 threads for a 960 window, where one
+// thread per column walked 960 dependent rows).
+constexpr int kSatChunkMax = 32;  // rows per chunk: size <= 32 * 32 = 1024 (else the serial kernel)
+__global__ void __launch_bounds__(1024) blob_sat_cols_kernel(const BlobParams p) {
+  __shared__ int tot[32][33];
+  const int S1 = p.size + 1;
+  const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const int x = blockIdx.x * 32 + cx;
+  const int R = (p.size + 31) / 32;  // rows per chunk (rows 1..size)
+  const int y0 = 1 + ry * R, y1 = min(p.size + 1, y0 + R);
+  int v[kSatChunkMax];
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < kSatChunkMax; ++k) {
+    const int y = y0 + k;
+    v[k] = (k < R && y < y1 && x < S1) ? p.sat[y * S1 + x] : 0;
+    sum += v[k];
+  }
+  tot[ry][cx] = sum;
+  __syncthreads();
+  int off = 0;
+  for (int j = 0; j < ry; ++j) off += tot[j][cx];
+  if (x < S1) {
+    if (ry == 0) p.sat[x] = 0;
+#pragma unroll
+    for (int k = 0; k < kSatChunkMax; ++k) {
+      const int y = y0 + k;
+      if (k < R && y < y1) {
+        off += v[k];
+        p.sat[y * S1 + x] = off;
+      }
+    }
+  }
+}
+__global__ void blob_sat_cols_serial_kernel(const BlobParams p) {  // size > 1024
   const int S1 = p.size + 1;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < S1; x += gridDim.x * blockDim.x) {
     p.sat[x] = 0;
@@ -131,48 +168,76 @@ __global__ void blob_sat_cols_kernel(const BlobParams p) {
   }
 }
 
-// Roots in raster order (single CTA, ballot compaction): comp[k] = (root,
-// xmin, ymin, xmax, ymax, count-in-box).
-__global__ void __launch_bounds__(1024) blob_collect_kernel(const BlobParams p, int32_t *comp,
-                                                             int32_t max_comp, int32_t *n_comp) {
-  __shared__ int warp_tot[32];
-  __shared__ int base;
-  if (threadIdx.x == 0) base = 0;
+// Roots in raster order over many CTAs: (1) roots per 1024-pixel block,
+// (2) one CTA scans the block counts, (3) every block writes its roots at
+// its offset in raster order (ballot ranks), with the box's on-pixel count
+// from the summed-area table.
+__global__ void __launch_bounds__(1024) blob_root_count_kernel(const BlobParams p, int32_t *cnt) {
+  __shared__ int wt[32];
+  const int n = p.size * p.size;
+  const int i = blockIdx.x * 1024 + threadIdx.x;
+  const bool root = i < n && p.parent[i] == i;
+  const unsigned bal = __ballot_sync(0xffffffffu, root);
+  if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = __popc(bal);
   __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 32; ++w) t += wt[w];
+    cnt[blockIdx.x] = t;
+  }
+}
+__global__ void __launch_bounds__(1024) blob_scan_kernel(int32_t *cnt, int nb, int32_t *n_comp) {
+  __shared__ int carry;
+  __shared__ int wt[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b0 = 0; b0 < nb; b0 += 1024) {
+    const int b = b0 + threadIdx.x;
+    const int c = b < nb ? cnt[b] : 0;
+    int v = c;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) wt[warp] = v;
+    __syncthreads();
+    int before = carry;
+    for (int w = 0; w < warp; ++w) before += wt[w];
+    if (b < nb) cnt[b] = before + v - c;  // exclusive offset
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = before + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_comp = carry;
+}
+__global__ void __launch_bounds__(1024) blob_emit_kernel(const BlobParams p, const int32_t *off,
+                                                         int32_t *comp, int32_t max_comp) {
+  __shared__ int wt[32];
   const int n = p.size * p.size;
   const int S1 = p.size + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-    const int i = i0 + threadIdx.x;
-    const bool root = i < n && p.parent[i] == i;
-    const unsigned bal = __ballot_sync(0xffffffffu, root);
-    if (lane == 0) warp_tot[warp] = __popc(bal);
-    __syncthreads();
-    int before = 0, total = 0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
-      if (w < warp) before += warp_tot[w];
-      total += warp_tot[w];
-    }
-    if (root) {
-      const int k = base + before + __popc(bal & ((1u << lane) - 1u));
-      if (k < max_comp) {
-        const int4 b = reinterpret_cast<const int4 *>(p.box)[i];
-        const int cnt = p.sat[(b.w + 1) * S1 + b.z + 1] - p.sat[b.y * S1 + b.z + 1] -
-                        p.sat[(b.w + 1) * S1 + b.x] + p.sat[b.y * S1 + b.x];
-        int32_t *c = comp + 6 * k;
-        c[0] = i;
-        c[1] = b.x;
-        c[2] = b.y;
-        c[3] = b.z;
-        c[4] = b.w;
-        c[5] = cnt;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) base += total;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *n_comp = base;
+  const int i = blockIdx.x * 1024 + threadIdx.x;
+  const bool root = i < n && p.parent[i] == i;
+  const unsigned bal = __ballot_sync(0xffffffffu, root);
+  if (lane == 0) wt[warp] = __popc(bal);
+  __syncthreads();
+  if (!root) return;
+  int before = off[blockIdx.x];
+  for (int w = 0; w < warp; ++w) before += wt[w];
+  const int k = before + __popc(bal & ((1u << lane) - 1u));
+  if (k >= max_comp) return;
+  const int4 b = reinterpret_cast<const int4 *>(p.box)[i];
+  const int c = p.sat[(b.w + 1) * S1 + b.z + 1] - p.sat[b.y * S1 + b.z + 1] -
+                p.sat[(b.w + 1) * S1 + b.x] + p.sat[b.y * S1 + b.x];
+  int32_t *o = comp + 6 * k;
+  o[0] = i;
+  o[1] = b.x;
+  o[2] = b.y;
+  o[3] = b.z;
+  o[4] = b.w;
+  o[5] = c;
 }
 
 }  // namespace camx
@@ -207,7 +272,14 @@ extern "C" int camx_blob_components(const uint8_t *mask, int32_t n_cams, int32_t
   blob_union_kernel<<<blocks, 256, 0, s>>>(p);
   blob_flatten_kernel<<<blocks, 256, 0, s>>>(p);
   blob_sat_rows_kernel<<<std::min(size, sm_count() * 16), 32, 0, s>>>(p);
-  blob_sat_cols_kernel<<<(size + 1 + 127) / 128, 128, 0, s>>>(p);
-  blob_collect_kernel<<<1, 1024, 0, s>>>(p, comp_out, max_comp, n_comp_out);
+  if (size <= 32 * kSatChunkMax)
+    blob_sat_cols_kernel<<<(size + 1 + 31) / 32, 1024, 0, s>>>(p);
+  else
+    blob_sat_cols_serial_kernel<<<(size + 1 + 127) / 128, 128, 0, s>>>(p);
+  const int nb = static_cast<int>((n + 1023) / 1024);
+  int32_t *cnt = p.sat + static_cast<int64_t>(size + 1) * (size + 1);  // [nb] block offsets
+  blob_root_count_kernel<<<nb, 1024, 0, s>>>(p, cnt);
+  blob_scan_kernel<<<1, 1024, 0, s>>>(cnt, nb, n_comp_out);
+  blob_emit_kernel<<<nb, 1024, 0, s>>>(p, cnt, comp_out, max_comp);
   return launch_status();
 }

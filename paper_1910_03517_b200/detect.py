@@ -211,7 +211,8 @@ def blob_components(mask, window: DetectorWindow, n_cams: int = 1, max_comp: int
     m = m.reshape(n_cams, *m.shape[-2:]).contiguous()
     H, W = m.shape[-2:]
     S = int(window.size)
-    scratch = t.empty((6 * S * S + 2 * S + 1 + 3,), dtype=t.int32, device="cuda")
+    scratch = t.empty((6 * S * S + 2 * S + 1 + (S * S + 1023) // 1024 + 3,), dtype=t.int32,
+                      device="cuda")
     comp = t.empty((max_comp, 6), dtype=t.int32, device="cuda")
     n = t.zeros((1,), dtype=t.int32, device="cuda")
     _lib.call("camx_blob_components", m.data_ptr(), int(n_cams), int(H), int(W), int(window.x),

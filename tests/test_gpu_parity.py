@@ -728,6 +728,19 @@ class TestBlobDetector:               # test_detect.py:155-179 + scipy oracle
             want = O.blob_components(mosaic[y:y + s, x:x + s])
             np.testing.assert_array_equal(got[:, 1:], want)
 
+    @pytest.mark.parametrize("size,p", [(960, 0.01), (1100, 0.3)])
+    def test_large_windows_vs_scipy(self, size, p):
+        """Windows of detector size: the chunked summed-area column scan (960)
+        and the serial one (> 1024), root compaction over > 1024 blocks."""
+        rng = np.random.default_rng(size)
+        N, H, W = 2, size + 8, 600
+        masks = rng.random((N, H, W)) < p
+        mosaic = np.concatenate(list(masks), axis=1)
+        x, y = 70, 5
+        got = detect.blob_components(masks, detect.DetectorWindow(x, y, size), n_cams=N)
+        want = O.blob_components(mosaic[y:y + size, x:x + size])
+        np.testing.assert_array_equal(got[:, 1:], want)
+
 
 @pytest.mark.parametrize("mode", [xp.ExposureMode.SMOOTHING, xp.ExposureMode.OBJECT_REMOVAL])
 def test_graph_replay_matches_eager(mode):

@@ -12,7 +12,8 @@ fr = synthetic_batch(2, N, H, W, seed=7)
 mask = torch.empty((N, H, W), dtype=torch.uint8, device="cuda")
 _lib.call("camx_mask_diff", fr[1].data_ptr(), fr[0].data_ptr(), N * H * W, 20, mask.data_ptr(),
           None)
-scratch = torch.empty((6 * S * S + 2 * S + 1 + 3,), dtype=torch.int32, device="cuda")
+scratch = torch.empty((6 * S * S + 2 * S + 1 + (S * S + 1023) // 1024 + 3,), dtype=torch.int32,
+                      device="cuda")
 comp = torch.empty((65536, 6), dtype=torch.int32, device="cuda")
 n = torch.zeros((1,), dtype=torch.int32, device="cuda")
 
