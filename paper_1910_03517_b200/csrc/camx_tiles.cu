@@ -246,6 +246,19 @@ __global__ void tiles_shard_kernel(const ShardTileParams p) {
   }
 }
 
+// 16-byte global -> shared copies without a register round trip
+// (cp.async.cg: every copy of a band in flight at once, instead of one
+// load -> store latency per element of the staging loop).
+__device__ __forceinline__ void stage16(void *smem_dst, const void *gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void stage_wait() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // Band-staged downscale kernel (out < size, size <= W, 16-byte aligned
 // rows): CTA = (tile, band of kBandRows output rows).  The 2 x kBandRows
 // source rows of the band (the two taps of each output row; a strict
@@ -353,8 +366,7 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TilePara
         const bool first = v < nv0;
         const uint4 *src = reinterpret_cast<const uint4 *>(first ? src0_s[r] : src1_s[r]) +
                            (first ? v : v - nv0);
-        *reinterpret_cast<uint4 *>(rows + r * pitch + (first ? v * 16 : off1 + (v - nv0) * 16)) =
-            __ldg(src);
+        stage16(rows + r * pitch + (first ? v * 16 : off1 + (v - nv0) * 16), src);
         r += step_r;
         v += step_v;
         if (v >= nv) {
@@ -362,6 +374,7 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TilePara
           ++r;
         }
       }
+      stage_wait();
     }
     __syncthreads();
     int ol = threadIdx.x / out, ox = threadIdx.x - ol * out;
@@ -521,8 +534,7 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_shard_kernel(const Sh
         const bool first = v < nv0;
         const uint4 *src = reinterpret_cast<const uint4 *>(first ? src0_s[r] : src1_s[r]) +
                            (first ? v : v - nv0);
-        *reinterpret_cast<uint4 *>(rows + r * pitch + (first ? v * 16 : off1 + (v - nv0) * 16)) =
-            __ldg(src);
+        stage16(rows + r * pitch + (first ? v * 16 : off1 + (v - nv0) * 16), src);
         r += step_r;
         v += step_v;
         if (v >= nv) {
@@ -530,6 +542,7 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_shard_kernel(const Sh
           ++r;
         }
       }
+      stage_wait();
     }
     __syncthreads();
     int ol = threadIdx.x / width, ox = threadIdx.x - ol * width;
