@@ -377,42 +377,45 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TilePara
       stage_wait();
     }
     __syncthreads();
-    int ol = threadIdx.x / out, ox = threadIdx.x - ol * out;
-    const int step_l = blockDim.x / out, step_x = blockDim.x - step_l * out;
-    while (ol < nr) {
-      const uint2 tv = tap[ox];
-      const uint32_t wyp = wy_s[ol];
-      const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
-      const uint8_t *ra = rows + (2 * ol) * pitch;
-      const uint8_t *rb = ra + pitch;
-      uint8_t *o = orow + ol * O3 + 3 * ox;
-      if (!(tv.x & kTapStraddle)) {
-        const uint32_t la = tv.x;
-        const uint32_t sh = la * 8u;
-        const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
-        const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
-        const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
-        const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
+    // warp-per-(row, column range): the row's weights and pointers are set
+    // once per unit, lanes stride the columns (no per-pixel index stepping)
+    {
+      constexpr int kUnitsPerRow = (kBandThreads / 32) / kBandRows > 0 ? (kBandThreads / 32) / kBandRows : 1;
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int u = warp; u < nr * kUnitsPerRow; u += kBandThreads / 32) {
+        const int ol = u / kUnitsPerRow, part = u - ol * kUnitsPerRow;
+        const int c0 = part * out / kUnitsPerRow, c1 = (part + 1) * out / kUnitsPerRow;
+        const uint32_t wyp = wy_s[ol];
+        const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
+        const uint8_t *ra = rows + (2 * ol) * pitch;
+        const uint8_t *rb = ra + pitch;
+        uint8_t *orow_l = orow + ol * O3;
+        for (int ox = c0 + lane; ox < c1; ox += 32) {
+          const uint2 tv = tap[ox];
+          uint8_t *o = orow_l + 3 * ox;
+          if (!(tv.x & kTapStraddle)) {
+            const uint32_t la = tv.x;
+            const uint32_t sh = la * 8u;
+            const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
+            const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
+            const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
+            const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
-          const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
-          const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
-          o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+            for (int ch = 0; ch < 3; ++ch) {
+              const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
+              const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
+              const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
+              o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+            }
+          } else {  // first tap = last pixel of segment 0, second = first of segment 1
+            const uint32_t a0 = tv.x & ~kTapStraddle;
+            const uint32_t w1 = tv.y >> 16;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+              o[ch] = static_cast<uint8_t>(bilerp_fx(ra[a0 + ch], ra[a1_straddle + ch], rb[a0 + ch],
+                                                     rb[a1_straddle + ch], w1, wy1));
+          }
         }
-      } else {  // first tap = last pixel of segment 0, second = first of segment 1
-        const uint32_t a0 = tv.x & ~kTapStraddle;
-        const uint32_t w1 = tv.y >> 16;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch)
-          o[ch] = static_cast<uint8_t>(bilerp_fx(ra[a0 + ch], ra[a1_straddle + ch], rb[a0 + ch],
-                                                 rb[a1_straddle + ch], w1, wy1));
-      }
-      ol += step_l;
-      ox += step_x;
-      if (ox >= out) {
-        ox -= out;
-        ++ol;
       }
     }
     __syncthreads();
