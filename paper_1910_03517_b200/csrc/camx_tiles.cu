@@ -548,49 +548,50 @@ __global__ void __launch_bounds__(kBandThreads) tiles_band_shard_kernel(const Sh
       stage_wait();
     }
     __syncthreads();
-    int ol = threadIdx.x / width, ox = threadIdx.x - ol * width;
-    const int step_l = blockDim.x / width, step_x = blockDim.x - step_l * width;
-    while (ol < nr) {
-      const int gox = ox_lo + ox;
-      const uint2 tv = tap[gox];
-      const uint32_t wyp = wy_s[ol];
-      const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
-      const uint8_t *ra = rows + (2 * ol) * pitch;
-      const uint8_t *rb = ra + pitch;
-      uint8_t *o = orow + ol * O3 + 3 * gox;
-      if (!(tv.x & kTapFlags)) {
-        const uint32_t la = tv.x;
-        const uint32_t sh = la * 8u;
-        const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
-        const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
-        const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
-        const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
+    // warp per (row, column half of the owned range), lanes stride the columns
+    {
+      constexpr int kUnitsPerRow = (kBandThreads / 32) / kBandRows > 0 ? (kBandThreads / 32) / kBandRows : 1;
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int u = warp; u < nr * kUnitsPerRow; u += kBandThreads / 32) {
+        const int ol = u / kUnitsPerRow, part = u - ol * kUnitsPerRow;
+        const int c0 = part * width / kUnitsPerRow, c1 = (part + 1) * width / kUnitsPerRow;
+        const uint32_t wyp = wy_s[ol];
+        const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
+        const uint8_t *ra = rows + (2 * ol) * pitch;
+        const uint8_t *rb = ra + pitch;
+        for (int ox = c0 + lane; ox < c1; ox += 32) {
+          const int gox = ox_lo + ox;
+          const uint2 tv = tap[gox];
+          uint8_t *o = orow + ol * O3 + 3 * gox;
+          if (!(tv.x & kTapFlags)) {
+            const uint32_t la = tv.x;
+            const uint32_t sh = la * 8u;
+            const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
+            const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
+            const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
+            const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const uint32_t sel = 0x0030u + 0x0011u * ch;
-          const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
-          const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
-          o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
-        }
-      } else {
-        const uint32_t a0 = tv.x & ~kTapFlags;
-        const uint32_t w1 = tv.y >> 16;
-        const bool use_halo = (tv.x & kTapHalo) != 0;
-        const uint8_t *ha = sp.halo + (b * p.H + srow_s[2 * ol]) * 3;
-        const uint8_t *hb = sp.halo + (b * p.H + srow_s[2 * ol + 1]) * 3;
+            for (int ch = 0; ch < 3; ++ch) {
+              const uint32_t sel = 0x0030u + 0x0011u * ch;
+              const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
+              const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
+              o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+            }
+          } else {
+            const uint32_t a0 = tv.x & ~kTapFlags;
+            const uint32_t w1 = tv.y >> 16;
+            const bool use_halo = (tv.x & kTapHalo) != 0;
+            const uint8_t *ha = sp.halo + (b * p.H + srow_s[2 * ol]) * 3;
+            const uint8_t *hb = sp.halo + (b * p.H + srow_s[2 * ol + 1]) * 3;
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const uint32_t A = ra[a0 + ch], C = rb[a0 + ch];
-          const uint32_t Bv = use_halo ? ha[ch] : ra[a1_seg1 + ch];
-          const uint32_t D = use_halo ? hb[ch] : rb[a1_seg1 + ch];
-          o[ch] = static_cast<uint8_t>(bilerp_fx(A, Bv, C, D, w1, wy1));
+            for (int ch = 0; ch < 3; ++ch) {
+              const uint32_t A = ra[a0 + ch], C = rb[a0 + ch];
+              const uint32_t Bv = use_halo ? ha[ch] : ra[a1_seg1 + ch];
+              const uint32_t D = use_halo ? hb[ch] : rb[a1_seg1 + ch];
+              o[ch] = static_cast<uint8_t>(bilerp_fx(A, Bv, C, D, w1, wy1));
+            }
+          }
         }
-      }
-      ol += step_l;
-      ox += step_x;
-      if (ox >= width) {
-        ox -= width;
-        ++ol;
       }
     }
     __syncthreads();
