@@ -314,14 +314,27 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
           uint32_t ex = 0u;
           if (MASKMODE == 2) ex = quad_exclusion<MASKMODE>(p, w[u], pw[u], mw[u]);
           if (HIST) {
+            // every pixel counted unconditionally (no per-pixel branch), the
+            // (rare) excluded ones taken back out
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              if ((ex >> e) & 1u) continue;
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
                 const int byte = 3 * e + c;  // compile-time position in the 12-byte quad
                 const uint32_t val = (w[u][byte >> 2] >> ((byte & 3) * 8)) & 0xFFu;
                 atomicAdd(cnt + c * 256 + val, 1u);
+              }
+            }
+            if (MASKMODE != 0 && ex != 0u) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                if (!((ex >> e) & 1u)) continue;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                  const int byte = 3 * e + c;
+                  const uint32_t val = (w[u][byte >> 2] >> ((byte & 3) * 8)) & 0xFFu;
+                  atomicSub(cnt + c * 256 + val, 1u);
+                }
               }
             }
           }
