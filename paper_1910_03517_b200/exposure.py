@@ -193,6 +193,18 @@ def _pixels(frame) -> np.ndarray:
     return frame.pixels if isinstance(frame, Frame) else np.asarray(frame)
 
 
+def _bands(px: np.ndarray, band_width: int) -> np.ndarray:
+    """The two seam bands of a frame packed side by side, (H, 2*bw[, 3]):
+    K1 over this image (width 2*bw) reads exactly the columns it would read
+    in the full frame (LEFT side = the last bw columns, RIGHT side = the
+    first bw), so the per-call drop-in ships ~2*bw/W of the frame over PCIe
+    instead of all of it."""
+    w = px.shape[1]
+    if 2 * band_width >= w:
+        return np.ascontiguousarray(px)
+    return np.concatenate((px[:, :band_width], px[:, w - band_width:]), axis=1)
+
+
 # ----------------------------------------------------------------- stage 1
 
 def band_stats(frame: Frame, side: Side, band_width: int, blocks: int,
@@ -203,13 +215,13 @@ def band_stats(frame: Frame, side: Side, band_width: int, blocks: int,
     h, w = frame.height, frame.width
     _check_band(w, band_width)
     block_bounds(h, blocks)
-    img = _dev.to_device(frame.pixels)[None]
+    img = _dev.to_device(_bands(frame.pixels, band_width))[None]
     msk = None
     if exclusion_mask is not None:
         m = np.asarray(exclusion_mask, dtype=bool)
         if m.shape != (h, w):
             raise ValueError(f"exclusion mask must be {(h, w)}, got {m.shape}")
-        msk = _dev.to_device(m.view(np.uint8))[None]
+        msk = _dev.to_device(_bands(m.view(np.uint8), band_width))[None]
     rec, _ = _stats_device(img, masks=msk, band_width=band_width, blocks=blocks)
     s = 0 if side is Side.LEFT else 1
     mean, std, valid, area = (_dev.to_host(x) for x in _moments(rec[0, s]))
@@ -296,12 +308,14 @@ def update_exposure(frames: tuple[Frame, Frame],
         # the array kernels index one geometry; fall back to per-side calls
         return _update_mixed_width(frames, prev_maps, mode, cfg, prev_frames)
     t = _dev.require_cuda()
-    imgs = _dev.to_device(np.stack([left_f.pixels, right_f.pixels]))
+    _check_band(left_f.width, cfg.band_width)
+    bw = cfg.band_width
+    imgs = _dev.to_device(np.stack([_bands(left_f.pixels, bw), _bands(right_f.pixels, bw)]))
     use_prev = mode is ExposureMode.OBJECT_REMOVAL and prev_frames is not None
-    prev = _dev.to_device(np.stack([prev_frames[0].pixels, prev_frames[1].pixels])) \
-        if use_prev else None
-    if prev is not None and prev.shape != imgs.shape:
+    if use_prev and any(pf.pixels.shape != f.pixels.shape for pf, f in zip(prev_frames, frames)):
         raise ValueError("pixel dimensions differ")
+    prev = _dev.to_device(np.stack([_bands(prev_frames[0].pixels, bw),
+                                    _bands(prev_frames[1].pixels, bw)])) if use_prev else None
     rec, _ = _stats_device(imgs, prev=prev, band_width=cfg.band_width, blocks=cfg.blocks,
                            t_diff=cfg.t_diff)
     return _solve_pair(rec.view(1, 2, 2, cfg.blocks, _lib.STAT_BYTES), prev_maps, mode, cfg,
@@ -333,13 +347,15 @@ def _update_mixed_width(frames, prev_maps, mode, cfg, prev_frames) -> SeamMaps:
     t = _dev.require_cuda()
     use_prev = mode is ExposureMode.OBJECT_REMOVAL and prev_frames is not None
     recs = []
+    bw = cfg.band_width
     for i, f in enumerate(frames):
-        img = _dev.to_device(f.pixels)[None]
+        _check_band(f.width, bw)
+        img = _dev.to_device(_bands(f.pixels, bw))[None]
         prev = None
         if use_prev:
-            prev = _dev.to_device(prev_frames[i].pixels)[None]
-            if prev.shape != img.shape:
+            if prev_frames[i].pixels.shape != f.pixels.shape:
                 raise ValueError("pixel dimensions differ")
+            prev = _dev.to_device(_bands(prev_frames[i].pixels, bw))[None]
         r, _ = _stats_device(img, prev=prev, band_width=cfg.band_width, blocks=cfg.blocks,
                              t_diff=cfg.t_diff)
         recs.append(r)
