@@ -340,6 +340,9 @@ constexpr int kFuseMaxWin = 48;  // windows per array-frame the fused path accep
 // window (orow[] is well defined)
 // ring of the fused kernel: 4-row stages (one CTA barrier and one hit
 // enumeration per stage); refill lags two stages (previous row resident)
+#ifndef CAMX_K3_MINB
+#define CAMX_K3_MINB 6  // K3 (no tiles): CTAs per SM the register budget is sized for (78 registers)
+#endif
 #ifndef CAMX_FUSE_ROWS
 #define CAMX_FUSE_ROWS 4
 #endif
@@ -424,7 +427,7 @@ __device__ __forceinline__ void resample_hit(const uint8_t *ringb, uint32_t offa
 }
 
 template <bool TILES, int ROWS, int STAGES>
-__global__ void __launch_bounds__(kApplyThreads, TILES ? CAMX_FUSE_MINB : 4)
+__global__ void __launch_bounds__(kApplyThreads, TILES ? CAMX_FUSE_MINB : CAMX_K3_MINB)
     apply_tma_kernel(const ApplyParams p, const TileFuse q) {
   extern __shared__ __align__(128) uint4 ring[];  // [STAGES][ROWS][kApplyThreads]
   __shared__ __align__(8) uint64_t full[STAGES];
