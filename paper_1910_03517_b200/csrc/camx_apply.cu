@@ -426,8 +426,11 @@ __device__ __forceinline__ void resample_hit(const uint8_t *ringb, uint32_t offa
   }
 }
 
-template <bool TILES, int ROWS, int STAGES>
-__global__ void __launch_bounds__(kApplyThreads, TILES ? CAMX_FUSE_MINB : CAMX_K3_MINB)
+// MINB: CTAs per SM the register budget is sized for (0: the default of the
+// TILES / plain variant); short-CTA launches use a leaner plain variant.
+template <bool TILES, int ROWS, int STAGES, int MINB = 0>
+__global__ void __launch_bounds__(kApplyThreads,
+                                  MINB > 0 ? MINB : (TILES ? CAMX_FUSE_MINB : CAMX_K3_MINB))
     apply_tma_kernel(const ApplyParams p, const TileFuse q) {
   extern __shared__ __align__(128) uint4 ring[];  // [STAGES][ROWS][kApplyThreads]
   __shared__ __align__(8) uint64_t full[STAGES];
@@ -816,11 +819,11 @@ static bool plan_fast(ApplyParams &p) {
   return true;
 }
 
-template <bool TILES, int ROWS = kTmaRows, int STAGES = kTmaStages>
+template <bool TILES, int ROWS = kTmaRows, int STAGES = kTmaStages, int MINB = 0>
 static int launch_tma(const ApplyParams &p, const TileFuse &q, cudaStream_t stream) {
   const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
   const size_t smem = STAGES * ROWS * kApplyThreads * 16 + (TILES ? fuse_smem_bytes(q) : 0);
-  cudaError_t e = cudaFuncSetAttribute(apply_tma_kernel<TILES, ROWS, STAGES>,
+  cudaError_t e = cudaFuncSetAttribute(apply_tma_kernel<TILES, ROWS, STAGES, MINB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
@@ -834,7 +837,7 @@ static int launch_tma(const ApplyParams &p, const TileFuse &q, cudaStream_t stre
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = p.pdl ? 1 : 0;
-  e = cudaLaunchKernelEx(&lc, apply_tma_kernel<TILES, ROWS, STAGES>, p, q);
+  e = cudaLaunchKernelEx(&lc, apply_tma_kernel<TILES, ROWS, STAGES, MINB>, p, q);
   return e == cudaSuccess ? launch_status() : static_cast<int>(e);
 }
 
@@ -850,6 +853,11 @@ static int launch_apply(ApplyParams &p, cudaStream_t stream) {
       apply_fast_kernel<<<static_cast<unsigned>(grid), kApplyThreads, 0, stream>>>(p);
       return launch_status();
     }
+    // short CTAs (<= 48 rows, e.g. 640x480 frames: 30-row blocks) spend more
+    // of their life in the prologue / first fills: one more resident CTA per
+    // SM (72 registers) hides it (config 1 K3 56.8 -> 51.3 us); whole 96-row
+    // blocks run best at 6 (config 2: 0.7275 vs 0.7302 ms per step)
+    if (p.rows_per_split <= 48) return launch_tma<false, kTmaRows, kTmaStages, 7>(p, TileFuse{}, stream);
     return launch_tma<false>(p, TileFuse{}, stream);
   }
   const int64_t npx = static_cast<int64_t>(p.n_img) * p.H * p.W;
