@@ -80,6 +80,9 @@ __device__ __noinline__ void fused_solve_tail(const StatsParams &p, int64_t unit
   solve_seam_block(p.solve, s, k, cand);
 }
 
+#ifndef CAMX_K1_MINB
+#define CAMX_K1_MINB 32  // one-warp CTAs: 64 registers, every warp slot of an SM usable
+#endif
 #ifndef CAMX_K1_WARPS
 #define CAMX_K1_WARPS 1
 #endif
@@ -493,7 +496,7 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
 // block) units, so the short per-unit load -> reduce phases of resident
 // CTAs overlap instead of running as many launch waves.
 template <bool HIST, int MASKMODE, int QUAD, bool FUSE>
-__global__ void __launch_bounds__(kStatsWarps * 32) band_stats_kernel(const StatsParams p) {
+__global__ void __launch_bounds__(kStatsWarps * 32, CAMX_K1_MINB) band_stats_kernel(const StatsParams p) {
   extern __shared__ uint32_t smem[];
   __shared__ uint64_t part[kStatsWarps][13];
   // let a programmatically dependent kernel launch early (K2 waits on
