@@ -231,3 +231,22 @@ class TestTileWire:                   # imgio.py:14-18, detect.py:297-301
             detect.encode_ppm(np.zeros((4, 4), np.uint8))
         with pytest.raises(ValueError):
             detect.detect_requests([DetectorWindow(0, 0, 1)], tiles)
+
+
+class TestBandPacking:                # the drop-in's per-call band transfer
+    def test_packed_bands_are_the_band_columns(self):
+        """K1 over the packed (H, 2 bw) image reads exactly the columns it
+        reads in the full frame: RIGHT side = the first bw columns, LEFT side
+        = the last bw (exposure.py:163-168), for frames and 2-D masks."""
+        rng = np.random.default_rng(5)
+        for (h, w, bw) in [(12, 40, 8), (7, 9, 4), (5, 16, 8)]:
+            px = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+            pk = xp._bands(px, bw)
+            assert pk.shape == ((h, 2 * bw, 3) if 2 * bw < w else (h, w, 3))
+            assert pk.flags["C_CONTIGUOUS"]
+            np.testing.assert_array_equal(pk[:, :bw], px[:, :bw])
+            np.testing.assert_array_equal(pk[:, -bw:], px[:, w - bw:])
+            m = rng.random((h, w)) < 0.5
+            pm = xp._bands(m.view(np.uint8), bw)
+            np.testing.assert_array_equal(pm[:, :bw], m[:, :bw].view(np.uint8))
+            np.testing.assert_array_equal(pm[:, -bw:], m[:, w - bw:].view(np.uint8))
