@@ -209,6 +209,14 @@ int camx_comm_available(void);
 int camx_comm_unique_id(uint8_t *id_out /* 128 bytes */);
 int camx_comm_init(void **comm_out, const uint8_t *id, int32_t n_ranks, int32_t rank);
 int camx_comm_destroy(void *comm);
+/* Test-only loopback group: `world` communicator handles (comms_out[rank])
+ * for ranks that live in ONE process on one GPU, each driven from its own
+ * host thread and stream (NCCL refuses two ranks per device).  The
+ * all-gather stages the bytes through a shared device buffer with event
+ * waits and host barriers, so the world > 1 code of the sharded entry
+ * points runs exactly as under NCCL.  Release each handle with
+ * camx_comm_destroy. */
+int camx_comm_loopback_create(int32_t world, void **comms_out);
 
 /* K2 on the all-gathered records: stats_all = [world][n_batch][cmax][2][K]
  * (rank-major, each rank's block padded to cmax cameras).  Otherwise as
@@ -255,7 +263,7 @@ int camx_correct_batch_sharded(const uint8_t *images, uint8_t *out,
  * step) is ordered after both.  images == NULL: no front half (flush);
  * apply_images == NULL: no back half (first step).  The caller double-buffers
  * the maps / records between consecutive steps.  One pipelined sequence per
- * device at a time. */
+ * (device, communicator) at a time. */
 int camx_correct_batch_sharded_step(
     const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch,
     int32_t n_cams, int32_t cam_begin, int32_t cam_count, int32_t world,
@@ -279,6 +287,12 @@ int camx_apply_map(const uint8_t *images, uint8_t *out, int64_t n_images,
  * n_pixels RGB pixels; mask_out bytes 0/1. */
 int camx_mask_diff(const uint8_t *a, const uint8_t *b, int64_t n_pixels,
                    int32_t t_diff, uint8_t *mask_out, void *stream);
+
+/* mask_diff over n_pixels pixels of `channels` interleaved uint8 channels
+ * (the reference takes the max over axis 2 of any (H, W, C) array). */
+int camx_mask_diff_channels(const uint8_t *a, const uint8_t *b, int64_t n_pixels,
+                            int32_t channels, int32_t t_diff, uint8_t *mask_out,
+                            void *stream);
 
 /* Per-window on-pixel counts of difference_plan (attention.py:96-100) on
  * the mosaic of n_cams images (mosaic col x -> camera x / width), without

@@ -68,6 +68,7 @@ SIGNATURES = {
     "camx_comm_unique_id": [P],
     "camx_comm_init": [P, P, I32, I32],
     "camx_comm_destroy": [P],
+    "camx_comm_loopback_create": [I32, P],
     "camx_correct_batch_sharded": [P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, I32,
                                    P, P, P, P, P, P, P, P, P, I32, P, P],
     "camx_correct_batch_sharded_step": [P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, I32,
@@ -81,6 +82,7 @@ SIGNATURES = {
     "camx_apply_array": [P, P, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P],
     "camx_apply_map": [P, P, I64, I32, I32, I32, I32, P, P, P],
     "camx_mask_diff": [P, P, I64, I32, P, P],
+    "camx_mask_diff_channels": [P, P, I64, I32, I32, P, P],
     "camx_window_counts": [P, P, P, I32, I32, I32, I32, P, I32, I32, P, P],
     "camx_tiles": [P, I32, I32, I32, P, I32, I32, I32, P, P],
     "camx_tiles_shard": [P, I32, I32, I32, I32, P, P, I32, I32, I32, P, P],

@@ -96,16 +96,37 @@ class ArrayCorrector:
 
     # ------------------------------------------------------------ state
     def reset(self) -> None:
-        """Forget previous maps / frames (next batch starts like tick 0)."""
+        """Forget previous maps / frames (next batch starts like tick 0).
+        Captured CUDA graphs baked "has previous maps" in: drop them."""
         self._prev_maps = None
         self._prev_frame = None
+        self._graphs = {}
 
     def set_prev_maps(self, maps: list[SeamMaps]) -> None:
+        """Seed the tick loop with host maps (seam s = cameras (s, s+1 mod N)).
+        They are copied into the one device state buffer that every path -
+        eager calls and captured graph replays alike - reads."""
         g = np.stack([[m.left.gain, m.right.gain] for m in maps])
         o = np.stack([[m.left.offset, m.right.offset] for m in maps])
         if g.shape != (self.S, 2, self.K, 3):
             raise ValueError("exposure map geometry mismatch")
-        self._prev_maps = (_dev.to_device(g), _dev.to_device(o))
+        pg, po = self._state()
+        pg.copy_(_dev.to_device(g))
+        po.copy_(_dev.to_device(o))
+        self._prev_maps = (pg, po)
+
+    def _state(self):
+        """Device tick-loop state: the last frame's maps (S, 2, K, 3), one
+        pair of buffers for the corrector's lifetime (graph replays read
+        them by address)."""
+        st = getattr(self, "_state_bufs", None)
+        if st is None:
+            t = _dev.require_cuda()
+            shape = (max(self.S, 1), 2, self.K, 3)
+            st = (t.ones(shape, dtype=t.float64, device="cuda"),
+                  t.zeros(shape, dtype=t.float64, device="cuda"))
+            self._state_bufs = st
+        return st
 
     def _buffers(self, B: int):
         buf = self._bufs.get(B)
@@ -119,8 +140,6 @@ class ArrayCorrector:
                 fit_ok=t.empty((B, max(S, 1), K), dtype=t.uint8, device="cuda"),
                 hist=(t.empty((B, N, 2, K, 3, 256), dtype=t.int32, device="cuda")
                       if self.histograms else None),
-                prev_g=t.ones((max(S, 1), 2, K, 3), dtype=t.float64, device="cuda"),
-                prev_o=t.zeros((max(S, 1), 2, K, 3), dtype=t.float64, device="cuda"),
             )
             self._bufs[B] = buf
         return buf
@@ -193,9 +212,10 @@ class ArrayCorrector:
         # carry the tick-loop state to the next batch
         with t.cuda.stream(main):
             if self.S > 0:
-                buf["prev_g"].copy_(gain[B - 1], non_blocking=True)
-                buf["prev_o"].copy_(off[B - 1], non_blocking=True)
-                self._prev_maps = (buf["prev_g"], buf["prev_o"])
+                pg, po = self._state()
+                pg.copy_(gain[B - 1], non_blocking=True)
+                po.copy_(off[B - 1], non_blocking=True)
+                self._prev_maps = (pg, po)
             if removal:
                 if self._prev_frame is None:
                     self._prev_frame = t.empty_like(frames[0])
@@ -311,8 +331,9 @@ class ArrayCorrector:
         its result is returned (the frames buffer may be refilled on
         `stream` right after the call: the call's end is joined into it).
         Maps and records are double-buffered: a returned result's gain /
-        offset / fit_ok / stats / hist stay valid until two more submits
-        (copy them to keep them).  The tick-loop state carries across
+        offset / fit_ok / stats / hist are views of the buffer the NEXT
+        submit() refills, so they stay valid until the next submit() (copy
+        them to keep them).  The tick-loop state carries across
         submits like correct()."""
         t = _dev.require_cuda()
         if self.S == 0:
@@ -366,11 +387,11 @@ class ArrayCorrector:
         pending = pipe["pending"]
         self._step_call(None, 0, None, None, None, None, pending, main)
         res = self._pending_result(pending, main)
-        buf = self._buffers(pending[0].shape[0])
+        pg, po = self._state()
         with t.cuda.stream(main):
-            buf["prev_g"].copy_(pending[2]["gain"][-1], non_blocking=True)
-            buf["prev_o"].copy_(pending[2]["offset"][-1], non_blocking=True)
-        self._prev_maps = (buf["prev_g"], buf["prev_o"])
+            pg.copy_(pending[2]["gain"][-1], non_blocking=True)
+            po.copy_(pending[2]["offset"][-1], non_blocking=True)
+        self._prev_maps = (pg, po)
         pipe["pending"] = None
         return res
 
@@ -484,9 +505,18 @@ class ArrayCorrector:
             return
         full_ptr = stats.data_ptr() + lo * rec_bytes
         if self.exchange is not None:
+            # Python exchange (any torch.distributed backend): host-synchronous
+            # on both sides.  Gloo's CUDA all-gather does not reliably order
+            # its device copies against a caller stream it did not create
+            # (K2 was measured reading the records before they landed), and
+            # this path exists for portability, not speed - the NCCL path is
+            # the stream-ordered camx_correct_batch_sharded.
             t = _dev.torch()
-            with t.cuda.stream(t.cuda.ExternalStream(sh)):
+            ext = t.cuda.ExternalStream(sh)
+            ext.synchronize()
+            with t.cuda.stream(ext):
                 full = self.exchange(stats[lo:hi])
+                t.cuda.synchronize()
                 if "full" not in buf:
                     buf["full"] = t.empty((buf["stats"].shape[0], self.n_cams, *full.shape[2:]),
                                           dtype=full.dtype, device=full.device)
@@ -518,10 +548,15 @@ class ArrayCorrector:
         dependencies, and the state carry - into a CUDA graph; later calls
         with the same (frames, out) buffers replay it, removing the per-call
         host cost (launch-bound small arrays).  Refill `frames` in place
-        between calls."""
+        between calls.  The graphs read the tick-loop state from the
+        corrector's fixed state buffers (_state: maps; the remembered
+        previous frame), so set_prev_maps() and eager calls in between
+        stay coherent; reset() drops the graphs."""
         t = _dev.require_cuda()
         key = (frames.data_ptr(), out.data_ptr(), tuple(frames.shape))
-        hit = self._graphs.get(key) if hasattr(self, "_graphs") else None
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+        hit = self._graphs.get(key) if self._prev_maps is not None or self.S == 0 else None
         if hit is not None:
             hit[0].replay()
             return hit[1]
@@ -532,8 +567,6 @@ class ArrayCorrector:
         with t.cuda.graph(g, stream=s):
             cap = self.correct(frames, out, stream=s)
         t.cuda.current_stream().wait_stream(s)
-        if not hasattr(self, "_graphs"):
-            self._graphs = {}
         self._graphs[key] = (g, cap)
         return res
 

@@ -358,6 +358,9 @@ constexpr int kFuseMaxWin = 48;  // windows per array-frame the fused path accep
 constexpr int kFuseRows = CAMX_FUSE_ROWS;
 constexpr int kFuseStages = CAMX_FUSE_STAGES;
 static_assert(kFuseRows == 4, "hit enumeration uses e >> 2 / e & 3");
+// a slot is refilled two stages after it was consumed (the previous stage
+// stays resident for the resample): two stages would never be issued
+static_assert(kFuseStages >= 3, "the fused ring needs at least 3 stages");
 
 struct FuseSmem {  // carved from dynamic shared memory after the ring
   uint2 *tap;              // [out] (3 * i0, dp2a weights (256 - w1) | w1 << 16);
@@ -514,14 +517,16 @@ __global__ void __launch_bounds__(kApplyThreads,
           if (xc + tap_i0(fs.tap[mid]) + 1 >= px_hi) hi2 = mid; else lo2 = mid + 1;
         }
         if (lo2 > lo) {
+          // bounded: the host caps max_tiles_per_frame at kFuseMaxWin, but
+          // frame_off is caller data - never write past the shared array
           const int slot = atomicAdd(&fs.counts[0], 1);
-          fs.win[slot] = make_int4(t, x0, y0, lo | (lo2 << 16));
+          if (slot < kFuseMaxWin) fs.win[slot] = make_int4(t, x0, y0, lo | (lo2 << 16));
         }
       }
     }
   }
   __syncthreads();
-  const int nwin = TILES ? fs.counts[0] : 0;
+  const int nwin = TILES ? min(fs.counts[0], kFuseMaxWin) : 0;
   const int xbase = 3 * cam * p.W + cb0;  // window column -> CTA byte offset
   // maps come from the preceding stats/solve grid (programmatic dependent
   // launch): only the raw-pixel prefetch above may run before it completes
@@ -574,6 +579,11 @@ __global__ void __launch_bounds__(kApplyThreads,
           if (TILES) ring[(slot * ROWS + i) * kApplyThreads + threadIdx.x] = o;
         }
     }
+    // TILES: the corrected rows were written into the slot through the
+    // generic proxy and the slot is refilled by cp.async.bulk (async proxy)
+    // two stages later: order the writes before that refill (PTX memory
+    // model: fence.proxy.async between the proxies)
+    if (TILES) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();  // slot consumed (and, with TILES, corrected rows visible)
     if (TILES) {
       // every thread has finished the previous stage's resample (it came

@@ -8,7 +8,10 @@
 // camx_correct_batch_sharded - no Python on the per-batch path.
 #include <dlfcn.h>
 
+#include <condition_variable>
 #include <mutex>
+#include <set>
+#include <vector>
 
 #include "camx_common.cuh"
 
@@ -60,8 +63,95 @@ const Api &api() {
 int status(Result r) { return r == 0 ? CAMX_OK : CAMX_ENCCL_BASE + r; }
 }  // namespace nccl
 
-// Used by camx_correct_batch_sharded (camx_apply.cu).
+// ---- loopback communicator (tests: W ranks inside ONE process on one GPU) --
+// NCCL refuses two ranks on one device, so with a single GPU the sharded
+// path's world > 1 code (record padding, in-place all-gather, rank-major K2,
+// the pipelined step) would never run.  A loopback group is W handles
+// driven from W host threads, each rank on its own stream; its all-gather
+// moves the bytes through one shared device staging buffer:
+//   (a) wait until every rank finished reading the previous call's staging
+//   (b) copy send -> staging[rank], record posted[rank]
+//   (c) host barrier: every rank has posted
+//   (d) wait on every posted[q], copy staging -> recv, record consumed[rank]
+//   (e) host barrier: every rank has enqueued its reads (so no rank's next
+//       call can re-post before they are ordered)
+// Only stream-order waits on events: no kernel ever spins on another rank.
+namespace loopback {
+struct Group {
+  int world = 0, live = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0, status = CAMX_OK;
+  uint64_t gen = 0;
+  uint8_t *staging = nullptr;
+  size_t staging_bytes = 0;
+  std::vector<cudaEvent_t> posted, consumed;
+};
+struct Handle {
+  Group *g;
+  int rank;
+};
+std::mutex reg_mu;
+std::set<const void *> &registry() {
+  static std::set<const void *> r;
+  return r;
+}
+bool is_loopback(const void *h) {
+  std::lock_guard<std::mutex> lock(reg_mu);
+  return registry().count(h) != 0;
+}
+// host barrier; `last` runs once, by the last thread to arrive, before the
+// others are released
+template <class F>
+int barrier(Group &g, F last) {
+  std::unique_lock<std::mutex> lock(g.mu);
+  const uint64_t gen = g.gen;
+  if (++g.arrived == g.world) {
+    g.status = last();
+    g.arrived = 0;
+    ++g.gen;
+    g.cv.notify_all();
+  } else {
+    g.cv.wait(lock, [&] { return g.gen != gen; });
+  }
+  return g.status;  // the last arriver's result, seen by every rank
+}
+int all_gather(const void *send, void *recv, size_t bytes, Handle &h, cudaStream_t s) {
+  Group &g = *h.g;
+  const size_t need = bytes * g.world;
+  // staging (re)allocation by the last arriver while every rank waits (the
+  // first call, or a larger message: cudaFree orders after in-flight reads)
+  int st = barrier(g, [&]() -> int {
+    if (g.staging_bytes >= need) return CAMX_OK;
+    if (g.staging) cudaFree(g.staging);
+    g.staging = nullptr;
+    g.staging_bytes = 0;
+    cudaError_t e = cudaMalloc(&g.staging, need);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    g.staging_bytes = need;
+    return CAMX_OK;
+  });
+  if (st != CAMX_OK) return st;
+  cudaError_t e = cudaSuccess;
+  for (int q = 0; e == cudaSuccess && q < g.world; ++q) e = cudaStreamWaitEvent(s, g.consumed[q], 0);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(g.staging + bytes * h.rank, send, bytes, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaEventRecord(g.posted[h.rank], s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  barrier(g, [] { return CAMX_OK; });
+  for (int q = 0; e == cudaSuccess && q < g.world; ++q) e = cudaStreamWaitEvent(s, g.posted[q], 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(recv, g.staging, need, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaEventRecord(g.consumed[h.rank], s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  barrier(g, [] { return CAMX_OK; });
+  return CAMX_OK;
+}
+}  // namespace loopback
+
+// Used by camx_correct_batch_sharded (camx_shard.cu).
 int comm_all_gather(const void *send, void *recv, size_t bytes, void *comm, cudaStream_t s) {
+  if (comm != nullptr && loopback::is_loopback(comm))
+    return loopback::all_gather(send, recv, bytes, *static_cast<loopback::Handle *>(comm), s);
   const nccl::Api &a = nccl::api();
   if (!a.ok) return CAMX_ENONCCL;
   return nccl::status(a.all_gather(send, recv, bytes, nccl::kUint8, comm, s));
@@ -104,8 +194,49 @@ extern "C" int camx_comm_init(void **comm_out, const uint8_t *id, int32_t n_rank
   return CAMX_OK;
 }
 
+extern "C" int camx_comm_loopback_create(int32_t world, void **comms_out) {
+  if (world < 1 || world > 64 || comms_out == nullptr) return CAMX_EINVAL;
+  auto *g = new loopback::Group();
+  g->world = g->live = world;
+  g->posted.resize(world);
+  g->consumed.resize(world);
+  for (int r = 0; r < world; ++r) {
+    cudaError_t e = cudaEventCreateWithFlags(&g->posted[r], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->consumed[r], cudaEventDisableTiming);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  std::lock_guard<std::mutex> lock(loopback::reg_mu);
+  for (int r = 0; r < world; ++r) {
+    auto *h = new loopback::Handle{g, r};
+    loopback::registry().insert(h);
+    comms_out[r] = h;
+  }
+  return CAMX_OK;
+}
+
 extern "C" int camx_comm_destroy(void *comm) {
   if (comm == nullptr) return CAMX_OK;
+  if (loopback::is_loopback(comm)) {
+    auto *h = static_cast<loopback::Handle *>(comm);
+    loopback::Group *g = h->g;
+    bool last = false;
+    {
+      std::lock_guard<std::mutex> lock(loopback::reg_mu);
+      loopback::registry().erase(h);
+      last = --g->live == 0;
+    }
+    delete h;
+    if (last) {
+      cudaDeviceSynchronize();
+      if (g->staging) cudaFree(g->staging);
+      for (int r = 0; r < g->world; ++r) {
+        cudaEventDestroy(g->posted[r]);
+        cudaEventDestroy(g->consumed[r]);
+      }
+      delete g;
+    }
+    return CAMX_OK;
+  }
   const nccl::Api &a = nccl::api();
   if (!a.ok) return CAMX_ENONCCL;
   return nccl::status(a.comm_destroy(comm));

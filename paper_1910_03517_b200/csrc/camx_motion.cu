@@ -55,6 +55,18 @@ __global__ void mask_diff_kernel(const uint8_t *a, const uint8_t *b, int64_t lo,
   }
 }
 
+// Any channel count (mask_diff's max over axis 2 of an (H, W, C) array).
+__global__ void mask_diff_channels_kernel(const uint8_t *a, const uint8_t *b, int64_t n,
+                                          int channels, int t_diff, uint8_t *mask) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int m = 0;
+    for (int c = 0; c < channels; ++c)
+      m = max(m, abs(static_cast<int>(a[channels * i + c]) - b[channels * i + c]));
+    mask[i] = m > t_diff ? 1 : 0;
+  }
+}
+
 // One CTA per (window, row slab).  Counts are exact int64 via one atomic
 // per CTA.
 struct CountParams {
@@ -350,6 +362,19 @@ extern "C" int camx_mask_diff(const uint8_t *a, const uint8_t *b, int64_t n_pixe
     mask_diff_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, b, done, n_pixels, t_diff,
                                                                     mask_out);
   }
+  return launch_status();
+}
+
+extern "C" int camx_mask_diff_channels(const uint8_t *a, const uint8_t *b, int64_t n_pixels,
+                                       int32_t channels, int32_t t_diff, uint8_t *mask_out,
+                                       void *stream) {
+  if (n_pixels < 0 || channels < 1 || !a || !b || !mask_out) return CAMX_EINVAL;
+  if (channels == 3) return camx_mask_diff(a, b, n_pixels, t_diff, mask_out, stream);
+  if (n_pixels == 0) return CAMX_OK;
+  int64_t blocks = (n_pixels + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  mask_diff_channels_kernel<<<static_cast<unsigned>(blocks), 256, 0, as_stream(stream)>>>(
+      a, b, n_pixels, channels, t_diff, mask_out);
   return launch_status();
 }
 

@@ -10,7 +10,9 @@
 //   camx_correct_batch_sharded_step  one step of a pipelined stream: the
 //                                    front half of batch k under K3 of
 //                                    batch k-1 (ArrayCorrector.submit)
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "camx_common.cuh"
 
@@ -31,23 +33,23 @@ int apply_camera_group(const uint8_t *images, uint8_t *out, int nb, int cam_begi
 
 constexpr int kMaxShardChunks = 8;
 
-// Library-owned side stream + events of the sharded pipelines (one set per
-// device; capture-safe: only event record / wait).  ev[0] fork, ev[1..]
-// per chunk, step[0] the join of camx_correct_batch_sharded_step.
+// Library-owned side stream + events of the sharded pipelines, one set per
+// (device, communicator) - several ranks of a loopback group share a device
+// but never a pipeline (capture-safe: only event record / wait).  ev[0]
+// fork, ev[1..] per chunk, step[0] the join of camx_correct_batch_sharded_step.
 struct SidePipe {
   cudaStream_t side = nullptr;
   cudaEvent_t ev[kMaxShardChunks + 1] = {};
   cudaEvent_t step[1] = {};
 };
 static std::mutex g_pipe_mu;
-static int side_pipe(SidePipe *&out) {
-  static SidePipe pipes[64];
+static int side_pipe(SidePipe *&out, void *comm) {
+  static std::map<std::pair<int, void *>, SidePipe> pipes;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return static_cast<int>(e);
-  if (dev < 0 || dev >= 64) return CAMX_EINVAL;
   std::lock_guard<std::mutex> lock(g_pipe_mu);
-  SidePipe &sp = pipes[dev];
+  SidePipe &sp = pipes[std::make_pair(dev, comm)];  // std::map: stable addresses
   if (sp.side == nullptr) {
     e = cudaStreamCreateWithFlags(&sp.side, cudaStreamNonBlocking);
     for (int i = 0; e == cudaSuccess && i < kMaxShardChunks + 1; ++i)
@@ -158,7 +160,7 @@ extern "C" int camx_correct_batch_sharded(
   SidePipe *sp = nullptr;
   cudaStream_t side = main;
   if (n_chunks > 1) {
-    st = side_pipe(sp);
+    st = side_pipe(sp, comm);
     if (st != CAMX_OK) return st;
     side = sp->side;
     cudaError_t e = cudaEventRecord(sp->ev[0], main);
@@ -223,7 +225,7 @@ extern "C" int camx_correct_batch_sharded_step(
     return CAMX_EINVAL;
   if (back && (!apply_out || !apply_gain || !apply_offset)) return CAMX_EINVAL;
   SidePipe *sp = nullptr;
-  st = side_pipe(sp);
+  st = side_pipe(sp, comm);
   if (st != CAMX_OK) return st;
   cudaStream_t main = as_stream(stream);
   cudaError_t e = cudaSuccess;

@@ -59,7 +59,9 @@ def make_stats_exchange(n_cams: int, group=None):
             chunks = list(recv.unbind(0))
         else:
             chunks = [t.empty_like(send) for _ in range(world)]
+            _host_sync(nccl, send)
             dist.all_gather(chunks, send, group=group)
+            _host_sync(nccl, send)
         return t.cat([chunks[g][:, :c] for g, (_, c) in enumerate(parts)], dim=1).contiguous()
 
     return exchange
@@ -103,6 +105,37 @@ class NcclComm:
             from . import _lib
             _lib.call("camx_comm_destroy", self.handle)
             self.handle = None
+
+
+class LoopbackComm:
+    """Rank `rank` of a test-only loopback group (camx_comm_loopback_create):
+    the W ranks of a camera-sharded array live in ONE process on one GPU,
+    each driven from its own host thread and CUDA stream.  Same attributes
+    as NcclComm (rank, world, handle), so ArrayCorrector(comm=...) runs its
+    world > 1 native path unchanged; the all-gather goes through a shared
+    device buffer with event waits and host barriers instead of NCCL (which
+    refuses two ranks per device)."""
+
+    def __init__(self, handle: int, rank: int, world: int):
+        self.handle, self.rank, self.world = handle, rank, world
+
+    def close(self) -> None:
+        if self.handle:
+            from . import _lib
+            _lib.call("camx_comm_destroy", self.handle)
+            self.handle = None
+
+
+def loopback_comms(world: int) -> list[LoopbackComm]:
+    """`world` LoopbackComm handles of one group (use each from its own
+    thread; every rank must enter every collective)."""
+    import ctypes
+
+    from . import _lib
+    _dev.require_cuda()
+    hs = (ctypes.c_void_p * world)()
+    _lib.call("camx_comm_loopback_create", world, hs)
+    return [LoopbackComm(hs[r], r, world) for r in range(world)]
 
 
 def sharded_corrector(n_cams: int, height: int, width: int,
@@ -155,8 +188,18 @@ def sharded_window_counts(origins, size: int, *, cur=None, prev=None, mask=None,
     part = t.as_tensor(np.asarray(counts_fn(local, size), dtype=np.int64))
     if dist.get_backend(group) == "nccl":
         part = part.cuda()
+    else:
+        _host_sync(False, cur if cur is not None else mask)
     dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
     return part.cpu().numpy()
+
+
+def _host_sync(nccl: bool, x) -> None:
+    """Non-NCCL backends on CUDA tensors: finish the device work on both
+    sides of the collective (gloo does not reliably order its copies
+    against the caller's stream; see ArrayCorrector._stats_solve)."""
+    if not nccl and getattr(x, "is_cuda", False):
+        _dev.torch().cuda.synchronize()
 
 
 def tile_homes(windows, size: int, n_cams: int, width: int, world: int):
@@ -212,7 +255,9 @@ def sharded_tiles(out_local, windows, *, size: int = 960, out_size: int = 416, n
     # (1) halo: every rank's first corrected column
     first = out_local[:, 0, :, 0, :].contiguous()  # (B, H, 3)
     cols = [t.empty_like(first) for _ in range(world)]
+    _host_sync(nccl, first)
     dist.all_gather(cols, first, group=group)
+    _host_sync(nccl, first)
     halo = cols[rank + 1] if rank + 1 < world else None
 
     if tiles_fn is None:
@@ -242,7 +287,9 @@ def sharded_tiles(out_local, windows, *, size: int = 960, out_size: int = 416, n
     if strad:
         if not nccl and part.dtype == t.uint8:  # gloo sums int32
             acc = part.to(t.int32)
+            _host_sync(nccl, acc)
             dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+            _host_sync(nccl, acc)
             part = acc.to(t.uint8)
         else:
             dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)

@@ -218,10 +218,27 @@ def band_stats(frame: Frame, side: Side, band_width: int, blocks: int,
     img = _dev.to_device(_bands(frame.pixels, band_width))[None]
     msk = None
     if exclusion_mask is not None:
+        # the reference slices the mask like the band (exposure.py:163-168)
+        # and boolean-indexes each block's pixels with it (:178-180): any
+        # mask whose band slice covers the band's rows and columns works
+        # (extra rows are never read); otherwise numpy raises IndexError
         m = np.asarray(exclusion_mask, dtype=bool)
-        if m.shape != (h, w):
-            raise ValueError(f"exclusion mask must be {(h, w)}, got {m.shape}")
-        msk = _dev.to_device(_bands(m.view(np.uint8), band_width))[None]
+        mb = m[:, w - band_width:] if side is Side.LEFT else m[:, :band_width]
+        if mb.ndim != 2 or mb.shape[0] < h or mb.shape[1] != band_width:
+            raise IndexError(f"boolean index did not match the band: mask {m.shape}, "
+                             f"band {(h, band_width)}")
+        mb = np.ascontiguousarray(mb[:h]).view(np.uint8)
+        full = np.zeros((h, 2 * band_width) if 2 * band_width < w else (h, w), dtype=np.uint8)
+        if 2 * band_width < w:  # the packed layout of _bands: RIGHT band, then LEFT band
+            if side is Side.LEFT:
+                full[:, band_width:] = mb
+            else:
+                full[:, :band_width] = mb
+        elif side is Side.LEFT:
+            full[:, w - band_width:] = mb
+        else:
+            full[:, :band_width] = mb
+        msk = _dev.to_device(full)[None]
     rec, _ = _stats_device(img, masks=msk, band_width=band_width, blocks=blocks)
     s = 0 if side is Side.LEFT else 1
     mean, std, valid, area = (_dev.to_host(x) for x in _moments(rec[0, s]))
@@ -323,20 +340,48 @@ def update_exposure(frames: tuple[Frame, Frame],
 
 
 def _solve_pair(rec, prev_maps, mode, cfg, use_prev, seam_id) -> SeamMaps:
+    """K2 for one seam, with the reference's checks on `prev_maps`:
+    * where the reference blends into them (SMOOTHING; OBJECT_REMOVAL with
+      prev_frames) smooth_exposure requires the same seam_id, side and K
+      (exposure.py:234-235, 304-307, 332-335);
+    * elsewhere they are only resolve()'s fallback (exposure.py:275-293):
+      no check at all when every block fits (:280-281), else numpy's
+      np.where broadcast of (K, 1) against the fallback's (K', 3), which
+      accepts K' in {1, K} and raises ValueError otherwise."""
     t = _dev.torch()
     K = cfg.blocks
+    blends = mode is ExposureMode.SMOOTHING or (mode is ExposureMode.OBJECT_REMOVAL and use_prev)
     pg = po = None
+    deferred = False  # a fallback that only fails if some block needs it
     if prev_maps is not None:
-        if prev_maps.left.block_count != K or prev_maps.right.block_count != K:
-            raise ValueError("exposure map geometry mismatch")
-        pg = _dev.to_device(np.stack([prev_maps.left.gain, prev_maps.right.gain]))
-        po = _dev.to_device(np.stack([prev_maps.left.offset, prev_maps.right.offset]))
+        sides = ((prev_maps.left, Side.LEFT), (prev_maps.right, Side.RIGHT))
+        if blends:
+            for pm, side in sides:
+                if (pm.seam_id, pm.side, pm.block_count) != (seam_id, side, K):
+                    raise ValueError("exposure map geometry mismatch")
+        coeffs = []
+        for pm, _ in sides:
+            if pm.block_count == K:
+                coeffs.append((pm.gain, pm.offset))
+            elif pm.block_count == 1:  # broadcasts against (K, 1) like np.where
+                coeffs.append((np.broadcast_to(pm.gain, (K, 3)),
+                               np.broadcast_to(pm.offset, (K, 3))))
+            else:
+                deferred = True
+        if not deferred:
+            pg = _dev.to_device(np.stack([c[0] for c in coeffs]))
+            po = _dev.to_device(np.stack([c[1] for c in coeffs]))
     gain = t.empty((1, 1, 2, K, 3), dtype=t.float64, device="cuda")
     off = t.empty_like(gain)
-    sc = _solve_config(mode, cfg, prev_maps is not None, use_prev)
+    ok = t.empty((1, 1, K), dtype=t.uint8, device="cuda")
+    sc = _solve_config(mode, cfg, pg is not None, use_prev)
     _lib.call("camx_seam_solve", rec.data_ptr(), 1, 2, 0, ctypes.byref(sc), _dev.ptr(pg),
-              _dev.ptr(po), gain.data_ptr(), off.data_ptr(), None, _dev.stream_handle())
+              _dev.ptr(po), gain.data_ptr(), off.data_ptr(), ok.data_ptr(), _dev.stream_handle())
     g, o = _dev.to_host(gain)[0, 0], _dev.to_host(off)[0, 0]
+    if deferred and not _dev.to_host(ok).all():
+        kp = [pm.block_count for pm, _ in sides if pm.block_count not in (1, K)][0]
+        raise ValueError(f"operands could not be broadcast together with shapes ({K},1) "
+                         f"({K},3) ({kp},3)")
     bw = cfg.band_width
     return SeamMaps(ExposureMap(seam_id, Side.LEFT, bw, g[0], o[0]),
                     ExposureMap(seam_id, Side.RIGHT, bw, g[1], o[1]))

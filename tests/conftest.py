@@ -9,3 +9,14 @@ for p in (ROOT, os.path.dirname(os.path.abspath(__file__))):
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libcamx.so")
+
+
+def pytest_collection_modifyitems(config, items):
+    # the reference's own test modules, vendored under tests/_ref and run
+    # unmodified against the drop-in (tests/_ref/camarray): they call the
+    # CUDA path, so they belong to the GPU tier
+    import pytest
+    ref = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref") + os.sep
+    for item in items:
+        if str(item.fspath).startswith(ref):
+            item.add_marker(pytest.mark.gpu)
