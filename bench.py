@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     ap.add_argument("--no-hist", action="store_true",
                     help="skip the seam-band histograms (K1 means/moments only)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="only the primary workload (default N=1 run also times config4 and "
+                         "config5 and reports them under 'secondary')")
     return ap.parse_args()
 
 
@@ -126,7 +129,7 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ CPU baseline
 
-def cpu_reference_sample(frames_np, n_frames: int, threads: int):
+def cpu_reference_sample(frames_np, n_frames: int, threads: int, wrap: bool = False):
     """The reference algorithm (numpy restatement in oracle/, fresh maps
     every frame: update_exposure per seam + apply_exposure per camera side)
     on host cores; returns seconds per array-frame."""
@@ -134,11 +137,11 @@ def cpu_reference_sample(frames_np, n_frames: int, threads: int):
 
     from oracle import camarray_oracle as O
     n = frames_np.shape[1]
-    S = n - 1
+    S = n if wrap else n - 1
 
     def solve_one(args):
         b, s = args
-        r = O.update_exposure(frames_np[b, s], frames_np[b, s + 1], None)
+        r = O.update_exposure(frames_np[b, s], frames_np[b, (s + 1) % n], None)
         return s, r
 
     times = []
@@ -149,7 +152,7 @@ def cpu_reference_sample(frames_np, n_frames: int, threads: int):
             res = dict(ex.map(solve_one, [(b, s) for s in range(S)]))
             gain = O.np.stack([[res[s]["gl"], res[s]["gr"]] for s in range(S)])
             off = O.np.stack([[res[s]["ol"], res[s]["orr"]] for s in range(S)])
-            O.apply_array(frames_np[b], gain, off, threads=threads)
+            O.apply_array(frames_np[b], gain, off, wrap=wrap, threads=threads)
             times.append(time.perf_counter() - t0)
     return times
 
@@ -197,19 +200,30 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def bench_frames(name, batch, device):
+    """The benchmark's synthetic array-frames: synth.synthetic_batch, seed
+    100 - device-independent bytes, so the GPU arm and the CPU reference arm
+    correct the same frames (the reference arm samples the first two)."""
+    from paper_1910_03517_b200.synth import synthetic_batch
+    n_cams, H, W, _, _ = WORKLOADS[name]
+    return synthetic_batch(batch, n_cams, H, W, seed=100, device=device)
+
+
+DATA = ("synthetic (synth.synthetic_batch seed 100: shared panorama + per-camera affine "
+        "distortion + moving objects; identical bytes in both arms)")
+
+
 def run_reference(args):
     """--impl reference: the reference CPU path, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import numpy as np
     name = args.workload or "config2"
     n_cams, H, W, _, desc = WORKLOADS[name]
-    from oracle import camarray_oracle as O
-    frames = np.stack([O.synthetic_array(n_cams, H, W, seed=100 + t, objects=4)
-                       for t in range(2)])
+    frames = bench_frames(name, 2, "cpu").numpy()
     threads = os.cpu_count() or 1
-    times = cpu_reference_sample(frames, args.warmup + args.steps, threads)[args.warmup:]
+    wrap = name == "config4"
+    times = cpu_reference_sample(frames, args.warmup + args.steps, threads, wrap)[args.warmup:]
     sec = sum(times) / len(times)
     mp = n_cams * H * W / 1e6
     val = mp / sec
@@ -217,10 +231,10 @@ def run_reference(args):
         "impl": "reference", "metric": "corrected megapixels/sec", "value": round(val, 3),
         "unit": "MP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (panorama + per-camera affine distortion)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": DATA,
         "array_frames_per_sec": round(1.0 / sec, 4),
-        "config": {"workload": f"{name}: {desc}", "step": "1 array-frame, STANDARD update + apply"},
+        "config": {"workload": f"{name}: {desc}", "step": "1 array-frame, STANDARD update + apply",
+                   "frames": "array-frames 0-1 of the GPU arm's batch, alternating"},
         "cpu_baseline": {"value": round(val, 3), "unit": "MP/s", "cores": threads, "kind": "port",
                          "sample": f"{args.steps} array-frames of {name} after {args.warmup} warm-up",
                          "cpu_model": cpu_model()},
@@ -233,15 +247,310 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ GPU arm
 
+def traffic_for(name, kernel_bytes, batch):
+    """ncu DRAM bytes (read + write) of the dominant kernel(s) per launch,
+    from a capture of this workload at this batch size (profiles/
+    traffic.json), else None."""
+    tp = ROOT / "profiles" / "traffic.json"
+    if not tp.exists():
+        return None
+    try:
+        for d in json.loads(tp.read_text()).get("entries", []):
+            if d.get("workload") == name and int(d.get("batch", -1)) == batch and \
+                    int(d.get("algorithmic_bytes_per_launch", -1)) == kernel_bytes:
+                return int(d["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+class Workload:
+    """One benchmarked configuration on this rank: frames resident in HBM,
+    a step function, and the dominant kernel's roofline leg."""
+
+    def __init__(self, name, B, args, world, rank, torch):
+        from paper_1910_03517_b200.array import ArrayCorrector
+        from paper_1910_03517_b200.dist import camera_partition, sharded_corrector
+        from paper_1910_03517_b200.exposure import ExposureConfig, ExposureMode
+        self.name, self.B, self.world, self.torch = name, B, world, torch
+        n_cams, H, W, _, self.desc = WORKLOADS[name]
+        self.n_cams, self.H, self.W = n_cams, H, W
+        self.mode = ExposureMode(args.mode)
+        self.cfg = ExposureConfig()
+        self.wrap = name == "config4"
+        self.hist = not args.no_hist
+        if world > 1:
+            self.ac = sharded_corrector(n_cams, H, W, self.cfg, self.mode, wrap=self.wrap,
+                                        histograms=self.hist)
+            self.begin, self.count = camera_partition(n_cams, world)[rank]
+        else:
+            self.ac = ArrayCorrector(n_cams, H, W, self.cfg, self.mode, wrap=self.wrap,
+                                     histograms=self.hist)
+            self.begin, self.count = 0, n_cams
+        full = bench_frames(name, B, "cuda")
+        self.frames = full[:, self.begin:self.begin + self.count].contiguous()
+        del full
+        self.out = torch.empty_like(self.frames)
+        self.stream = torch.cuda.Stream()
+        self.tiles = name == "config5"
+        self.tiles_buf = None
+        if self.tiles:
+            n_tiles = len(self.ac.tile_windows(960)) * B
+            self.tiles_buf = torch.empty((n_tiles, 416, 416, 3), dtype=torch.uint8, device="cuda")
+        self.use_graph = not args.no_graph and world == 1 and not self.tiles
+        # N > 1 over NCCL: the front half (K1 -> all-gather -> K2) of batch k on
+        # a side stream under K3 of batch k-1 (ArrayCorrector.submit)
+        self.use_pipe = (world > 1 and getattr(self.ac, "comm", None) is not None
+                         and not self.tiles and os.environ.get("CAMX_SHARD_PIPE", "1") != "0")
+
+    def step(self):
+        ac = self.ac
+        if self.tiles:
+            return ac.correct_and_tile(self.frames, out=self.out, tiles=self.tiles_buf,
+                                       stream=self.stream)[0]
+        if self.use_graph:  # CUDA graph replay of K1 -> K2 -> K3 (+ state carry)
+            return ac.correct_graphed(self.frames, self.out)
+        if self.use_pipe:
+            return ac.submit(self.frames, self.out, stream=self.stream)
+        return ac.correct(self.frames, self.out, stream=self.stream)
+
+    def launches_per_call(self, fn, a):
+        """Our kernels behind one _lib.call (camx entry points launch several)."""
+        from paper_1910_03517_b200.exposure import ExposureMode
+        removal = self.mode is ExposureMode.OBJECT_REMOVAL
+        if fn in ("camx_correct_batch", "camx_correct_batch_tiles"):
+            # K1 (x2 for OBJECT_REMOVAL with B > 1 and no previous frame) + K2 + K3
+            # (+ tile fix-up)
+            n = 3 if (removal and a[3] > 1 and a[2] is None) else 2
+            return n + (1 if fn == "camx_correct_batch" else 2)
+        if fn == "camx_correct_batch_sharded":  # K1 (x2) + K2 + K3 (+ NCCL, not ours)
+            return 4 if (removal and a[3] > 1 and a[2] is None) else 3
+        if fn == "camx_correct_batch_sharded_step":
+            n = 0
+            if a[0] is not None:  # front half: K1 (x2 without a previous frame) + K2
+                n += 3 if (removal and a[2] > 1 and a[1] is None) else 2
+            if a[21] is not None:  # back half: K3 of the previous batch
+                n += 1
+            return n
+        return 1 if fn.startswith("camx_") else 0
+
+    def run(self, steps, warmup, barrier):
+        torch = self.torch
+        from paper_1910_03517_b200 import _lib
+        with torch.cuda.stream(self.stream):
+            for _ in range(warmup):
+                self.step()
+        barrier()
+        n_launch = [0]
+        orig_call = _lib.call
+
+        def traced_call(fn, *a):
+            n_launch[0] += self.launches_per_call(fn, a)
+            orig_call(fn, *a)
+
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        _lib.call = traced_call
+        try:
+            with ClockSampler(torch.cuda.current_device()) as clk:
+                barrier()
+                start.record(self.stream)
+                with torch.cuda.stream(self.stream):
+                    for _ in range(steps):
+                        res = self.step()
+                stop.record(self.stream)
+                stop.synchronize()
+                barrier()
+        finally:
+            _lib.call = orig_call
+        if self.use_pipe:  # drain the pipeline (outside the timed region)
+            with torch.cuda.stream(self.stream):
+                res = self.ac.flush(stream=self.stream) or res
+            torch.cuda.synchronize()
+        if self.use_graph:  # replays do not pass through _lib.call: same kernels as an eager step
+            n_launch[0] = 3 * steps  # K1 (the captured tick has a previous frame), K2, K3
+        self.res = res
+        self.ms = start.elapsed_time(stop)
+        self.steps = steps
+        self.launches = n_launch[0]
+        self.clocks = clk.summary()
+        return self
+
+    def roofline_leg(self, reps):
+        """The dominant kernel alone (K3 apply; config 5: the fused apply +
+        tile kernel and its fix-up), same buffers and maps as the last step,
+        CUDA events on its stream around each launch."""
+        import numpy as np
+        torch = self.torch
+        from paper_1910_03517_b200 import _lib
+        B, H, W = self.B, self.H, self.W
+        res, cfg, stream = self.res, self.cfg, self.stream
+        nbytes = 6 * B * self.count * H * W
+        kname = "camx apply_tma_kernel (K3)"
+        if self.tiles:
+            wins = sorted(((b, x, y) for b in range(B) for (x, y) in self.ac.tile_windows(960)),
+                          key=lambda w: w[0])
+            per_b = np.bincount(np.asarray([w[0] for w in wins]), minlength=B)
+            w_dev = torch.as_tensor(np.asarray(wins, dtype=np.int32).reshape(-1, 3), device="cuda")
+            off_dev = torch.as_tensor(np.concatenate([[0], np.cumsum(per_b)]).astype(np.int32),
+                                      device="cuda")
+            nbytes += self.tiles_buf.numel()
+            kname = "camx apply_tma_kernel<fused tiles> + tile_fixup (K3+K5)"
+        ev = []
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                if self.tiles:
+                    _lib.call("camx_correct_and_tile", self.frames.data_ptr(), self.out.data_ptr(),
+                              B, self.n_cams, int(self.wrap), H, W, cfg.blocks,
+                              res.gain.data_ptr(), res.offset.data_ptr(), w_dev.data_ptr(),
+                              off_dev.data_ptr(), len(wins), int(per_b.max()), 960, 416,
+                              self.tiles_buf.data_ptr(), stream.cuda_stream)
+                else:
+                    _lib.call("camx_apply_array", self.frames.data_ptr(), self.out.data_ptr(), B,
+                              self.begin, self.count, self.n_cams, int(self.wrap), H, W,
+                              cfg.blocks, res.gain.data_ptr(), res.offset.data_ptr(),
+                              stream.cuda_stream)
+                e1.record(stream)
+                ev.append((e0, e1))
+        torch.cuda.synchronize()
+        self.k_ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
+        self.k_bytes = nbytes
+        self.k_name = kname
+        self.k_reps = len(ev)
+
+    def summary(self, peak, peak_kind):
+        """Throughput + roofline fields (after max-over-ranks timing)."""
+        ms_step = self.ms / self.steps
+        px = self.B * self.n_cams * self.H * self.W
+        achieved = self.k_bytes / (self.k_ms / 1e3) / 1e9
+        return {
+            "workload": f"{self.name}: {self.desc}",
+            "value": round(px / 1e6 / (ms_step / 1e3), 2), "unit": "MP/s",
+            "ms_per_step": round(ms_step, 4),
+            "array_frames_per_sec": round(self.B / (ms_step / 1e3), 2),
+            "roofline": {"bound": "hbm", "kernel": self.k_name, "achieved": round(achieved, 1),
+                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic_for(self.name, self.k_bytes, self.B),
+                         "peak_kind": peak_kind, "k_ms_per_launch": round(self.k_ms, 4),
+                         "k_bytes_per_launch": self.k_bytes, "k_launches_timed": self.k_reps,
+                         "k_share_of_step": round(self.k_ms * self.steps / self.ms, 4)},
+        }
+
+    def config(self):
+        return {"workload": f"{self.name}: {self.desc}", "batch": self.B,
+                "mode": self.mode.value, "histograms": self.hist, "wrap": self.wrap,
+                "tiles_per_step": (self.tiles_buf.shape[0] if self.tiles else 0),
+                "cameras_per_gpu": self.count, "frame": f"{self.W}x{self.H}",
+                "step": ("K1 band stats" + (" + histograms" if self.hist else "") +
+                         " + K2 seam solve + K3 apply" +
+                         (" fused with 36 attention tiles 960->416" if self.tiles else "") +
+                         " per array-frame"),
+                "l2": "inputs larger than L2 (batch >> 126 MB)",
+                "parallelism": f"camera-shard{self.world}" if self.world > 1 else "single",
+                "launch": ("cuda-graph replay" if self.use_graph else
+                           "software-pipelined: K1 -> NCCL all-gather -> K2 of batch k on "
+                           "a side stream under K3 of batch k-1" if self.use_pipe else
+                           "eager (PDL-chained)")}
+
+    def free(self):
+        for k in ("frames", "out", "tiles_buf", "res", "ac"):
+            if hasattr(self, k):
+                delattr(self, k)
+        self.torch.cuda.empty_cache()
+
+
+def e2e_ring(wl, Be, steps, warmup, barrier, world):
+    """End to end through the streaming API (ring.FrameRing): frames sit in
+    the ring's pinned host slots (the producer - a decoder - writes them
+    there; the bench fills the R slots once, outside the timed region), and
+    every step publishes one slot: H2D on the copy stream -> K1, K2, K3 on
+    the compute stream -> D2H of the corrected batch and its maps into the
+    slot's pinned output, then get() + release() by the consumer.  Wall
+    clock from the first publish to the last completed D2H."""
+    torch = wl.torch
+    from paper_1910_03517_b200.ring import FrameRing
+    ac = wl.ac
+    ac.reset()
+    slots = 3
+    ring = FrameRing(ac, slots=slots, batch=Be)
+    host = wl.frames[: min(wl.B, slots * Be)].cpu()
+    for j in range(slots):  # the producer's writes (decode) - not timed
+        lo = (j * Be) % max(1, host.shape[0] - Be + 1)
+        ring.acquire(block=False)[...] = host[lo:lo + Be].numpy()
+        ring.publish(tag=j)
+    for r in ring.drain():
+        ring.release(r)
+
+    def run(n):
+        done = 0
+        for k in range(n):
+            ring.acquire(block=False)  # the slot still holds its frames
+            ring.publish(tag=k)
+            if ring.pending() >= slots:
+                ring.release(ring.get())
+                done += 1
+        for r in ring.drain():
+            ring.release(r)
+
+    run(max(1, warmup))
+    barrier()
+    t0 = time.perf_counter()
+    run(steps)
+    ms = (time.perf_counter() - t0) * 1e3
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt[0])
+    ms_step = ms / steps
+    px = Be * wl.n_cams * wl.H * wl.W
+    return {"value": round(px / 1e6 / (ms_step / 1e3), 2), "unit": "MP/s",
+            "h2d_bytes_per_step": ring.h2d_bytes_per_batch * world,
+            "d2h_bytes_per_step": ring.d2h_bytes_per_batch * world,
+            "array_frames_per_sec": round(Be / (ms_step / 1e3), 2),
+            "batch": Be, "steps": steps, "slots": slots,
+            "path": "ring.FrameRing (pinned host slots -> H2D copy stream -> K1/K2/K3 compute "
+                    "stream -> D2H copy-back stream; wall clock)",
+            "pcie_bytes_per_sec_each_way": round(ring.h2d_bytes_per_batch / (ms_step / 1e3) / 1e9,
+                                                 2)}
+
+
+def cpu_baseline_line(wl, args):
+    threads = os.cpu_count() or 1
+    fr = bench_frames(wl.name, 2, "cpu").numpy()  # = the GPU arm's array-frames 0-1
+    sample = 3 if wl.H * wl.W <= 4_000_000 else 2
+    times = cpu_reference_sample(fr, sample + 1, threads, wl.wrap)[1:]
+    sec = sum(times) / len(times)
+    mp_frame = wl.n_cams * wl.H * wl.W / 1e6
+    cpu = {"value": round(mp_frame / sec, 3), "unit": "MP/s", "cores": threads, "kind": "port",
+           "sample": f"{sample} array-frames of {wl.name} (the GPU arm's frames 0-1; numpy "
+                     f"restatement of the reference: update_exposure per seam + apply_exposure "
+                     f"per side, fresh maps, {threads} threads)",
+           "array_frames_per_sec": round(1.0 / sec, 4), "cpu_model": cpu_model(),
+           "nproc": threads}
+    try:  # SURVEY 8d variants: one thread, and steady state (cached maps)
+        t1 = cpu_reference_sample(fr, 1, 1, wl.wrap)
+        g = wl.res.gain[0].cpu().numpy()
+        o = wl.res.offset[0].cpu().numpy()
+        tc = cpu_cached_apply_sample(fr, sample + 1, threads, g, o, wl.wrap)[1:]
+        tc1 = cpu_cached_apply_sample(fr, 2, 1, g, o, wl.wrap)[1:]
+        cpu["variants"] = {
+            "fresh_maps_all_threads_mp_s": cpu["value"],
+            "fresh_maps_1_thread_mp_s": round(mp_frame / t1[0], 3),
+            "cached_maps_all_threads_mp_s": round(mp_frame / (sum(tc) / len(tc)), 3),
+            "cached_maps_1_thread_mp_s": round(mp_frame / tc1[0], 3),
+        }
+    except Exception as e:  # pragma: no cover
+        cpu["variants"] = {"failed": str(e)}
+    return cpu
+
+
 def run_camx(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
-
-    from paper_1910_03517_b200.array import ArrayCorrector
-    from paper_1910_03517_b200.dist import camera_partition, sharded_corrector
-    from paper_1910_03517_b200.exposure import ExposureConfig, ExposureMode
-    from paper_1910_03517_b200.synth import synthetic_batch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -256,24 +565,6 @@ def run_camx(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
-    name = args.workload or ("config3" if world > 1 else "config2")
-    n_cams, H, W, B0, desc = WORKLOADS[name]
-    B = args.batch or B0
-    mode = ExposureMode(args.mode)
-    cfg = ExposureConfig()
-    wrap = name == "config4"
-    if world > 1:
-        ac = sharded_corrector(n_cams, H, W, cfg, mode, wrap=wrap, histograms=not args.no_hist)
-        begin, count = camera_partition(n_cams, world)[rank]
-    else:
-        ac = ArrayCorrector(n_cams, H, W, cfg, mode, wrap=wrap, histograms=not args.no_hist)
-        begin, count = 0, n_cams
-    full = synthetic_batch(B, n_cams, H, W, seed=100)
-    frames = full[:, begin:begin + count].contiguous()
-    del full
-    out = torch.empty_like(frames)
-    stream = torch.cuda.Stream()
-    px_per_frame = n_cams * H * W                      # whole-job pixels per array-frame
 
     def barrier():
         # drain this rank's GPU work first: the sharded path's own NCCL
@@ -284,248 +575,66 @@ def run_camx(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    tiles_mode = name == "config5"
-    tiles_buf = None
-    if tiles_mode:
-        n_tiles = len(ac.tile_windows(960)) * B
-        tiles_buf = torch.empty((n_tiles, 416, 416, 3), dtype=torch.uint8, device="cuda")
-
-    use_graph = not args.no_graph and world == 1 and not tiles_mode
-    # N > 1 over NCCL: the front half (K1 -> all-gather -> K2) of batch k on a
-    # side stream under K3 of batch k-1 (ArrayCorrector.submit)
-    use_pipe = (world > 1 and getattr(ac, "comm", None) is not None and not tiles_mode
-                and os.environ.get("CAMX_SHARD_PIPE", "1") != "0")
-
-    def step():
-        if tiles_mode:
-            return ac.correct_and_tile(frames, out=out, tiles=tiles_buf, stream=stream)[0]
-        if use_graph:  # CUDA graph replay of K1 -> K2 -> K3 (+ state carry)
-            return ac.correct_graphed(frames, out)
-        if use_pipe:
-            return ac.submit(frames, out, stream=stream)
-        return ac.correct(frames, out, stream=stream)
-
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            step()
-    barrier()
-
-    # timed region: K steps, events on the launching stream, every camx
-    # kernel launch counted
-    n_launch = [0]
-    from paper_1910_03517_b200 import _lib
-    orig_call = _lib.call
-
-    def traced_call(fn, *a):
-        if fn in ("camx_correct_batch", "camx_correct_batch_tiles"):
-            # K1 (x2 for OBJECT_REMOVAL with B > 1 and no previous frame) + K2 + K3
-            # (+ tile fix-up)
-            two_k1 = mode is ExposureMode.OBJECT_REMOVAL and a[3] > 1 and a[2] is None
-            n_launch[0] += 3 if two_k1 else 2
-            n_launch[0] += 1 if fn == "camx_correct_batch" else 2
-        elif fn == "camx_correct_batch_sharded":  # K1 (x2) + K2 + K3 (+ NCCL, not ours)
-            two_k1 = mode is ExposureMode.OBJECT_REMOVAL and a[3] > 1 and a[2] is None
-            n_launch[0] += 4 if two_k1 else 3
-        elif fn == "camx_correct_batch_sharded_step":
-            if a[0] is not None:  # front half: K1 (x2 without a previous frame) + K2
-                two_k1 = mode is ExposureMode.OBJECT_REMOVAL and a[2] > 1 and a[1] is None
-                n_launch[0] += 3 if two_k1 else 2
-            if a[21] is not None:  # back half: K3 of the previous batch
-                n_launch[0] += 1
-        elif fn.startswith("camx_"):
-            n_launch[0] += 1
-        orig_call(fn, *a)
-
-    start = torch.cuda.Event(enable_timing=True)
-    stop = torch.cuda.Event(enable_timing=True)
-    _lib.call = traced_call
-    try:
-        with ClockSampler(torch.cuda.current_device()) as clk:
-            barrier()
-            start.record(stream)
-            with torch.cuda.stream(stream):
-                for _ in range(args.steps):
-                    res = step()
-            stop.record(stream)
-            stop.synchronize()
-            barrier()
-    finally:
-        _lib.call = orig_call
-    if use_pipe:  # drain the pipeline (outside the timed region)
-        with torch.cuda.stream(stream):
-            res = ac.flush(stream=stream) or res
-        torch.cuda.synchronize()
-    if use_graph:  # replays do not pass through _lib.call: same kernels as an eager step
-        per_step = 3  # K1 (one launch: the captured tick has a previous frame), K2, K3
-        n_launch[0] = per_step * args.steps
-
-    # roofline leg: the dominant kernel (K3 apply) alone, same buffers and
-    # maps as the last step, CUDA events on its stream around each launch
-    # (config 5: the fused apply+tile kernel and its fix-up, whose
-    # algorithmic bytes add the tile writes to K3's read + write)
-    k3_ev = []
-    k3_launch_bytes = 6 * B * count * H * W
-    k3_name = "camx apply_tma_kernel (K3)"
-    if tiles_mode:
-        wins = sorted((b, x, y) for b in range(B) for (x, y) in ac.tile_windows(960))
-        wins = sorted(wins, key=lambda w: w[0])
-        per_b = np.bincount(np.asarray([w[0] for w in wins]), minlength=B)
-        w_dev = torch.as_tensor(np.asarray(wins, dtype=np.int32).reshape(-1, 3), device="cuda")
-        off_dev = torch.as_tensor(np.concatenate([[0], np.cumsum(per_b)]).astype(np.int32),
-                                  device="cuda")
-        k3_launch_bytes += tiles_buf.numel()
-        k3_name = "camx apply_tma_kernel<fused tiles> + tile_fixup (K3+K5)"
-    with torch.cuda.stream(stream):
-        for _ in range(max(3, min(args.steps, 20))):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            if tiles_mode:
-                _lib.call("camx_correct_and_tile", frames.data_ptr(), out.data_ptr(), B, n_cams,
-                          int(wrap), H, W, cfg.blocks, res.gain.data_ptr(),
-                          res.offset.data_ptr(), w_dev.data_ptr(), off_dev.data_ptr(),
-                          len(wins), int(per_b.max()), 960, 416, tiles_buf.data_ptr(),
-                          stream.cuda_stream)
-            else:
-                _lib.call("camx_apply_array", frames.data_ptr(), out.data_ptr(), B, begin, count,
-                          n_cams, int(wrap), H, W, cfg.blocks, res.gain.data_ptr(),
-                          res.offset.data_ptr(), stream.cuda_stream)
-            e1.record(stream)
-            k3_ev.append((e0, e1))
-    torch.cuda.synchronize()
-    ms = start.elapsed_time(stop)
-    k3_ms = sum(a.elapsed_time(b) for a, b in k3_ev) / len(k3_ev)
-    k3_share = k3_ms * args.steps / ms
-    if world > 1:
-        tt = torch.tensor([ms, k3_ms], device="cuda", dtype=torch.float64)
+    def max_ranks(*vals):
+        if world == 1:
+            return vals
+        tt = torch.tensor(vals, device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, k3_ms = float(tt[0]), float(tt[1])
-        k3_share = k3_ms * args.steps / ms
-    ms_per_step = ms / args.steps
-    mp_per_s = B * px_per_frame / 1e6 / (ms_per_step / 1e3)
-    afps = B / (ms_per_step / 1e3)
+        return tuple(float(v) for v in tt)
+
     peak, peak_kind = peaks()
-    achieved = k3_launch_bytes / (k3_ms / 1e3) / 1e9
-    traffic = None
-    tp = ROOT / "profiles" / "apply_traffic.json"
-    if tp.exists():
-        try:
-            entries = json.loads(tp.read_text())
-            entries = entries.get("entries", [entries])
-            for d in entries:
-                if d.get("workload") == name:
-                    # DRAM bytes per algorithmic byte of the captured launch,
-                    # scaled to this run's launch size (streaming kernel)
-                    traffic = int(d["dram_bytes_per_launch"] / d["algorithmic_bytes_per_launch"]
-                                  * k3_launch_bytes)
-        except Exception:
-            pass
+    name = args.workload or ("config3" if world > 1 else "config2")
+    B = args.batch or WORKLOADS[name][3]
+    wl = Workload(name, B, args, world, rank, torch).run(args.steps, args.warmup, barrier)
+    wl.roofline_leg(max(3, min(args.steps, 20)))
+    wl.ms, wl.k_ms = max_ranks(wl.ms, wl.k_ms)
+    main = wl.summary(peak, peak_kind)
 
-    # e2e through the public host API (pinned host in -> pinned host out)
     e2e = None
-    if not args.no_e2e and not tiles_mode:
-        Be = min(args.e2e_batch, B)
-        host_in = frames[:Be].cpu().pin_memory()
-        host_out = torch.empty_like(host_in).pin_memory()
-        ac.reset()
-        for _ in range(max(1, min(args.warmup, 2))):
-            ac.correct_host(host_in, host_out)
-        torch.cuda.synchronize()
-        e_steps = max(2, min(args.steps, 10))
-        barrier()
-        t0 = time.perf_counter()
-        e_start = torch.cuda.Event(enable_timing=True)
-        e_stop = torch.cuda.Event(enable_timing=True)
-        e_start.record()
-        last = None
-        for _ in range(e_steps):  # a stream of batches: consecutive calls pipeline
-            _, last = ac.correct_host(host_in, host_out, wait=False)
-        torch.cuda.current_stream().wait_event(last)
-        e_stop.record()
-        e_stop.synchronize()
-        e_ms = e_start.elapsed_time(e_stop)
-        if world > 1:
-            tt = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e_ms = float(tt[0])
-        wall = time.perf_counter() - t0
-        e_ms_step = e_ms / e_steps
-        # every rank copies its camera shard: whole-job bytes = world x this rank's
-        # (shards are equal for the benchmark configs)
-        e2e = {"value": round(Be * px_per_frame / 1e6 / (e_ms_step / 1e3), 2), "unit": "MP/s",
-               "h2d_bytes_per_step": int(host_in.numel()) * world,
-               "d2h_bytes_per_step": int(host_out.numel()) * world,
-               "array_frames_per_sec": round(Be / (e_ms_step / 1e3), 2),
-               "batch": Be, "steps": e_steps, "wall_s": round(wall, 3),
-               "path": "ArrayCorrector.correct_host (pinned ring, 3 streams, batches pipelined)",
-               "pcie_bytes_per_sec_each_way": round(host_in.numel() / (e_ms_step / 1e3) / 1e9, 2)}
-
+    if not args.no_e2e and not wl.tiles:
+        e2e = e2e_ring(wl, min(args.e2e_batch, B), max(2, min(args.steps, 10)), args.warmup,
+                       barrier, world)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
-            fr = frames[:2].cpu().numpy()
-            sample = 3 if H * W <= 4_000_000 else 2
-            times = cpu_reference_sample(fr, sample + 1, threads)[1:]
-            sec = sum(times) / len(times)
-            mp_frame = n_cams * H * W / 1e6
-            cpu = {"value": round(mp_frame / sec, 3), "unit": "MP/s", "cores": threads,
-                   "kind": "port",
-                   "sample": f"{sample} array-frames of {name} (numpy restatement of the "
-                             f"reference: update_exposure per seam + apply_exposure per side, "
-                             f"fresh maps, {threads} threads)",
-                   "array_frames_per_sec": round(1.0 / sec, 4),
-                   "cpu_model": cpu_model(), "nproc": threads}
-            # SURVEY 8d variants: one thread, and steady state (cached maps)
-            try:
-                t1 = cpu_reference_sample(fr, 1, 1)
-                g = res.gain[0].cpu().numpy()
-                o = res.offset[0].cpu().numpy()
-                tc = cpu_cached_apply_sample(fr, sample + 1, threads, g, o, wrap)[1:]
-                tc1 = cpu_cached_apply_sample(fr, 2, 1, g, o, wrap)[1:]
-                cpu["variants"] = {
-                    "fresh_maps_all_threads_mp_s": cpu["value"],
-                    "fresh_maps_1_thread_mp_s": round(mp_frame / t1[0], 3),
-                    "cached_maps_all_threads_mp_s": round(mp_frame / (sum(tc) / len(tc)), 3),
-                    "cached_maps_1_thread_mp_s": round(mp_frame / tc1[0], 3),
-                }
-            except Exception as e:  # pragma: no cover
-                cpu["variants"] = {"failed": str(e)}
+            cpu = cpu_baseline_line(wl, args)
         except Exception as e:  # pragma: no cover
-            cpu = {"value": None, "unit": "MP/s", "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+            cpu = {"value": None, "unit": "MP/s", "cores": 0, "kind": "port",
+                   "sample": f"failed: {e}"}
+    line_cfg = wl.config()
+    clocks, launches = wl.clocks, wl.launches
+    wl.free()
+
+    # the other single-GPU workloads BASELINE.json names, each timed and
+    # rooflined the same way (same steps / warm-up, own clocks)
+    secondary = []
+    if world == 1 and args.workload is None and not args.no_secondary:
+        for nm in ("config4", "config5"):
+            w2 = Workload(nm, WORKLOADS[nm][3], args, world, rank, torch).run(
+                args.steps, args.warmup, barrier)
+            w2.roofline_leg(max(3, min(args.steps, 20)))
+            d = w2.summary(peak, peak_kind)
+            d.update(config=w2.config(), clocks=w2.clocks, gpu_launches=w2.launches,
+                     steps=args.steps, warmup=args.warmup)
+            secondary.append(d)
+            w2.free()
 
     if rank == 0:
         line = {
-            "metric": "corrected megapixels/sec", "value": round(mp_per_s, 2), "unit": "MP/s",
+            "metric": "corrected megapixels/sec", "value": main["value"], "unit": "MP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (on-device panorama + per-camera affine distortion + moving objects)",
-            "array_frames_per_sec": round(afps, 2),
-            "config": {"workload": f"{name}: {desc}", "batch": B, "mode": mode.value,
-                       "histograms": not args.no_hist,
-                       "tiles_per_step": (tiles_buf.shape[0] if tiles_mode else 0),
-                       "cameras_per_gpu": count, "frame": f"{W}x{H}",
-                       "step": ("K1 band stats" + ("" if args.no_hist else " + histograms") +
-                                " + K2 seam solve + K3 apply per array-frame"),
-                       "l2": "inputs larger than L2 (batch >> 126 MB)",
-                       "parallelism": f"camera-shard{world}" if world > 1 else "single",
-                       "launch": ("cuda-graph replay" if use_graph else
-                                  "software-pipelined: K1 -> NCCL all-gather -> K2 of batch k on "
-                                  "a side stream under K3 of batch k-1" if use_pipe else
-                                  "eager (PDL-chained)")},
-            "roofline": {"bound": "hbm", "kernel": k3_name,
-                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "peak_kind": peak_kind, "k3_ms_per_launch": round(k3_ms, 4),
-                         "k3_bytes_per_launch": k3_launch_bytes,
-                         "k3_launches_timed": len(k3_ev),
-                         "k3_share_of_step": round(k3_share, 4)},
-            "clocks": clk.summary(),
+            "ms_per_step": main["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": DATA,
+            "array_frames_per_sec": main["array_frames_per_sec"],
+            "config": line_cfg,
+            "roofline": main["roofline"],
+            "clocks": clocks,
             "e2e": e2e,
-            "gpu_launches": n_launch[0],
+            "gpu_launches": launches,
             "cpu_baseline": cpu,
         }
+        if secondary:
+            line["secondary"] = secondary
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

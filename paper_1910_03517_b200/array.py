@@ -18,7 +18,9 @@ maps (and, for OBJECT_REMOVAL, its last frame) seed the next batch.
 
 `correct_host` is the end-to-end entry point from pinned host memory: a
 3-slot device ring with H2D, compute and D2H on separate streams so the
-PCIe copies of chunk i+1 / i-1 overlap the kernels of chunk i.
+PCIe copies of chunk i+1 / i-1 overlap the kernels of chunk i.  The
+streaming frame source with library-owned pinned slots and a producer /
+consumer API is ring.FrameRing.
 """
 
 from __future__ import annotations
@@ -638,25 +640,39 @@ class ArrayCorrector:
         return maps
 
     # ------------------------------------------------------------ host path
-    def correct_host(self, frames_host, out_host=None, *, chunk: int = 1, wait: bool = True):
+    def correct_host(self, frames_host, out_host=None, *, chunk: int = 1, wait: bool = True,
+                     stage: bool = False):
         """End-to-end correction of host frames (B, N, H, W, 3) uint8.
 
-        frames_host/out_host: pinned torch CPU tensors for full-speed async
-        copies (numpy arrays are accepted and wrapped, at pageable-copy
-        speed).  H2D, kernels and D2H of consecutive chunks overlap on three
-        streams.  wait=True returns out_host once it is filled; wait=False
-        returns (out_host, event) right away so consecutive calls pipeline
-        (the next batch's H2D overlaps this batch's D2H) - synchronize the
-        event before reading out_host or reusing frames_host."""
+        frames_host/out_host: PINNED torch CPU tensors (async copies at full
+        PCIe speed; ring.FrameRing hands out such buffers).  Pageable input
+        (numpy arrays, unpinned tensors) is rejected with ValueError unless
+        stage=True, which copies it into a pinned staging tensor first -
+        explicitly, never silently.  H2D, kernels and D2H of consecutive
+        chunks overlap on three streams.  wait=True returns out_host once
+        it is filled; wait=False returns (out_host, event) right away so
+        consecutive calls pipeline (the next batch's H2D overlaps this
+        batch's D2H) - synchronize the event before reading out_host or
+        reusing frames_host."""
         t = _dev.require_cuda()
         src = frames_host if isinstance(frames_host, t.Tensor) else t.from_numpy(
             np.ascontiguousarray(frames_host))
+        if src.is_cuda:
+            raise ValueError("correct_host takes host frames; use correct() for CUDA tensors")
+        if not src.is_pinned():
+            if not stage:
+                raise ValueError("frames_host is pageable memory: pass a pinned tensor "
+                                 "(tensor.pin_memory(), ring.FrameRing) or stage=True")
+            src = src.pin_memory()
         if src.dim() == 4:
             src = src[None]
         B = src.shape[0]
         if out_host is None:
             out_host = t.empty(src.shape, dtype=t.uint8, pin_memory=True)
         dst = out_host if isinstance(out_host, t.Tensor) else t.from_numpy(out_host)
+        if not dst.is_pinned():
+            raise ValueError("out_host must be pinned memory (a D2H into pageable memory "
+                             "is synchronous)")
         ring = self._host_ring(chunk)
         n_chunks = (B + chunk - 1) // chunk
         cur = t.cuda.current_stream()

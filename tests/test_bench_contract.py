@@ -56,7 +56,7 @@ def test_camx_arm_json_line_on_gpu():
     launches), clocks sampled in the timed region, e2e through the host path,
     and a non-zero count of our own kernel launches."""
     r = _run(["--steps", "3", "--warmup", "3", "--batch", "4", "--e2e-batch", "2",
-              "--no-cpu-baseline"])
+              "--no-cpu-baseline", "--no-secondary"])
     assert r.returncode == 0, r.stderr[-2000:]
     d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip()][-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
@@ -70,3 +70,20 @@ def test_camx_arm_json_line_on_gpu():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 3 * d["steps"]
     assert "workload" in d["config"]
+    assert "FrameRing" in d["e2e"]["path"]
+
+
+@pytest.mark.gpu
+def test_camx_arm_secondary_workloads_on_gpu():
+    """The default N=1 line also carries config4 and config5, each with its
+    own roofline and clocks."""
+    r = _run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"], timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip()][-1])
+    sec = {x["workload"].split(":")[0]: x for x in d["secondary"]}
+    assert set(sec) == {"config4", "config5"}
+    for x in sec.values():
+        assert x["value"] > 0 and x["roofline"]["bound"] == "hbm" and "clocks" in x
+        assert 0 < x["roofline"]["frac"] <= 1.2 and x["gpu_launches"] >= 3 * x["steps"]
+    assert sec["config4"]["config"]["wrap"] and sec["config4"]["config"]["batch"] == 64
+    assert sec["config5"]["config"]["tiles_per_step"] == 36 * 30
