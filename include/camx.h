@@ -128,25 +128,6 @@ int camx_seam_solve(const camx_band_stat *stats, int32_t n_batch,
                     const double *prev_offset, double *gain_out,
                     double *offset_out, uint8_t *fit_ok_out, void *stream);
 
-/* Fused K1 + K2 for array-frames [frame_begin, frame_begin + frame_count)
- * of an n_batch x n_cams batch: band statistics of those frames (images
- * points at frame frame_begin; prev_images, if non-NULL, at the frame
- * preceding it, OBJECT_REMOVAL's in-band motion mask with t_diff), and -
- * by the last CTA to publish a record of each (seam, block) - the whole
- * batch's camx_seam_solve for that seam block.  stats/hist/maps point at
- * the WHOLE batch; `counters` is an int32 [S*K] device array that must be
- * zero before the first launch of a batch and is re-armed to zero by the
- * solve.  Several launches may cover one batch (OBJECT_REMOVAL: frame 0
- * against the previous batch, frames 1.. against their predecessors). */
-int camx_band_stats_solve(const uint8_t *images, const uint8_t *prev_images,
-                          int32_t n_batch, int32_t n_cams, int32_t frame_begin,
-                          int32_t frame_count, int32_t height, int32_t width,
-                          int32_t band_width, int32_t t_diff, int32_t wrap,
-                          const camx_solve_config *cfg, const double *prev_gain,
-                          const double *prev_offset, camx_band_stat *stats,
-                          uint32_t *hist, double *gain_out, double *offset_out,
-                          uint8_t *fit_ok_out, int32_t *counters, void *stream);
-
 /* fit_affine (exposure.py:188-229) on float moments (BandStats fields).
  * l_mean/l_std/r_mean/r_std: [K][3]; l_valid/r_valid: [K].
  * gain_out/offset_out: [2 sides][K][3]; fit_ok_out: [K] bytes. */
@@ -184,11 +165,12 @@ int camx_apply_array(const uint8_t *images, uint8_t *out, int32_t n_batch,
 /* The whole hot path for a batch of n_batch array-frames x n_cams cameras
  * on one GPU: K1 band statistics, K2 seam solve and K3 apply, K2 and K3 as
  * programmatic dependent launches (K3's TMA pixel prefetch overlaps the
- * solve).  `counters` is unused (reserved for the fused
- * camx_band_stats_solve variant; may be NULL).  = update_exposure for every seam + apply of
+ * solve).  `counters` is unused (reserved; may be NULL).  = update_exposure for every seam + apply of
  * both seam sides of every camera, tick loop over the batch.  prev_frame
  * (n_cams images, OBJECT_REMOVAL only, may be NULL) is the array-frame
- * before frame 0.  Buffers as camx_band_stats_solve / camx_apply_array. */
+ * before frame 0.  stats [n_batch][n_cams][2][K] records; hist (optional)
+ * [n_batch][n_cams][2][K][3][256]; gain/offset [n_batch][S][2][K][3];
+ * fit_ok [n_batch][S][K]. */
 int camx_correct_batch(const uint8_t *images, uint8_t *out,
                        const uint8_t *prev_frame, int32_t n_batch,
                        int32_t n_cams, int32_t wrap, int32_t height,

@@ -73,8 +73,6 @@ SIGNATURES = {
                                    P, P, P, P, P, P, P, P, P, I32, P, P],
     "camx_correct_batch_sharded_step": [P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, I32,
                                         P, P, P, P, P, P, P, P, P, P, P, I32, P, P, P, P],
-    "camx_band_stats_solve": [P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P,
-                              P, P, P, P, P],
     "camx_correct_batch": [P, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P,
                            P],
     "camx_fit_affine": [P, P, P, P, P, P, I32, F64, I64, P, P, P, P],

@@ -26,7 +26,6 @@ consumer API is ring.FrameRing.
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -174,37 +173,14 @@ class ArrayCorrector:
         if self.comm is not None and self.S > 0:
             self._correct_sharded(frames, out, buf, _dev.stream_handle(main), pf)
             return self._finish(frames, out, buf, main, removal)
-        if self.exchange is None and self.S > 0 and self.pipeline_chunks <= 1 and self.fused:
+        if self.exchange is None and self.S > 0 and self.fused:
             self._correct_fused(frames, out, buf, _dev.stream_handle(main), pf, _tile_args)
             return self._finish(frames, out, buf, main, removal)
-        # Chunked pipeline: K1+K2 of chunk i+1 run on a side stream while K3
-        # of chunk i streams on `main`; the tick-loop state flows between
-        # chunks through device pointers (no copies).
-        n_chunks = max(1, min(self.pipeline_chunks, B))
-        bounds = [(B * i) // n_chunks for i in range(n_chunks + 1)]
-        side = self._side_stream() if n_chunks > 1 else main
-        if side is not main:
-            side.wait_stream(main)
-        prev_maps = self._prev_maps
-        prev_frame_ptr = _dev.ptr(pf)
-        ready = []
-        for i in range(n_chunks):
-            lo, hi = bounds[i], bounds[i + 1]
-            if hi <= lo:
-                continue
-            self._stats_solve(frames, buf, lo, hi, _dev.stream_handle(side), prev_maps,
-                              prev_frame_ptr if removal else None)
-            ev = t.cuda.Event()
-            ev.record(side)
-            ready.append((lo, hi, ev))
-            if self.S > 0:
-                prev_maps = (buf["gain"][hi - 1], buf["offset"][hi - 1])
-            prev_frame_ptr = frames[hi - 1].data_ptr()
-        for lo, hi, ev in ready:
-            main.wait_event(ev)
-            self._apply(frames, out, buf, lo, hi, _dev.stream_handle(main))
-        if side is not main:
-            main.wait_stream(side)
+        # separate launches: K1 (+ the Python stats exchange of a camera shard
+        # on a non-NCCL backend) -> K2 -> K3, all on `main`
+        sh = _dev.stream_handle(main)
+        self._stats_solve(frames, buf, 0, B, sh, self._prev_maps, _dev.ptr(pf) if removal else None)
+        self._apply(frames, out, buf, 0, B, sh)
         return self._finish(frames, out, buf, main, removal)
 
     def _finish(self, frames, out, buf, main, removal) -> CorrectResult:
@@ -232,18 +208,13 @@ class ArrayCorrector:
         return CorrectResult(out, gain[:, : self.S], off[:, : self.S], buf["fit_ok"][:, : self.S],
                              full, buf["hist"])
 
-    # >1: K1+K2 of chunk i+1 on a side stream under K3 of chunk i.  Measured
-    # slower than the fused single-chunk path on B200 (smaller K3 launches,
-    # SM contention), so only the sharded path uses chunks.
-    pipeline_chunks = 1
-    # fused K1+K2 (+PDL K3) single call; CAMX_FUSED=0 selects K1, K2, K3 launches
-    fused = os.environ.get("CAMX_FUSED", "1") != "0"
-    # camx_band_stats_solve (K1+K2 in one kernel, last-arriver solve) instead
-    # of K1 -> K2 (PDL); measured slower on B200 (96 regs, serial tail)
-    fused_stats_solve = os.environ.get("CAMX_FUSED_K12", "0") == "1"
+    # K1 -> K2 -> K3 as one camx_correct_batch call (K2, K3 programmatic
+    # dependents).  False: the separate-launch path the Python stats
+    # exchange needs (kept testable on one GPU).
+    fused = True
 
     def _correct_fused(self, frames, out, buf, sh, pf, tile_args=None):
-        """camx_correct_batch: fused K1+K2 (last-arriver solve) + K3 (PDL)."""
+        """camx_correct_batch: K1 -> K2 -> K3 (PDL-chained) in one C call."""
         cfg = self.cfg
         B = frames.shape[0]
         removal = self.mode is ExposureMode.OBJECT_REMOVAL
@@ -253,25 +224,6 @@ class ArrayCorrector:
                               float(cfg.min_valid_fraction), int(have_prev),
                               int(removal and pf is not None))
         pg, po = self._prev_maps if have_prev else (None, None)
-        if "counters" not in buf:
-            buf["counters"] = _dev.torch().zeros((self.S * self.K,), dtype=_dev.torch().int32,
-                                                 device="cuda")
-        if self.fused_stats_solve:
-            N, H, W = self.n_cams, self.height, self.width
-            fb = N * H * W * 3
-            base = frames.data_ptr()
-            common = (H, W, cfg.band_width, cfg.t_diff, int(self.wrap), ctypes.byref(sc),
-                      _dev.ptr(pg), _dev.ptr(po), buf["stats"].data_ptr(), _dev.ptr(buf["hist"]),
-                      buf["gain"].data_ptr(), buf["offset"].data_ptr(), buf["fit_ok"].data_ptr(),
-                      buf["counters"].data_ptr(), sh)
-            if removal and B > 1:
-                _lib.call("camx_band_stats_solve", base + fb, base, B, N, 1, B - 1, *common)
-                _lib.call("camx_band_stats_solve", base, _dev.ptr(pf), B, N, 0, 1, *common)
-            else:
-                _lib.call("camx_band_stats_solve", base, _dev.ptr(pf) if removal else None, B, N,
-                          0, B, *common)
-            self._apply(frames, out, buf, 0, B, sh)
-            return
         common = (frames.data_ptr(), out.data_ptr(), _dev.ptr(pf) if removal else None, B,
                   self.n_cams, int(self.wrap), self.height, self.width, cfg.band_width,
                   cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),
@@ -280,7 +232,7 @@ class ArrayCorrector:
         if tile_args is not None:
             _lib.call("camx_correct_batch_tiles", *common, *tile_args, sh)
         else:
-            _lib.call("camx_correct_batch", *common, buf["counters"].data_ptr(), sh)
+            _lib.call("camx_correct_batch", *common, None, sh)
 
     def _correct_sharded(self, frames, out, buf, sh, pf):
         """camx_correct_batch_sharded: K1 on this rank's cameras, NCCL
@@ -463,21 +415,14 @@ class ArrayCorrector:
                 0, self._pipe["index"]).view(B, self.n_cams, 2, self.K, R)
         return CorrectResult(out, b["gain"], b["offset"], b["fit_ok"], full, b["hist"])
 
-    @staticmethod
-    def shard_chunks(world: int) -> int:
-        """Chunks of the sharded batch (K1 + all-gather + K2 of chunk c+1
-        under K3 of chunk c).  Measured slower at every N on B200 (smaller
-        K3 launches, per-chunk launch and collective latency:
-        tools/shard_probe_native.py), so 1 unless CAMX_SHARD_CHUNKS says."""
-        env = os.environ.get("CAMX_SHARD_CHUNKS")
-        if env:
-            return max(1, min(8, int(env)))
-        return 1
+    # camx_correct_batch_sharded can split a batch into chunks (K1 + all-
+    # gather + K2 of chunk c+1 on a side stream under K3 of chunk c); measured
+    # slower at every N on B200 (smaller K3 launches, per-chunk launch and
+    # collective latency: tools/shard_probe_native.py), so one chunk.
+    shard_chunk_count = 1
 
-    def _side_stream(self):
-        if getattr(self, "_side", None) is None:
-            self._side = _dev.torch().cuda.Stream()
-        return self._side
+    def shard_chunks(self, world: int) -> int:
+        return max(1, min(8, int(self.shard_chunk_count)))
 
     def _stats_solve(self, frames, buf, lo, hi, sh, prev_maps, prev_frame_ptr):
         """K1 + (exchange) + K2 for array-frames [lo, hi) on stream `sh`."""
@@ -611,7 +556,7 @@ class ArrayCorrector:
             tiles = t.empty((T, out_size, out_size, 3), dtype=t.uint8, device="cuda")
         tile_args = (wd[0].data_ptr(), wd[1].data_ptr(), T, wd[2], int(size), int(out_size),
                      tiles.data_ptr())
-        if self.exchange is None and self.S > 0 and self.fused and not self.fused_stats_solve:
+        if self.exchange is None and self.S > 0 and self.fused:
             if frames.dim() == 4:
                 frames = frames[None]
             if out is None:

@@ -124,7 +124,6 @@ __device__ __forceinline__ void coef_f32(int col, int ch, int k, int W, const do
 // ---------------------------------------------------------------- fast path
 // Requires row_bytes % 16 == 0 and 16-byte aligned src/dst.
 constexpr int kApplyThreads = 128;
-constexpr int kUnroll = 4;
 
 struct Coef16 {
   uint64_t m[8];  // pairs (M/256, M/256) for sub-pixels (2i, 2i+1)
@@ -211,80 +210,13 @@ __device__ __forceinline__ uint4 correct16(uint4 v, const Coef16 &cf) {
   return r;
 }
 
-__global__ void __launch_bounds__(kApplyThreads, 4) apply_fast_kernel(const ApplyParams p) {
-  int64_t item = blockIdx.x;
-  const int cg = static_cast<int>(item % p.col_groups);
-  item /= p.col_groups;
-  const int rs = static_cast<int>(item % p.row_splits);
-  item /= p.row_splits;
-  const int k = static_cast<int>(item % p.K);
-  const int64_t img = item / p.K;
-
-  const int j = cg * kApplyThreads + threadIdx.x;  // 16-byte chunk in the row
-  if (j >= p.chunks_per_row) return;
-
-  const int blk_r0 = k * p.bh;
-  const int blk_r1 = (k == p.K - 1) ? p.H : blk_r0 + p.bh;
-  const int r0 = blk_r0 + rs * p.rows_per_split;
-  const int r1 = min(blk_r1, r0 + p.rows_per_split);
-  if (r0 >= r1) return;
-
-  const double *gl, *bl, *gr, *br;
-  map_ptrs(p, img, gl, bl, gr, br);
-
-  Coef16 cf;
-  {
-    const int q0 = j * 16;
-    int col = q0 / 3;
-    int ch = q0 - col * 3;
-    float m[16], a[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      coef_f32(col, ch, k, p.W, gl, bl, gr, br, m[i], a[i]);
-      if (++ch == 3) {
-        ch = 0;
-        ++col;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 16; i += 2) {
-      cf.m[i >> 1] = pack2(m[i] * 0.00390625f, m[i + 1] * 0.00390625f);
-      cf.c[i >> 1] = pack2(m[i] * -32768.0f, m[i + 1] * -32768.0f);
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      // |A| < 2^-110 cannot change rn(p*M + A) (see header); zero it so the
-      // 2^-8 scaling stays exact (no subnormal).
-      cf.a[i] = fabsf(a[i]) < 7.7037197787136e-34f ? 0.0f : a[i] * 0.00390625f;
-    }
-  }
-
-  const uint8_t *src = p.src + img * p.img_bytes + static_cast<int64_t>(r0) * p.row_bytes + j * 16;
-  uint8_t *dst = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * p.row_bytes + j * 16;
-  const int64_t rb = p.row_bytes;
-  int r = r0;
-  for (; r + kUnroll <= r1; r += kUnroll) {
-    uint4 v[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream_v4(src + u * rb);
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) st_stream_v4(dst + u * rb, correct16(v[u], cf));
-    src += kUnroll * rb;
-    dst += kUnroll * rb;
-  }
-  for (; r < r1; ++r) {
-    st_stream_v4(dst, correct16(ld_stream_v4(src), cf));
-    src += rb;
-    dst += rb;
-  }
-}
-
 // ------------------------------------------------- TMA bulk-copy pipeline
-// Same work decomposition as apply_fast_kernel, but the rows stream through
-// a kStages-deep shared-memory ring filled by 1-D bulk async copies
-// (cp.async.bulk, the TMA engine) completing on mbarriers, so the bytes in
-// flight per SM no longer depend on registers x occupancy (the LDG version
-// is long-scoreboard bound at 16 warps/SM).  Thread 0 issues; every thread
+// CTA = one 2 KB column group of one row block (split) of one image, thread
+// = one 16-byte chunk; the rows stream through a kStages-deep shared-memory
+// ring filled by 1-D bulk async copies (cp.async.bulk, the TMA engine)
+// completing on mbarriers, so the bytes in flight per SM do not depend on
+// registers x occupancy (a plain 128-bit LDG version was long-scoreboard
+// bound at 16 warps/SM and ~5% slower: profiles/r01/SUMMARY.md).  Thread 0 issues; every thread
 // consumes its 16-byte column chunk of each row from shared memory.
 constexpr int kTmaStages = 6;
 constexpr int kTmaRows = 2;  // rows per stage
@@ -854,15 +786,6 @@ static int launch_tma(const ApplyParams &p, const TileFuse &q, cudaStream_t stre
 static int launch_apply(ApplyParams &p, cudaStream_t stream) {
   if (p.n_img <= 0 || p.H <= 0 || p.W <= 0) return CAMX_OK;
   if (plan_fast(p)) {
-    static const int use_ldg = [] {
-      const char *e = getenv("CAMX_APPLY_KERNEL");
-      return (e != nullptr && e[0] == 'l') ? 1 : 0;
-    }();
-    if (use_ldg) {
-      const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
-      apply_fast_kernel<<<static_cast<unsigned>(grid), kApplyThreads, 0, stream>>>(p);
-      return launch_status();
-    }
     // short CTAs (<= 48 rows, e.g. 640x480 frames: 30-row blocks) spend more
     // of their life in the prologue / first fills: one more resident CTA per
     // SM (72 registers) hides it (config 1 K3 56.8 -> 51.3 us); whole 96-row
@@ -1055,11 +978,7 @@ static int apply_and_tile(ApplyParams &p, const int32_t *windows, const int32_t 
   if (n_tiles < 0 || size < 1 || out_size < 1 || size > p.H || size > p.n_cams * p.W)
     return CAMX_EINVAL;
   if (n_tiles > 0 && (windows == nullptr || tiles_out == nullptr)) return CAMX_EINVAL;
-  static const bool fuse_enabled = [] {
-    const char *e = getenv("CAMX_TILE_FUSE");
-    return !(e != nullptr && e[0] == '0');
-  }();
-  if (fuse_enabled && n_tiles > 0 && frame_off != nullptr && max_tiles_per_frame > 0 &&
+  if (n_tiles > 0 && frame_off != nullptr && max_tiles_per_frame > 0 &&
       p.cam_count == p.n_cams) {
     TileFuse q{};
     q.wins = windows;
@@ -1088,7 +1007,7 @@ extern "C" int camx_correct_batch(const uint8_t *images, uint8_t *out, const uin
                                   const double *prev_offset, camx_band_stat *stats,
                                   uint32_t *hist, double *gain_out, double *offset_out,
                                   uint8_t *fit_ok_out, int32_t *counters, void *stream) {
-  (void)counters;  // reserved for the fused camx_band_stats_solve variant
+  (void)counters;  // reserved (ABI v1 slot; may be NULL)
   if (out == nullptr) return CAMX_EINVAL;
   int st = stats_and_solve(images, prev_frame, n_batch, n_cams, wrap, height, width, band_width,
                            t_diff, cfg, prev_gain, prev_offset, stats, hist, gain_out, offset_out,

@@ -409,11 +409,7 @@ extern "C" int camx_window_counts(const uint8_t *mask, const uint8_t *cur, const
   auto al4 = [](const void *x) { return reinterpret_cast<uintptr_t>(x) % 4 == 0; };
   auto al16 = [](const void *x) { return reinterpret_cast<uintptr_t>(x) % 16 == 0; };
   const bool quad = width % 4 == 0 && (mask ? al4(mask) : (al4(cur) && al4(prev)));
-  static const bool tile_enabled = [] {
-    const char *e = getenv("CAMX_K4_TILE");
-    return !(e != nullptr && e[0] == '0');
-  }();
-  if (tile_enabled && width % 16 == 0 && (mask ? al16(mask) : (al16(cur) && al16(prev)))) {
+  if (width % 16 == 0 && (mask ? al16(mask) : (al16(cur) && al16(prev)))) {
     const int64_t total_w = static_cast<int64_t>(n_cams) * width;
     const dim3 grid(static_cast<unsigned>((total_w + kTileW - 1) / kTileW),
                     static_cast<unsigned>((height + kTileH - 1) / kTileH));

@@ -26,7 +26,7 @@
 
 #include <cstdlib>
 
-#include "camx_solve.cuh"
+#include "camx_common.cuh"
 
 namespace camx {
 
@@ -43,42 +43,7 @@ struct StatsParams {
   int32_t H, W, bw, K, bh, t_diff;
   camx_band_stat *out;
   uint32_t *hist;        // optional
-  // fused stats + solve (camx_band_stats_solve)
-  int64_t img_begin;     // absolute image index of this launch's image 0
-  int32_t n_cams, wrap;
-  int32_t *counters;     // [S*K] arrivals, zero between launches
-  SolveParams solve;
 };
-
-// Last-arriver solve: every K1 CTA whose band feeds seam (s, k) bumps
-// counters[s*K+k] after publishing its record; the CTA that completes the
-// 2*B records of that seam block runs the K2 solve for it (whole batch) and
-// re-arms the counter.  Removes the separate K2 launch and its record
-// round trip.
-__device__ __noinline__ void fused_solve_tail(const StatsParams &p, int64_t unit_abs) {
-  __shared__ Cand cand[kSolveFrames][3];
-  __shared__ int last;
-  const int K = p.K;
-  const int k = static_cast<int>(unit_abs % K);
-  const int side = static_cast<int>((unit_abs / K) % 2);
-  const int cam = static_cast<int>((unit_abs / (2 * K)) % p.n_cams);
-  int s = -1;
-  if (side == CAMX_SIDE_LEFT)
-    s = (cam < p.n_cams - 1 || p.wrap) ? cam : -1;
-  else
-    s = cam >= 1 ? cam - 1 : (p.wrap ? p.n_cams - 1 : -1);
-  if (s < 0) return;  // edge band of a non-wrapped array: no seam
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const int old = atomicAdd(&p.counters[s * K + k], 1);
-    last = (old == 2 * p.solve.B - 1);
-    if (last) p.counters[s * K + k] = 0;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  solve_seam_block(p.solve, s, k, cand);
-}
 
 #ifndef CAMX_K1_MINB
 #define CAMX_K1_MINB 32  // one-warp CTAs: 64 registers, every warp slot of an SM usable
@@ -184,7 +149,7 @@ __device__ __forceinline__ uint32_t quad_exclusion(const StatsParams &p, const u
   return 0u;
 }
 
-template <bool HIST, int MASKMODE, int QUAD, bool FUSE>
+template <bool HIST, int MASKMODE, int QUAD>
 __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t unit,
                                            uint32_t *smem, uint64_t (*part)[13]) {
   // quads per lane per step: 6 (18 loads in flight; a default 96-row x
@@ -489,13 +454,12 @@ __device__ __forceinline__ void stats_unit(const StatsParams &p, const int64_t u
     }
     p.out[unit] = o;
   }
-  if (FUSE) fused_solve_tail(p, p.img_begin * 2 * p.K + unit);
 }
 
 // Persistent: a grid of a few CTAs per SM loops over the (image, side,
 // block) units, so the short per-unit load -> reduce phases of resident
 // CTAs overlap instead of running as many launch waves.
-template <bool HIST, int MASKMODE, int QUAD, bool FUSE>
+template <bool HIST, int MASKMODE, int QUAD>
 __global__ void __launch_bounds__(kStatsWarps * 32, CAMX_K1_MINB) band_stats_kernel(const StatsParams p) {
   extern __shared__ uint32_t smem[];
   __shared__ uint64_t part[kStatsWarps][13];
@@ -503,50 +467,42 @@ __global__ void __launch_bounds__(kStatsWarps * 32, CAMX_K1_MINB) band_stats_ker
   // griddepcontrol.wait; K3 only prefetches raw pixels before it)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
-    stats_unit<HIST, MASKMODE, QUAD, FUSE>(p, unit, smem, part);
+    stats_unit<HIST, MASKMODE, QUAD>(p, unit, smem, part);
     __syncthreads();  // `part` / counters reused by the next unit
   }
 }
 
-template <bool HIST, int MASKMODE, int QUAD, bool FUSE>
+template <bool HIST, int MASKMODE, int QUAD>
 static void launch_stats(const StatsParams &p, cudaStream_t s) {
   const int warps = kStatsWarps;
   const size_t smem = HIST ? static_cast<size_t>(warps) * kHistWords * sizeof(uint32_t) : 0;
   if (HIST) {
-    cudaFuncSetAttribute(band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>,
+    cudaFuncSetAttribute(band_stats_kernel<HIST, MASKMODE, QUAD>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   }
-  static const int env_per_sm = [] {  // experiment hook
-    const char *e = getenv("CAMX_K1_PER_SM");
-    return e != nullptr ? atoi(e) : 0;
-  }();
   // 32 CTAs per SM for the plain path (8 resident): units are scheduled
   // dynamically, ~6% faster than a one-wave persistent grid (tools/k1_probe.py)
-  const int per_sm = env_per_sm > 0 ? env_per_sm : 128 / kStatsWarps;
+  const int per_sm = 128 / kStatsWarps;
   const int64_t grid = std::min<int64_t>(p.n_units, static_cast<int64_t>(sm_count()) * per_sm);
-  band_stats_kernel<HIST, MASKMODE, QUAD, FUSE>
+  band_stats_kernel<HIST, MASKMODE, QUAD>
       <<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(p);
 }
 
 // 16-pixel groups: whole 16-byte-aligned 48-byte runs in every band row
 static bool k1_g16(const StatsParams &p) {
-  static const bool enabled = [] {
-    const char *e = getenv("CAMX_K1_G16");
-    return !(e != nullptr && e[0] == '0');
-  }();
   auto al16 = [](const void *x) { return reinterpret_cast<uintptr_t>(x) % 16 == 0; };
-  return enabled && p.bw % 16 == 0 && (3 * p.W) % 16 == 0 && (3 * (p.W - p.bw)) % 16 == 0 &&
+  return p.bw % 16 == 0 && (3 * p.W) % 16 == 0 && (3 * (p.W - p.bw)) % 16 == 0 &&
          al16(p.img) && (p.prev == nullptr || al16(p.prev)) && p.mask == nullptr;
 }
 
-template <bool HIST, int MASKMODE, bool FUSE = false>
+template <bool HIST, int MASKMODE>
 static void launch_stats_q(const StatsParams &p, bool quad, cudaStream_t s) {
   if (quad && MASKMODE != 1 && k1_g16(p))
-    launch_stats<HIST, MASKMODE, 2, FUSE>(p, s);
+    launch_stats<HIST, MASKMODE, 2>(p, s);
   else if (quad)
-    launch_stats<HIST, MASKMODE, 1, FUSE>(p, s);
+    launch_stats<HIST, MASKMODE, 1>(p, s);
   else
-    launch_stats<HIST, MASKMODE, 0, FUSE>(p, s);
+    launch_stats<HIST, MASKMODE, 0>(p, s);
 }
 
 // ---- moments --------------------------------------------------------------
@@ -663,72 +619,5 @@ extern "C" int camx_band_moments(const camx_band_stat *stats, int64_t n_records,
   band_moments_kernel<<<static_cast<unsigned>(blocks > 4096 ? 4096 : blocks), 128, 0,
                         as_stream(stream)>>>(stats, n_records, use_raw, mean_out, std_out,
                                              valid_out, area_out);
-  return launch_status();
-}
-
-extern "C" int camx_band_stats_solve(const uint8_t *images, const uint8_t *prev_images,
-                                     int32_t n_batch, int32_t n_cams, int32_t frame_begin,
-                                     int32_t frame_count, int32_t height, int32_t width,
-                                     int32_t band_width, int32_t t_diff, int32_t wrap,
-                                     const camx_solve_config *cfg, const double *prev_gain,
-                                     const double *prev_offset, camx_band_stat *stats,
-                                     uint32_t *hist, double *gain_out, double *offset_out,
-                                     uint8_t *fit_ok_out, int32_t *counters, void *stream) {
-  if (cfg == nullptr || images == nullptr || stats == nullptr || counters == nullptr ||
-      gain_out == nullptr || offset_out == nullptr)
-    return CAMX_EINVAL;
-  const int32_t blocks = cfg->blocks;
-  if (n_batch < 1 || n_cams < 2 || frame_begin < 0 || frame_count < 0 ||
-      frame_begin + frame_count > n_batch)
-    return CAMX_EINVAL;
-  if (height < 1 || width < 1 || band_width < 1 || band_width > width / 2) return CAMX_EINVAL;
-  if (blocks < 1 || blocks > height) return CAMX_EINVAL;
-  if (cfg->mode < CAMX_MODE_STANDARD || cfg->mode > CAMX_MODE_SMOOTHING) return CAMX_EINVAL;
-  if (cfg->have_prev_maps && (prev_gain == nullptr || prev_offset == nullptr)) return CAMX_EINVAL;
-  if (hist != nullptr && (reinterpret_cast<uintptr_t>(hist) % 16) != 0) return CAMX_EALIGN;
-  if (frame_count == 0) return CAMX_OK;
-  StatsParams p{};
-  p.img = images;
-  p.prev = prev_images;
-  p.H = height;
-  p.W = width;
-  p.bw = band_width;
-  p.K = blocks;
-  p.bh = height / blocks;
-  p.img_bytes = static_cast<int64_t>(height) * width * 3;
-  p.mask_bytes = static_cast<int64_t>(height) * width;
-  const int64_t first = static_cast<int64_t>(frame_begin) * n_cams;
-  p.n_units = static_cast<int64_t>(frame_count) * n_cams * 2 * blocks;
-  p.out = stats + first * 2 * blocks;
-  p.hist = hist == nullptr ? nullptr : hist + first * 2 * blocks * 768;
-  p.img_begin = first;
-  p.n_cams = n_cams;
-  p.wrap = wrap;
-  p.counters = counters;
-  p.solve.stats = stats;
-  p.solve.B = n_batch;
-  p.solve.N = n_cams;
-  p.solve.S = wrap ? n_cams : n_cams - 1;
-  p.solve.K = blocks;
-  p.solve.wrap = wrap;
-  p.solve.cfg = *cfg;
-  p.solve.prev_gain = prev_gain;
-  p.solve.prev_offset = prev_offset;
-  p.solve.gain = gain_out;
-  p.solve.offset = offset_out;
-  p.solve.fit_ok = fit_ok_out;
-  p.t_diff = t_diff;
-  cudaStream_t s = as_stream(stream);
-  auto al4 = [](const void *x) { return reinterpret_cast<uintptr_t>(x) % 4 == 0; };
-  const bool mm2 = prev_images != nullptr;
-  const bool quad = (width % 4 == 0) && (band_width % 4 == 0) && al4(images) &&
-                    (!mm2 || al4(prev_images));
-  if (hist != nullptr) {
-    if (mm2) launch_stats_q<true, 2, true>(p, quad, s);
-    else launch_stats_q<true, 0, true>(p, quad, s);
-  } else {
-    if (mm2) launch_stats_q<false, 2, true>(p, quad, s);
-    else launch_stats_q<false, 0, true>(p, quad, s);
-  }
   return launch_status();
 }

@@ -737,11 +737,7 @@ static int launch_tiles(const uint8_t *images, int32_t n_cams, int32_t height, i
     tiles_kernel<<<dim3(static_cast<unsigned>(bx), n_tiles), 256, 0, s>>>(p);
     return launch_status();
   }
-  static const bool band_enabled = [] {
-    const char *e = getenv("CAMX_TILES_BAND");
-    return !(e != nullptr && e[0] == '0');
-  }();
-  if (band_enabled && out_size < size && (width * 3) % 16 == 0 &&
+  if (out_size < size && (width * 3) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(images) % 16 == 0) {
     // segments: the window's columns cross at most one camera boundary
     const int pitch = ((size * 3 + 15) & ~15) + 64;  // two supersets + word-read slack
@@ -843,11 +839,7 @@ static int tiles_shard_launch(const uint8_t *images, int32_t n_cams, int32_t hei
   p.col_begin = col_begin;
   p.local_cols = n_cams * width;
   p.halo = halo;
-  static const bool band_enabled = [] {
-    const char *e = getenv("CAMX_TILES_BAND");
-    return !(e != nullptr && e[0] == '0');
-  }();
-  if (band_enabled && out_size < size && size <= width && (width * 3) % 16 == 0 &&
+  if (out_size < size && size <= width && (width * 3) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(images) % 16 == 0) {
     const int pitch = ((size * 3 + 15) & ~15) + 64;
     const size_t smem = ((out_size * 8 + 15) & ~15) + 2 * kBandRows * pitch +

@@ -364,8 +364,7 @@ def test_long_band_counter_flush():
     np.testing.assert_allclose(s.std, sd, rtol=1e-12)
 
 
-PATHS = {"pdl": dict(), "fused_k12": dict(fused_stats_solve=True),
-         "separate": dict(fused=False), "chunked": dict(fused=False, pipeline_chunks=2)}
+PATHS = {"pdl": dict(), "separate": dict(fused=False)}
 
 
 @pytest.mark.parametrize("mode,om", [(xp.ExposureMode.STANDARD, O.STANDARD),
@@ -913,7 +912,7 @@ def test_seam_solve_on_rank_major_records(N, world, wrap, mode):
 @pytest.mark.parametrize("use_comm", [False, True])
 @pytest.mark.parametrize("mode", [xp.ExposureMode.STANDARD, xp.ExposureMode.OBJECT_REMOVAL,
                                   xp.ExposureMode.SMOOTHING])
-def test_correct_batch_sharded_one_rank_matches_array(use_comm, mode, chunks, monkeypatch):
+def test_correct_batch_sharded_one_rank_matches_array(use_comm, mode, chunks):
     """camx_correct_batch_sharded with world = 1 (optionally through a real
     one-rank NCCL communicator: dlopen of the process's libnccl, unique id,
     comm init, all-gather; optionally in 3 chunks on the side-stream
@@ -922,7 +921,6 @@ def test_correct_batch_sharded_one_rank_matches_array(use_comm, mode, chunks, mo
     import ctypes
 
     from paper_1910_03517_b200 import _lib
-    monkeypatch.setenv("CAMX_SHARD_CHUNKS", str(chunks))
     N, H, W, B, K = 4, 96, 128, 3, 4
     frames = np.stack([O.synthetic_array(N, H, W, seed=77, objects=2, frame_index=t)
                        for t in range(2 * B)])
@@ -951,6 +949,7 @@ def test_correct_batch_sharded_one_rank_matches_array(use_comm, mode, chunks, mo
 
     comm = OneRank()
     ac = ArrayCorrector(N, H, W, cfg, mode, histograms=True, comm=comm)
+    ac.shard_chunk_count = chunks
     got = [keep(ac.correct(d[:B])), keep(ac.correct(d[B:]))]
     for g_, w_ in zip(got, want):
         np.testing.assert_array_equal(g_.out.cpu().numpy(), w_.out.cpu().numpy())

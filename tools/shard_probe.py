@@ -35,7 +35,6 @@ for world in (1, 2, 4, 8):
                 return full
 
             ac = ArrayCorrector(N, H, W, cam_begin=0, cam_count=c, exchange=exchange)
-            ac.pipeline_chunks = int(sys.argv[1]) if len(sys.argv) > 1 else 1
         for _ in range(5):
             ac.correct(frames, out)
         torch.cuda.synchronize()

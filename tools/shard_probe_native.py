@@ -21,7 +21,6 @@ _lib.call("camx_comm_init", ctypes.byref(h), uid.data_ptr(), 1, 0)
 N, H, W = 8, 1536, 2048
 for world, B, ch in [(1, 30, 1), (2, 30, 1), (2, 30, 2), (4, 30, 1), (4, 30, 2), (4, 30, 3),
                      (8, 30, 1), (8, 30, 2), (8, 30, 3), (8, 30, 5), (8, 60, 1), (8, 60, 3)]:
-    os.environ["CAMX_SHARD_CHUNKS"] = str(ch)
     if True:
         b0, c = camera_partition(N, world)[0]
 
@@ -32,6 +31,7 @@ for world, B, ch in [(1, 30, 1), (2, 30, 1), (2, 30, 2), (4, 30, 1), (4, 30, 2),
         frames = synthetic_batch(B, c, H, W, seed=1)
         out = torch.empty_like(frames)
         ac = ArrayCorrector(N, H, W, cam_begin=b0, cam_count=c, comm=Comm())
+        ac.shard_chunk_count = ch
         for _ in range(5):
             ac.correct(frames, out)
         torch.cuda.synchronize()
@@ -52,7 +52,6 @@ for world, B, ch in [(1, 30, 1), (2, 30, 1), (2, 30, 2), (4, 30, 1), (4, 30, 2),
         torch.cuda.empty_cache()
 
 print("-- pipelined (ArrayCorrector.submit: front half of batch k under K3 of batch k-1)")
-os.environ["CAMX_SHARD_CHUNKS"] = "1"
 for world, B in [(1, 30), (2, 30), (4, 30), (8, 30), (8, 60)]:
     b0, c = camera_partition(N, world)[0]
 
