@@ -503,3 +503,115 @@ def read_maps_table(text: str, band_width: int = 32) -> list[SeamMaps]:
             gain[bi, ci], off[bi, ci] = a, b
         sides.setdefault(sid, {})[side] = ExposureMap(sid, side, band_width, gain, off)
     return [SeamMaps(sides[s][Side.LEFT], sides[s][Side.RIGHT]) for s in sorted(sides)]
+
+
+# ------------------------------------------------- band statistics export
+
+_STATS_VERSION = "camarray-bandstats-v1"
+_STAT_FIELDS = ("area", "valid", "sum", "sumsq", "raw_sum", "raw_sumsq")
+
+
+def write_stats_table(stats, hist=None, camera_ids=None, frame_indices=None) -> str:
+    """Versioned text export of K1's exact band statistics (and, when given,
+    the 256-bin histograms) - the stage-1 counterpart of the maps table
+    (exposure.py:448-463 is the model: a version line, one record per line,
+    exact values).  stats: camx_band_stat records (B, N, 2, K) as the
+    structured _lib.STAT_DTYPE array or the raw (B, N, 2, K, 112) uint8
+    bytes of CorrectResult.stats; hist: uint32/int32 (B, N, 2, K, 3, 256).
+    Lines:
+      rec  frame camera side block area valid sum[3] sumsq[3] raw_sum[3] raw_sumsq[3]
+      hist frame camera side block channel <256 counts>
+    side is the reference's Side value ("left" = band at the frame's right
+    edge, exposure.py:163-168); every value is an exact integer, so the
+    table round-trips bit for bit.  BandStats' mean / std follow exactly
+    from (valid, sum, sumsq)."""
+    rec = _as_records(stats)
+    B, N, _, K = rec.shape
+    cams = list(camera_ids) if camera_ids is not None else list(range(N))
+    frames = list(frame_indices) if frame_indices is not None else list(range(B))
+    if len(cams) != N or len(frames) != B:
+        raise ValueError("camera_ids / frame_indices do not match the records")
+    h = None
+    if hist is not None:
+        h = np.asarray(hist).view(np.uint32) if np.asarray(hist).dtype == np.int32 \
+            else np.asarray(hist, dtype=np.uint32)
+        if h.shape != (B, N, 2, K, 3, 256):
+            raise ValueError(f"histograms must be {(B, N, 2, K, 3, 256)}, got {h.shape}")
+    sides = (Side.LEFT.value, Side.RIGHT.value)
+    out = [f"# {_STATS_VERSION}", f"# frames {B} cameras {N} blocks {K} histograms "
+           f"{'yes' if h is not None else 'no'}",
+           "# rec frame camera side block area valid sum[rgb] sumsq[rgb] raw_sum[rgb] "
+           "raw_sumsq[rgb]", "# hist frame camera side block channel counts[256]"]
+    for b in range(B):
+        for n in range(N):
+            for s in range(2):
+                for k in range(K):
+                    r = rec[b, n, s, k]
+                    vals = [int(r["area"]), int(r["valid"])]
+                    for f in _STAT_FIELDS[2:]:
+                        vals.extend(int(v) for v in r[f])
+                    out.append(f"rec {frames[b]} {cams[n]} {sides[s]} {k} " +
+                               " ".join(map(str, vals)))
+                    if h is not None:
+                        for c in range(3):
+                            out.append(f"hist {frames[b]} {cams[n]} {sides[s]} {k} "
+                                       f"{CHANNELS[c]} " + " ".join(map(str, h[b, n, s, k, c])))
+    return "\n".join(out) + "\n"
+
+
+def read_stats_table(text: str):
+    """Parse write_stats_table output -> (records (B, N, 2, K) _lib.STAT_DTYPE,
+    histograms uint32 (B, N, 2, K, 3, 256) or None, camera_ids,
+    frame_indices).  ValueError on a missing / unknown version line or a
+    malformed record."""
+    lines = text.strip().splitlines()
+    if not lines or lines[0] != f"# {_STATS_VERSION}":
+        raise ValueError("missing or unknown band statistics table version")
+    recs, hists = {}, {}
+    for ln in lines[1:]:
+        if not ln or ln.startswith("#"):
+            continue
+        parts = ln.split()
+        key = (int(parts[1]), int(parts[2]), Side(parts[3]), int(parts[4]))
+        if parts[0] == "rec":
+            if len(parts) != 19:
+                raise ValueError(f"malformed record line: {ln[:60]}")
+            recs[key] = [int(v) for v in parts[5:]]
+        elif parts[0] == "hist":
+            if len(parts) != 262:
+                raise ValueError(f"malformed histogram line: {ln[:60]}")
+            hists[key + (CHANNELS.index(parts[5]),)] = [int(v) for v in parts[6:]]
+        else:
+            raise ValueError(f"unknown line kind {parts[0]!r}")
+    frames = sorted({k[0] for k in recs})
+    cams = sorted({k[1] for k in recs})
+    K = max(k[3] for k in recs) + 1 if recs else 0
+    rec = np.zeros((len(frames), len(cams), 2, K), dtype=_lib.STAT_DTYPE)
+    fi = {f: i for i, f in enumerate(frames)}
+    ci = {c: i for i, c in enumerate(cams)}
+    si = {Side.LEFT: 0, Side.RIGHT: 1}
+    for (f, c, s, k), v in recs.items():
+        r = rec[fi[f], ci[c], si[s], k]
+        r["area"], r["valid"] = v[0], v[1]
+        for j, name in enumerate(_STAT_FIELDS[2:]):
+            r[name] = v[2 + 3 * j: 5 + 3 * j]
+    if len(recs) != rec.size:
+        raise ValueError("band statistics table is missing records")
+    h = None
+    if hists:
+        h = np.zeros((len(frames), len(cams), 2, K, 3, 256), dtype=np.uint32)
+        for (f, c, s, k, ch), v in hists.items():
+            h[fi[f], ci[c], si[s], k, ch] = v
+    return rec, h, cams, frames
+
+
+def _as_records(stats) -> np.ndarray:
+    a = stats
+    if hasattr(a, "detach"):  # torch tensor (device or host)
+        a = a.detach().cpu().numpy()
+    a = np.asarray(a)
+    if a.dtype == _lib.STAT_DTYPE:
+        return a
+    if a.dtype == np.uint8 and a.shape[-1] == _lib.STAT_BYTES:
+        return np.ascontiguousarray(a).view(_lib.STAT_DTYPE)[..., 0]
+    raise ValueError("stats must be camx_band_stat records (STAT_DTYPE or (..., 112) bytes)")

@@ -28,6 +28,18 @@ SCENE = load("scene")
 C1 = load("config1")
 GAIN_RTOL = 1e-12
 GAIN_ATOL = 1e-9
+# Solved-map pixel gate: north_star allows +-1 LSB; the path is designed to be
+# bit-exact (no FMA, f64 maps in numpy's operation order) and has shown 0
+# flips on every fixture, so the tests bound the FLIP COUNT, not a fraction:
+# a systematic 1-LSB drift would fail at once.
+MAX_FLIPS = 0
+
+
+def assert_pixels(got, want, max_flips=MAX_FLIPS):
+    d = np.abs(np.asarray(got).astype(np.int16) - np.asarray(want).astype(np.int16))
+    flips = int(np.count_nonzero(d))
+    assert d.max(initial=0) <= 1, f"max |diff| {d.max()} LSB"
+    assert flips <= max_flips, f"{flips} LSB flips of {d.size} (bound {max_flips})"
 
 
 def frame(px, cam=0, idx=0):
@@ -173,9 +185,9 @@ def test_array_corrector_tick_loop_golden(arr, name, mode, om):
     np.testing.assert_allclose(g, sc[f"{name}_gain"], rtol=GAIN_RTOL, atol=GAIN_ATOL)
     np.testing.assert_allclose(o, sc[f"{name}_offset"], rtol=GAIN_RTOL, atol=GAIN_ATOL)
     out = res.out.cpu().numpy()
-    diff = np.abs(out.astype(int) - sc[f"{name}_out"].astype(int))
-    assert diff.max() <= 1
-    assert (diff > 0).mean() < 1e-5
+    # reference maps come from numpy's pairwise float sums (~1e-15 off the
+    # exact integer moments), so a rare 1-LSB tie flip is allowed here only
+    assert_pixels(out, sc[f"{name}_out"], max_flips=8)
 
 
 def test_config1_golden():
@@ -389,8 +401,7 @@ def test_array_vs_oracle_synthetic(mode, om, wrap, path):
     g = np.concatenate([g1, r2.gain.cpu().numpy()])
     want_out, want_g, _, _ = O.correct_sequence(frames, None, om, ocfg, None, wrap)
     np.testing.assert_allclose(g, want_g, rtol=GAIN_RTOL, atol=GAIN_ATOL)
-    d = np.abs(out.astype(int) - want_out.astype(int))
-    assert d.max() <= 1 and (d > 0).mean() < 1e-5
+    assert_pixels(out, want_out)
 
 
 def test_apply_array_bit_exact_given_maps():
@@ -638,8 +649,7 @@ def test_random_geometry_sweep_vs_oracle(case):
     np.testing.assert_allclose(res.gain.cpu().numpy(), wg, rtol=GAIN_RTOL, atol=GAIN_ATOL)
     np.testing.assert_allclose(res.offset.cpu().numpy(), wo, rtol=GAIN_RTOL, atol=GAIN_ATOL)
     np.testing.assert_array_equal(res.fit_ok.cpu().numpy().astype(bool), wok)
-    d = np.abs(res.out.cpu().numpy().astype(int) - want.astype(int))
-    assert d.max() <= 1 and (d > 0).mean() < 1e-4
+    assert_pixels(res.out.cpu().numpy(), want)
     hist = res.hist.cpu().numpy().view(np.uint32)
     for b in range(B):
         mask = None
@@ -845,8 +855,8 @@ def test_correct_array_one_tick_with_previous_state(om):
         assert maps[s].left.seam_id == (s, s + 1)
         np.testing.assert_allclose(maps[s].left.gain, wg[s, 0], rtol=GAIN_RTOL, atol=GAIN_ATOL)
         np.testing.assert_allclose(maps[s].right.offset, wo[s, 1], rtol=GAIN_RTOL, atol=GAIN_ATOL)
-    d = np.abs(out.astype(int) - want.astype(int))
-    assert isinstance(out, np.ndarray) and d.max() <= 1 and (d > 0).mean() < 1e-4
+    assert isinstance(out, np.ndarray)
+    assert_pixels(out, want)
     for c in range(N):
         mask = O.mask_diff(cur[c], prev[c], 20) if om == O.OBJECT_REMOVAL else None
         for s, side in ((0, O.LEFT), (1, O.RIGHT)):
@@ -1062,8 +1072,7 @@ def test_full_size_config2_and_config5_vs_oracle(mode, om):
     np.testing.assert_allclose(res.offset.cpu().numpy(), wo, rtol=GAIN_RTOL, atol=GAIN_ATOL)
     np.testing.assert_array_equal(res.fit_ok.cpu().numpy().astype(bool), wok)
     out = res.out.cpu().numpy()
-    diff = np.abs(out.astype(int) - want_out.astype(int))
-    assert diff.max() <= 1 and (diff > 0).mean() < 1e-6
+    assert_pixels(out, want_out)
     hist = res.hist.cpu().numpy().view(np.uint32)  # (B, N, 2, K, 3, 256)
     from paper_1910_03517_b200 import _lib
     stats = res.stats.cpu().numpy().view(_lib.STAT_DTYPE).reshape(B, N, 2, K)
@@ -1097,8 +1106,7 @@ def test_full_size_config4_wrap_vs_oracle():
     res = ac.correct(d)
     want_out, wg, wo, _ = O.correct_sequence(frames, None, O.STANDARD, O.Cfg(), None, True)
     np.testing.assert_allclose(res.gain.cpu().numpy(), wg, rtol=GAIN_RTOL, atol=GAIN_ATOL)
-    diff = np.abs(res.out.cpu().numpy().astype(int) - want_out.astype(int))
-    assert diff.max() <= 1 and (diff > 0).mean() < 1e-6
+    assert_pixels(res.out.cpu().numpy(), want_out)
 
 
 @pytest.mark.parametrize("t_diff", [-1, 0, 20, 255])
@@ -1146,8 +1154,7 @@ def test_batch_longer_than_a_solve_chunk(mode, om):
     np.testing.assert_allclose(res.gain.cpu().numpy(), wg, rtol=GAIN_RTOL, atol=GAIN_ATOL)
     np.testing.assert_allclose(res.offset.cpu().numpy(), wo, rtol=GAIN_RTOL, atol=GAIN_ATOL)
     np.testing.assert_array_equal(res.fit_ok.cpu().numpy().astype(bool), wok)
-    d = np.abs(res.out.cpu().numpy().astype(int) - want.astype(int))
-    assert d.max() <= 1 and (d > 0).mean() < 1e-5
+    assert_pixels(res.out.cpu().numpy(), want)
 
 
 @pytest.mark.parametrize("out_size", [31, 64, 95])
@@ -1185,3 +1192,26 @@ def test_more_tiles_than_one_grid_dimension(out_size):
     for i in [0, 65534, 65535, 65536, T - 1] + [int(v) for v in rng.integers(0, T, 200)]:
         _, x, y = wins[i]
         np.testing.assert_array_equal(got[i], O.resize_bilinear(O.crop(mosaic, x, y, S), out_size))
+
+
+def test_stats_table_export_of_a_corrected_batch():
+    """K1's records + histograms of a real batch through the versioned
+    camarray-bandstats-v1 text table: exact round trip, and the reloaded
+    records still give the oracle's band moments (exposure.py:152-185)."""
+    N, H, W, B, K = 3, 96, 128, 2, 4
+    frames = np.stack([O.synthetic_array(N, H, W, seed=12, objects=2, frame_index=t)
+                       for t in range(B)])
+    ac = ArrayCorrector(N, H, W, xp.ExposureConfig(band_width=16, blocks=K), histograms=True)
+    res = ac.correct(torch.from_numpy(frames).cuda())
+    text = xp.write_stats_table(res.stats, res.hist)
+    rec, hist, cams, fr = xp.read_stats_table(text)
+    assert cams == list(range(N)) and fr == list(range(B))
+    assert rec.tobytes() == res.stats.cpu().numpy().tobytes()
+    np.testing.assert_array_equal(hist, res.hist.cpu().numpy().view(np.uint32))
+    for b in range(B):
+        for c in range(N):
+            for s, side in ((0, O.LEFT), (1, O.RIGHT)):
+                m, sd, valid, _ = O.band_stats(frames[b, c], side, 16, K)
+                r = rec[b, c, s]
+                np.testing.assert_array_equal(r["valid"], valid)
+                np.testing.assert_allclose(r["sum"] / r["valid"][:, None], m, rtol=1e-14)

@@ -250,3 +250,48 @@ class TestBandPacking:                # the drop-in's per-call band transfer
             pm = xp._bands(m.view(np.uint8), bw)
             np.testing.assert_array_equal(pm[:, :bw], m[:, :bw].view(np.uint8))
             np.testing.assert_array_equal(pm[:, -bw:], m[:, w - bw:].view(np.uint8))
+
+
+class TestStatsTable:                 # band-statistics export
+    def _records(self, B=2, N=3, K=4, seed=0):
+        from paper_1910_03517_b200 import _lib
+        rng = np.random.default_rng(seed)
+        rec = np.zeros((B, N, 2, K), dtype=_lib.STAT_DTYPE)
+        rec["area"] = rng.integers(0, 10**6, rec.shape)
+        rec["valid"] = rng.integers(0, 10**6, rec.shape)
+        for f in ("sum", "sumsq", "raw_sum", "raw_sumsq"):
+            rec[f] = rng.integers(0, 2**63, rec.shape + (3,), dtype=np.uint64) * 2 + 1
+        hist = rng.integers(0, 2**32, (B, N, 2, K, 3, 256), dtype=np.uint64).astype(np.uint32)
+        return rec, hist
+
+    def test_round_trip_exact(self):
+        rec, hist = self._records()
+        text = xp.write_stats_table(rec, hist, camera_ids=[4, 5, 6], frame_indices=[10, 11])
+        assert text.startswith("# camarray-bandstats-v1\n")
+        got, gh, cams, frames = xp.read_stats_table(text)
+        assert cams == [4, 5, 6] and frames == [10, 11]
+        assert got.tobytes() == rec.tobytes()
+        np.testing.assert_array_equal(gh, hist)
+
+    def test_raw_record_bytes_and_int32_hist(self):
+        rec, hist = self._records(B=1, N=2, K=2, seed=3)
+        raw = rec.view(np.uint8).reshape(1, 2, 2, 2, 112)  # CorrectResult.stats layout
+        text = xp.write_stats_table(raw, hist.view(np.int32))
+        got, gh, _, _ = xp.read_stats_table(text)
+        assert got.tobytes() == rec.tobytes()
+        np.testing.assert_array_equal(gh, hist)
+
+    def test_without_histograms(self):
+        rec, _ = self._records(B=1, N=1, K=3)
+        got, gh, _, _ = xp.read_stats_table(xp.write_stats_table(rec))
+        assert gh is None and got.tobytes() == rec.tobytes()
+
+    def test_version_and_shape_errors(self):
+        rec, hist = self._records(B=1, N=1, K=2)
+        with pytest.raises(ValueError):
+            xp.read_stats_table("rec 0 0 left 0 " + "1 " * 14)
+        with pytest.raises(ValueError):
+            xp.write_stats_table(rec, hist[:, :, :, :1])
+        text = xp.write_stats_table(rec).splitlines()
+        with pytest.raises(ValueError):
+            xp.read_stats_table("\n".join(text[:-1]) + "\n")  # a record missing
