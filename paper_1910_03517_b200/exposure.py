@@ -533,8 +533,10 @@ def write_stats_table(stats, hist=None, camera_ids=None, frame_indices=None) -> 
         raise ValueError("camera_ids / frame_indices do not match the records")
     h = None
     if hist is not None:
-        h = np.asarray(hist).view(np.uint32) if np.asarray(hist).dtype == np.int32 \
-            else np.asarray(hist, dtype=np.uint32)
+        if hasattr(hist, "detach"):  # torch tensor (device or host)
+            hist = hist.detach().cpu().numpy()
+        h = np.asarray(hist)
+        h = h.view(np.uint32) if h.dtype == np.int32 else h.astype(np.uint32)
         if h.shape != (B, N, 2, K, 3, 256):
             raise ValueError(f"histograms must be {(B, N, 2, K, 3, 256)}, got {h.shape}")
     sides = (Side.LEFT.value, Side.RIGHT.value)
