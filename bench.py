@@ -49,7 +49,9 @@ def parse():
                     default="standard")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-batch", type=int, default=8)
+    ap.add_argument("--e2e-batch", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=60)
+    ap.add_argument("--e2e-slots", type=int, default=4)
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     ap.add_argument("--no-hist", action="store_true",
                     help="skip the seam-band histograms (K1 means/moments only)")
@@ -320,7 +322,7 @@ class Workload:
         removal = self.mode is ExposureMode.OBJECT_REMOVAL
         if fn in ("camx_correct_batch", "camx_correct_batch_tiles"):
             # K1 (x2 for OBJECT_REMOVAL with B > 1 and no previous frame) + K2 + K3
-            # (+ tile fix-up)
+            # (+ the tile kernel)
             n = 3 if (removal and a[3] > 1 and a[2] is None) else 2
             return n + (1 if fn == "camx_correct_batch" else 2)
         if fn == "camx_correct_batch_sharded":  # K1 (x2) + K2 + K3 (+ NCCL, not ours)
@@ -377,8 +379,8 @@ class Workload:
         return self
 
     def roofline_leg(self, reps):
-        """The dominant kernel alone (K3 apply; config 5: the fused apply +
-        tile kernel and its fix-up), same buffers and maps as the last step,
+        """The dominant kernel alone (K3 apply; config 5: K3 + the tile
+        kernel, against the one-pass bytes), same buffers and maps as the last step,
         CUDA events on its stream around each launch."""
         import numpy as np
         torch = self.torch
@@ -395,7 +397,7 @@ class Workload:
             off_dev = torch.as_tensor(np.concatenate([[0], np.cumsum(per_b)]).astype(np.int32),
                                       device="cuda")
             nbytes += self.tiles_buf.numel()
-            kname = "camx apply_tma_kernel<fused tiles> + tile_fixup (K3+K5)"
+            kname = "camx apply_tma_kernel + tiles_tma_kernel (K3 then K5; one-pass bytes)"
         ev = []
         with torch.cuda.stream(stream):
             for _ in range(reps):
@@ -446,7 +448,7 @@ class Workload:
                 "cameras_per_gpu": self.count, "frame": f"{self.W}x{self.H}",
                 "step": ("K1 band stats" + (" + histograms" if self.hist else "") +
                          " + K2 seam solve + K3 apply" +
-                         (" fused with 36 attention tiles 960->416" if self.tiles else "") +
+                         (" + 36 attention tiles 960->416 from the corrected frames" if self.tiles else "") +
                          " per array-frame"),
                 "l2": "inputs larger than L2 (batch >> 126 MB)",
                 "parallelism": f"camera-shard{self.world}" if self.world > 1 else "single",
@@ -462,7 +464,7 @@ class Workload:
         self.torch.cuda.empty_cache()
 
 
-def e2e_ring(wl, Be, steps, warmup, barrier, world):
+def e2e_ring(wl, Be, steps, warmup, barrier, world, slots=4):
     """End to end through the streaming API (ring.FrameRing): frames sit in
     the ring's pinned host slots (the producer - a decoder - writes them
     there; the bench fills the R slots once, outside the timed region), and
@@ -474,7 +476,8 @@ def e2e_ring(wl, Be, steps, warmup, barrier, world):
     from paper_1910_03517_b200.ring import FrameRing
     ac = wl.ac
     ac.reset()
-    slots = 3
+    # 4 slots of 4 array-frames: the shape that saturates PCIe both ways
+    # (tools/ring_probe.py: 48.0 GB/s each way = the measured H2D || D2H ceiling)
     ring = FrameRing(ac, slots=slots, batch=Be)
     host = wl.frames[: min(wl.B, slots * Be)].cpu()
     for j in range(slots):  # the producer's writes (decode) - not timed
@@ -507,6 +510,7 @@ def e2e_ring(wl, Be, steps, warmup, barrier, world):
         ms = float(tt[0])
     ms_step = ms / steps
     px = Be * wl.n_cams * wl.H * wl.W
+    ceiling = pcie_ceiling(torch, ring)
     return {"value": round(px / 1e6 / (ms_step / 1e3), 2), "unit": "MP/s",
             "h2d_bytes_per_step": ring.h2d_bytes_per_batch * world,
             "d2h_bytes_per_step": ring.d2h_bytes_per_batch * world,
@@ -515,7 +519,32 @@ def e2e_ring(wl, Be, steps, warmup, barrier, world):
             "path": "ring.FrameRing (pinned host slots -> H2D copy stream -> K1/K2/K3 compute "
                     "stream -> D2H copy-back stream; wall clock)",
             "pcie_bytes_per_sec_each_way": round(ring.h2d_bytes_per_batch / (ms_step / 1e3) / 1e9,
-                                                 2)}
+                                                 2),
+            "pcie_ceiling_gbs_each_way": ceiling,
+            "pcie_ceiling_how": "plain H2D || D2H copies of one slot on two streams, same run"}
+
+
+def pcie_ceiling(torch, ring, reps=8):
+    """Bidirectional PCIe ceiling: a slot's pinned input -> device and a
+    device buffer -> the slot's pinned output at the same time (GB/s each)."""
+    src, dst = ring._in[0], ring._out[0]
+    a = torch.empty(src.shape, dtype=torch.uint8, device="cuda")
+    b = torch.empty_like(a)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def both():
+        with torch.cuda.stream(s1):
+            a.copy_(src, non_blocking=True)
+        with torch.cuda.stream(s2):
+            dst.copy_(b, non_blocking=True)
+    both()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        both()
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / reps
+    return round(src.numel() / sec / 1e9, 2)
 
 
 def cpu_baseline_line(wl, args):
@@ -592,8 +621,8 @@ def run_camx(args):
 
     e2e = None
     if not args.no_e2e and not wl.tiles:
-        e2e = e2e_ring(wl, min(args.e2e_batch, B), max(2, min(args.steps, 10)), args.warmup,
-                       barrier, world)
+        e2e = e2e_ring(wl, min(args.e2e_batch, B), max(2, args.e2e_steps), args.warmup,
+                       barrier, world, args.e2e_slots)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

@@ -196,6 +196,187 @@ __global__ void __launch_bounds__(kTileThreads) tiles_rows_kernel(const TilePara
   }
 }
 
+// ---- TMA-staged resize (the default resize path) ---------------------------
+// CTA = (tile, band of output rows), 4 warps; warp w resamples output rows
+// w, w + 4, ... of the band, one whole row at a time: lane l owns output
+// columns l + 32 j (j < J), whose tap byte offsets and dp2a weights sit in
+// registers for the CTA's life.  Per output row, lane 0 stages the two tap
+// source rows of the window with 1-D bulk copies (TMA engine, completion on
+// a per-slot mbarrier; kTmaTileSlots rows in flight per warp): a window row
+// spanning several cameras is one segment per camera, and the segments land
+// back to back - the first ends at its camera's row end and the next starts
+// at its camera's row start, both 16-byte aligned - so the staged row is the
+// contiguous mosaic byte range from `head` on and a tap pair straddling two
+// cameras needs no special case.  The output row is assembled in shared
+// memory and leaves with one bulk store.  Per output pixel: 6 LDS, 4 funnel
+// shifts, 6 PRMT, 6 dp2a, 6 IMAD/IMUL, 3 shifts, 3 byte STS (camx_resize.cuh
+// bilerp_fx arithmetic: bit-identical to the other tile paths).
+constexpr int kTmaTileWarps = 4;
+constexpr int kTmaTileSlots = 2;
+
+struct TmaTileGeom {
+  int pitch;         // staged source row bytes (16-multiple, with read slack)
+  int opitch;        // output row buffer bytes (16-multiple)
+  int rows_per_cta;  // output rows per CTA
+  int bulk_out;      // output rows leave by bulk store (3 * out % 16 == 0, aligned tiles)
+};
+
+__host__ __device__ __forceinline__ int tma_tile_pitch(int size) {
+  return (size * 3 + 32 + 15) & ~15;
+}
+__host__ __device__ __forceinline__ size_t tma_tile_smem(const TmaTileGeom &g) {
+  return static_cast<size_t>(kTmaTileWarps) * kTmaTileSlots * (2 * g.pitch + g.opitch);
+}
+
+template <int J>
+__global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const TileParams p,
+                                                                       const TmaTileGeom g) {
+  extern __shared__ __align__(128) uint8_t tts[];
+  __shared__ __align__(8) uint64_t full[kTmaTileWarps][kTmaTileSlots];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.y;
+  const int64_t b = p.wins[3 * t];
+  const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
+  const int out = p.out, O3 = out * 3;
+  const int64_t rowbytes = static_cast<int64_t>(p.W) * 3;
+  const int64_t img_bytes = static_cast<int64_t>(p.H) * rowbytes;
+  const int cam0 = x0 / p.W, cam1 = (x0 + p.size - 1) / p.W;
+  const int sb = (x0 - cam0 * p.W) * 3;                          // first wanted byte (cam0 row)
+  const int head = sb & 15;
+  const int eb = ((x0 + p.size - cam1 * p.W) * 3 + 15) & ~15;    // staged end (cam1 row)
+  const uint32_t n_first = static_cast<uint32_t>((cam0 == cam1 ? eb : rowbytes) - (sb - head));
+  const uint32_t row_tx = cam0 == cam1 ? n_first
+      : n_first + static_cast<uint32_t>((cam1 - cam0 - 1) * rowbytes + eb);
+  const uint8_t *frame = p.img + b * p.n_cams * img_bytes;
+  const int slot_bytes = 2 * g.pitch + g.opitch;
+  uint8_t *wbase = tts + warp * kTmaTileSlots * slot_bytes;
+
+  uint32_t off[J], wt[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int ox = lane + 32 * j;
+    int a = 0, c, w1 = 0;
+    if (ox < out) src_coord_w(ox, p.scale, p.size, a, c, w1);
+    off[j] = static_cast<uint32_t>(head + 3 * a);
+    wt[j] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
+  }
+  const int oy0 = blockIdx.x * g.rows_per_cta;
+  const int oy1 = min(out, oy0 + g.rows_per_cta);
+  const int n_rows = oy1 - oy0 > warp ? (oy1 - oy0 - warp + kTmaTileWarps - 1) / kTmaTileWarps : 0;
+  if (lane == 0) {
+    for (int s = 0; s < kTmaTileSlots; ++s) mbar_init(&full[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  auto issue = [&](int i) {  // lane 0: the two tap rows of this warp's i-th output row
+    const int oy = oy0 + warp + i * kTmaTileWarps;
+    int ya, yb, w;
+    src_coord_w(oy, p.scale, p.size, ya, yb, w);
+    uint8_t *dst = wbase + (i % kTmaTileSlots) * slot_bytes;
+    uint64_t *bar = &full[warp][i % kTmaTileSlots];
+    mbar_expect_tx(bar, 2 * row_tx);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int64_t y = y0 + (r ? yb : ya);
+      uint8_t *d = dst + r * g.pitch;
+      bulk_g2s(d, frame + cam0 * img_bytes + y * rowbytes + (sb - head), n_first, bar);
+      if (cam1 > cam0) {
+        d += n_first;
+        for (int c = cam0 + 1; c < cam1; ++c, d += rowbytes)
+          bulk_g2s(d, frame + c * img_bytes + y * rowbytes, static_cast<uint32_t>(rowbytes), bar);
+        bulk_g2s(d, frame + cam1 * img_bytes + y * rowbytes, static_cast<uint32_t>(eb), bar);
+      }
+    }
+  };
+  if (lane == 0)
+    for (int i = 0; i < min(kTmaTileSlots, n_rows); ++i) issue(i);
+
+  uint8_t *tile = p.tiles + static_cast<int64_t>(t) * out * O3;
+  for (int i = 0; i < n_rows; ++i) {
+    const int slot = i % kTmaTileSlots;
+    const int oy = oy0 + warp + i * kTmaTileWarps;
+    int ya, yb, w1y;
+    src_coord_w(oy, p.scale, p.size, ya, yb, w1y);
+    const uint32_t wy1 = static_cast<uint32_t>(w1y), wy0 = 256u - wy1;
+    const uint8_t *ra = wbase + slot * slot_bytes;
+    const uint8_t *rb = ra + g.pitch;
+    uint8_t *ob = wbase + slot * slot_bytes + 2 * g.pitch;
+    uint8_t *orow = g.bulk_out ? ob : tile + static_cast<int64_t>(oy) * O3;
+    mbar_wait(&full[warp][slot], (i / kTmaTileSlots) & 1);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int ox = lane + 32 * j;
+      if (ox < out) {
+        const uint32_t la = off[j];
+        const uint32_t sh = la * 8u;  // funnel shifts use the low 5 bits
+        const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
+        const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
+        const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
+        const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
+        uint8_t *o = orow + 3 * ox;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
+          const uint32_t v0 = __dp2a_lo(wt[j], __byte_perm(alo, ahi, sel), 0u);
+          const uint32_t v1 = __dp2a_lo(wt[j], __byte_perm(blo, bhi, sel), 0u);
+          o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+        }
+      }
+    }
+    if (g.bulk_out) {
+      fence_proxy_async_smem();  // this lane's row bytes before the bulk store reads them
+      __syncwarp();
+      if (lane == 0) {
+        bulk_s2g(tile + static_cast<int64_t>(oy) * O3, ob, static_cast<uint32_t>(O3));
+        bulk_commit();
+      }
+    }
+    __syncwarp();  // every lane is done with the slot's source rows
+    if (lane == 0) {
+      if (i + kTmaTileSlots < n_rows) issue(i + kTmaTileSlots);
+      // the next row writes the output buffer last read by row i + 1 - slots
+      if (g.bulk_out) bulk_wait_read<kTmaTileSlots - 1>();
+    }
+    __syncwarp();
+  }
+  if (g.bulk_out && lane == 0) bulk_wait<0>();
+}
+
+static int launch_tiles_tma(const TileParams &p, int32_t n_tiles, cudaStream_t s) {
+  const int J = (p.out + 31) / 32;
+  TmaTileGeom g{};
+  g.pitch = tma_tile_pitch(p.size);
+  g.opitch = (p.out * 3 + 15) & ~15;
+  g.bulk_out = ((p.out * 3) % 16 == 0 && reinterpret_cast<uintptr_t>(p.tiles) % 16 == 0) ? 1 : 0;
+  // enough CTAs for ~3 waves of 4 CTAs per SM, bands of >= 8 output rows
+  const int64_t want = static_cast<int64_t>(sm_count()) * 12;
+  int64_t per_tile = (want + n_tiles - 1) / n_tiles;
+  per_tile = std::max<int64_t>(1, std::min<int64_t>(per_tile, (p.out + 7) / 8));
+  g.rows_per_cta = static_cast<int>((p.out + per_tile - 1) / per_tile);
+  const size_t smem = tma_tile_smem(g);
+  const dim3 grid(static_cast<unsigned>((p.out + g.rows_per_cta - 1) / g.rows_per_cta),
+                  static_cast<unsigned>(n_tiles));
+  auto go = [&](auto kern) -> int {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    kern<<<grid, kTmaTileWarps * 32, smem, s>>>(p, g);
+    return launch_status();
+  };
+  if (J <= 2) return go(tiles_tma_kernel<2>);
+  if (J <= 4) return go(tiles_tma_kernel<4>);
+  if (J <= 8) return go(tiles_tma_kernel<8>);
+  if (J <= 13) return go(tiles_tma_kernel<13>);
+  return go(tiles_tma_kernel<16>);
+}
+
+static bool tiles_tma_ok(const TileParams &p) {
+  const TmaTileGeom g{tma_tile_pitch(p.size), (p.out * 3 + 15) & ~15, 1, 0};
+  return p.out <= 16 * 32 && (p.W * 3) % 16 == 0 &&
+         reinterpret_cast<uintptr_t>(p.img) % 16 == 0 && tma_tile_smem(g) <= 200 * 1024;
+}
+
 // ---- camera-sharded tiles ---------------------------------------
 // Rank g holds cameras [c0, c0 + n_cams) of the array, i.e. mosaic columns
 // [col_begin, col_begin + n_cams * W).  Output column ox of a window belongs
@@ -259,17 +440,7 @@ __device__ __forceinline__ void stage_wait() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// Band-staged downscale kernel (out < size, size <= W, 16-byte aligned
-// rows): CTA = (tile, band of kBandRows output rows).  The 2 x kBandRows
-// source rows of the band (the two taps of each output row; a strict
-// downscale never shares them) are staged once - every window row as one
-// or two camera segments copied as 16-byte-aligned supersets with one
-// barrier - and a per-column tap table (byte offset of the first tap in a
-// staged row, dp2a weights) is built once per CTA.  Each output pixel is
-// then the fused kernel's fixed-point path (3 aligned words per row, funnel
-// shift, PRMT, dp2a, IMAD; camx_resize.cuh bilerp_fx arithmetic); the band's
-// output rows are assembled in shared memory and written with 16-byte stores
-// (they are contiguous in the tile).
+// Band-staging constants and segment records (camera-shard tile kernel).
 #ifndef CAMX_TILES_BAND_ROWS
 #define CAMX_TILES_BAND_ROWS 4
 #endif
@@ -291,143 +462,6 @@ struct BandSeg {
 
 __device__ __forceinline__ int band_byte(const BandSeg &s0, const BandSeg &s1, int x) {
   return x < s0.x_end ? s0.off + s0.head + 3 * x : s1.off + s1.head + 3 * (x - s1.x_begin);
-}
-
-__global__ void __launch_bounds__(kBandThreads) tiles_band_kernel(const TileParams p, int pitch,
-                                                                   int nseg, int bands_per_cta) {
-  extern __shared__ __align__(16) uint8_t bsm[];
-  const int t = blockIdx.y;
-  const int64_t b = p.wins[3 * t];
-  const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
-  const int out = p.out;
-  const int O3 = out * 3;
-  uint2 *tap = reinterpret_cast<uint2 *>(bsm);                       // [out]
-  uint8_t *rows = bsm + ((out * 8 + 15) & ~15);                      // [2 * kBandRows][pitch]
-  uint8_t *orow = rows + 2 * kBandRows * pitch;                      // [kBandRows][O3]
-  __shared__ uint32_t wy_s[kBandRows];
-  __shared__ const uint8_t *src0_s[2 * kBandRows], *src1_s[2 * kBandRows];
-  // segments of the window's columns (CTA-uniform; <= 2 since size <= W)
-  BandSeg sg[2];
-  {
-    int x = x0, off = 0;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int cam = min(x / p.W, p.n_cams - 1);
-      const int xe = i < nseg ? min(x0 + p.size, (cam + 1) * p.W) : x;
-      sg[i].x_begin = x - x0;
-      sg[i].x_end = xe - x0;
-      sg[i].cam = cam;
-      sg[i].head = ((x - cam * p.W) * 3) & 15;
-      sg[i].nvec = xe > x ? (sg[i].head + (xe - x) * 3 + 15) >> 4 : 0;  // empty: none
-      sg[i].off = off;
-      off += sg[i].nvec * 16;
-      x = xe;
-    }
-  }
-  // per-column taps: built once, used by every band of this CTA
-  for (int ox = threadIdx.x; ox < out; ox += blockDim.x) {
-    int a, c, w1;
-    src_coord_w(ox, p.scale, p.size, a, c, w1);
-    uint32_t o = static_cast<uint32_t>(band_byte(sg[0], sg[1], a));
-    if (nseg > 1 && a < sg[0].x_end && c >= sg[0].x_end) o |= kTapStraddle;
-    tap[ox] = make_uint2(o, static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16));
-  }
-  const int64_t rowbytes = static_cast<int64_t>(p.W) * 3;
-  const int64_t img_bytes = static_cast<int64_t>(p.H) * rowbytes;
-  const uint8_t *seg0 = p.img + (b * p.n_cams + sg[0].cam) * img_bytes +
-                        (x0 + sg[0].x_begin - sg[0].cam * p.W) * 3 - sg[0].head;
-  const uint8_t *seg1 = p.img + (b * p.n_cams + sg[1].cam) * img_bytes +
-                        (x0 + sg[1].x_begin - sg[1].cam * p.W) * 3 - sg[1].head;
-  const int nv0 = sg[0].nvec, nv = nv0 + sg[1].nvec;
-  const int off1 = sg[1].off;
-  const uint32_t a1_straddle = static_cast<uint32_t>(sg[1].off + sg[1].head);
-  const int band0 = blockIdx.x * bands_per_cta;
-  for (int band = band0; band < band0 + bands_per_cta; ++band) {
-    const int oy0 = band * kBandRows;
-    if (oy0 >= out) break;  // CTA-uniform
-    const int nr = min(kBandRows, out - oy0);
-    __syncthreads();  // previous band: its rows consumed, its output rows stored
-    if (threadIdx.x < nr) {
-      int a, c, w1;
-      src_coord_w(oy0 + threadIdx.x, p.scale, p.size, a, c, w1);
-      wy_s[threadIdx.x] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
-      src0_s[2 * threadIdx.x] = seg0 + (y0 + a) * rowbytes;
-      src0_s[2 * threadIdx.x + 1] = seg0 + (y0 + c) * rowbytes;
-      src1_s[2 * threadIdx.x] = seg1 + (y0 + a) * rowbytes;
-      src1_s[2 * threadIdx.x + 1] = seg1 + (y0 + c) * rowbytes;
-    }
-    __syncthreads();
-    // stage the 2 * nr tap rows (both segments) with 16-byte loads; the
-    // (row, vector) pair advances incrementally (no division per element)
-    {
-      int r = threadIdx.x / nv, v = threadIdx.x - r * nv;
-      const int step_r = blockDim.x / nv, step_v = blockDim.x - step_r * nv;
-      while (r < 2 * nr) {
-        const bool first = v < nv0;
-        const uint4 *src = reinterpret_cast<const uint4 *>(first ? src0_s[r] : src1_s[r]) +
-                           (first ? v : v - nv0);
-        stage16(rows + r * pitch + (first ? v * 16 : off1 + (v - nv0) * 16), src);
-        r += step_r;
-        v += step_v;
-        if (v >= nv) {
-          v -= nv;
-          ++r;
-        }
-      }
-      stage_wait();
-    }
-    __syncthreads();
-    // warp-per-(row, column range): the row's weights and pointers are set
-    // once per unit, lanes stride the columns (no per-pixel index stepping)
-    {
-      constexpr int kUnitsPerRow = (kBandThreads / 32) / kBandRows > 0 ? (kBandThreads / 32) / kBandRows : 1;
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      for (int u = warp; u < nr * kUnitsPerRow; u += kBandThreads / 32) {
-        const int ol = u / kUnitsPerRow, part = u - ol * kUnitsPerRow;
-        const int c0 = part * out / kUnitsPerRow, c1 = (part + 1) * out / kUnitsPerRow;
-        const uint32_t wyp = wy_s[ol];
-        const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
-        const uint8_t *ra = rows + (2 * ol) * pitch;
-        const uint8_t *rb = ra + pitch;
-        uint8_t *orow_l = orow + ol * O3;
-        for (int ox = c0 + lane; ox < c1; ox += 32) {
-          const uint2 tv = tap[ox];
-          uint8_t *o = orow_l + 3 * ox;
-          if (!(tv.x & kTapStraddle)) {
-            const uint32_t la = tv.x;
-            const uint32_t sh = la * 8u;
-            const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
-            const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
-            const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
-            const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-              const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
-              const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
-              const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
-              o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
-            }
-          } else {  // first tap = last pixel of segment 0, second = first of segment 1
-            const uint32_t a0 = tv.x & ~kTapStraddle;
-            const uint32_t w1 = tv.y >> 16;
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch)
-              o[ch] = static_cast<uint8_t>(bilerp_fx(ra[a0 + ch], ra[a1_straddle + ch], rb[a0 + ch],
-                                                     rb[a1_straddle + ch], w1, wy1));
-          }
-        }
-      }
-    }
-    __syncthreads();
-    uint8_t *dst = p.tiles + (static_cast<int64_t>(t) * out + oy0) * O3;
-    const int nbytes = nr * O3;
-    if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (nbytes & 15) == 0) {
-      for (int v = threadIdx.x; v < nbytes / 16; v += blockDim.x)
-        reinterpret_cast<uint4 *>(dst)[v] = reinterpret_cast<const uint4 *>(orow)[v];
-    } else {
-      for (int i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = orow[i];
-    }
-  }
 }
 
 // Band-staged kernel for a camera shard (camx_tiles_shard): as
@@ -730,36 +764,13 @@ static int launch_tiles(const uint8_t *images, int32_t n_cams, int32_t height, i
     tiles_kernel<<<dim3(static_cast<unsigned>(bx), n_tiles), 256, 0, s>>>(p);
     return launch_status();
   }
+  if (tiles_tma_ok(p)) return launch_tiles_tma(p, n_tiles, s);
   if (size > width) {  // a window row spans > 2 cameras: per-pixel gather kernel
     const int64_t npx = static_cast<int64_t>(out_size) * out_size;
     int64_t bx = (npx + 255) / 256;
     if (bx > 64) bx = 64;
     tiles_kernel<<<dim3(static_cast<unsigned>(bx), n_tiles), 256, 0, s>>>(p);
     return launch_status();
-  }
-  if (out_size < size && (width * 3) % 16 == 0 &&
-      reinterpret_cast<uintptr_t>(images) % 16 == 0) {
-    // segments: the window's columns cross at most one camera boundary
-    const int pitch = ((size * 3 + 15) & ~15) + 64;  // two supersets + word-read slack
-    const int O3 = out_size * 3;
-    const size_t smem = ((out_size * 8 + 15) & ~15) + 2 * kBandRows * pitch + kBandRows * O3;
-    if (smem <= 200 * 1024) {
-      if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(tiles_band_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return static_cast<int>(e);
-      }
-      // one or two camera segments per window: decided per window on the
-      // device would diverge the staging; launch with nseg = 2 (a one-segment
-      // window gets an empty second segment)
-      // a CTA walks several bands of one tile: the tap table is built once
-      const int nbands = (out_size + kBandRows - 1) / kBandRows;
-      const int bpc = (nbands + kBandCtasPerTile - 1) / kBandCtasPerTile;
-      dim3 grid((nbands + bpc - 1) / bpc, n_tiles);
-      tiles_band_kernel<<<grid, kBandThreads, smem, s>>>(p, pitch, 2, bpc);
-      return launch_status();
-    }
   }
   const int S3p = ((size * 3 + 15) & ~15) + 64;
   const int smem = 2 * S3p + ((out_size * 3 + 15) & ~15);
