@@ -35,4 +35,53 @@ __device__ __forceinline__ uint32_t bilerp_fx(uint32_t a, uint32_t b, uint32_t c
   return (h0 * (256u - wy) + h1 * wy + 32768u) >> 16;
 }
 
+// One output row of a tile from two staged source rows (contiguous mosaic
+// bytes: `ra` = first tap row, `rb` = second), lane l producing columns
+// l + 32 j: off[j] = byte offset of the column's first tap pixel in a
+// staged row (the second tap is the next 3 bytes), wt[j] = dp2a weights
+// (256 - w1) | w1 << 16.  Per pixel: 3 aligned words per row + funnel shift
+// (the 8 bytes from the tap pair on), channel pairs by PRMT, horizontal
+// blend by dp2a, vertical by IMAD (bilerp_fx arithmetic, bit-identical).
+template <int J>
+__device__ __forceinline__ void resample_row_lanes(const uint8_t *ra, const uint8_t *rb,
+                                                   const uint32_t (&off)[J],
+                                                   const uint32_t (&wt)[J], uint32_t wy1,
+                                                   uint8_t *orow, int out, int lane) {
+  const uint32_t wy0 = 256u - wy1;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int ox = lane + 32 * j;
+    if (ox < out) {
+      const uint32_t la = off[j];
+      const uint32_t sh = la * 8u;  // funnel shifts use the low 5 bits
+      const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
+      const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
+      const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
+      const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
+      uint8_t *o = orow + 3 * ox;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
+        const uint32_t v0 = __dp2a_lo(wt[j], __byte_perm(alo, ahi, sel), 0u);
+        const uint32_t v1 = __dp2a_lo(wt[j], __byte_perm(blo, bhi, sel), 0u);
+        o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
+      }
+    }
+  }
+}
+
+// Per-lane column taps of resample_row_lanes (lane l: columns l + 32 j).
+template <int J>
+__device__ __forceinline__ void lane_taps(int lane, int out, float scale, int size, int head,
+                                          uint32_t (&off)[J], uint32_t (&wt)[J]) {
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int ox = lane + 32 * j;
+    int a = 0, c, w1 = 0;
+    if (ox < out) src_coord_w(ox, scale, size, a, c, w1);
+    off[j] = static_cast<uint32_t>(head + 3 * a);
+    wt[j] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
+  }
+}
+
 }  // namespace camx

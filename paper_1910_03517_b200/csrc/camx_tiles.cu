@@ -252,14 +252,7 @@ __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const Til
   uint8_t *wbase = tts + warp * kTmaTileSlots * slot_bytes;
 
   uint32_t off[J], wt[J];
-#pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const int ox = lane + 32 * j;
-    int a = 0, c, w1 = 0;
-    if (ox < out) src_coord_w(ox, p.scale, p.size, a, c, w1);
-    off[j] = static_cast<uint32_t>(head + 3 * a);
-    wt[j] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
-  }
+  lane_taps<J>(lane, out, p.scale, p.size, head, off, wt);
   const int oy0 = blockIdx.x * g.rows_per_cta;
   const int oy1 = min(out, oy0 + g.rows_per_cta);
   const int n_rows = oy1 - oy0 > warp ? (oy1 - oy0 - warp + kTmaTileWarps - 1) / kTmaTileWarps : 0;
@@ -298,32 +291,11 @@ __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const Til
     const int oy = oy0 + warp + i * kTmaTileWarps;
     int ya, yb, w1y;
     src_coord_w(oy, p.scale, p.size, ya, yb, w1y);
-    const uint32_t wy1 = static_cast<uint32_t>(w1y), wy0 = 256u - wy1;
     const uint8_t *ra = wbase + slot * slot_bytes;
-    const uint8_t *rb = ra + g.pitch;
     uint8_t *ob = wbase + slot * slot_bytes + 2 * g.pitch;
     uint8_t *orow = g.bulk_out ? ob : tile + static_cast<int64_t>(oy) * O3;
     mbar_wait(&full[warp][slot], (i / kTmaTileSlots) & 1);
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int ox = lane + 32 * j;
-      if (ox < out) {
-        const uint32_t la = off[j];
-        const uint32_t sh = la * 8u;  // funnel shifts use the low 5 bits
-        const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
-        const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
-        const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
-        const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
-        uint8_t *o = orow + 3 * ox;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
-          const uint32_t v0 = __dp2a_lo(wt[j], __byte_perm(alo, ahi, sel), 0u);
-          const uint32_t v1 = __dp2a_lo(wt[j], __byte_perm(blo, bhi, sel), 0u);
-          o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
-        }
-      }
-    }
+    resample_row_lanes<J>(ra, ra + g.pitch, off, wt, static_cast<uint32_t>(w1y), orow, out, lane);
     if (g.bulk_out) {
       fence_proxy_async_smem();  // this lane's row bytes before the bulk store reads them
       __syncwarp();
