@@ -33,6 +33,9 @@ WORKLOADS = {
     "config3": (8, 1536, 2048, 30, "8-camera 25 MP array sharded one camera group per GPU"),
     "config4": (14, 2160, 3840, 64, "14-camera 360-degree 4K array (wrap seam), 64-frame batches"),
     "config5": (8, 1536, 2048, 30, "config 2 + 36 attention tiles/array-frame, 960 -> 416x416"),
+    "config5m": (8, 1536, 2048, 30, "config 2 + motion counts fused into the apply pass + "
+                 "attention tick (Scheduler, budget 4) + 960 -> 416x416 tiles of the chosen "
+                 "windows"),
 }
 FALLBACK_HBM_GBS = 6650.0
 
@@ -295,11 +298,19 @@ class Workload:
         self.out = torch.empty_like(self.frames)
         self.stream = torch.cuda.Stream()
         self.tiles = name == "config5"
+        self.attend = name == "config5m"
+        if self.attend:
+            from paper_1910_03517_b200.array import AttendPipeline
+            from paper_1910_03517_b200.attention import Scheduler
+            self.scheduler = Scheduler((n_cams * W, H))
+            self.pipe = AttendPipeline(self.ac, self.scheduler)
+            self.frame_index = 0
+            self.tiles_attended = 0
         self.tiles_buf = None
         if self.tiles:
             n_tiles = len(self.ac.tile_windows(960)) * B
             self.tiles_buf = torch.empty((n_tiles, 416, 416, 3), dtype=torch.uint8, device="cuda")
-        self.use_graph = not args.no_graph and world == 1 and not self.tiles
+        self.use_graph = not args.no_graph and world == 1 and not self.tiles and not self.attend
         # N > 1 over NCCL: the front half (K1 -> all-gather -> K2) of batch k on
         # a side stream under K3 of batch k-1 (ArrayCorrector.submit)
         self.use_pipe = (world > 1 and getattr(self.ac, "comm", None) is not None
@@ -307,6 +318,17 @@ class Workload:
 
     def step(self):
         ac = self.ac
+        if self.attend:
+            # batch k: K1 -> K2 -> K3 + motion counts, counts D2H (async); batch
+            # k-1: Scheduler per array-frame on the host under k's kernels,
+            # then its tiles (AttendPipeline)
+            r = self.pipe.submit(self.frames, frame_index=self.frame_index, stream=self.stream)
+            self.frame_index += self.B
+            if r is None:
+                return None
+            self.tiles_attended += r.tiles.shape[0]
+            self.frames_attended = r.frame_index + self.B
+            return r.result
         if self.tiles:
             return ac.correct_and_tile(self.frames, out=self.out, tiles=self.tiles_buf,
                                        stream=self.stream)[0]
@@ -320,6 +342,10 @@ class Workload:
         """Our kernels behind one _lib.call (camx entry points launch several)."""
         from paper_1910_03517_b200.exposure import ExposureMode
         removal = self.mode is ExposureMode.OBJECT_REMOVAL
+        if fn == "camx_correct_batch_motion":  # K1 (x2 as above) + K2 + K3 with motion counts
+            return 4 if (removal and a[3] > 1 and a[2] is None) else 3
+        if fn == "camx_tiles":
+            return 1
         if fn in ("camx_correct_batch", "camx_correct_batch_tiles"):
             # K1 (x2 for OBJECT_REMOVAL with B > 1 and no previous frame) + K2 + K3
             # (+ the tile kernel)
@@ -365,6 +391,10 @@ class Workload:
                 barrier()
         finally:
             _lib.call = orig_call
+        if self.attend:  # the last batch's ticks and tiles (outside the timed region)
+            with torch.cuda.stream(self.stream):
+                self.pipe.flush(stream=self.stream)
+            torch.cuda.synchronize()
         if self.use_pipe:  # drain the pipeline (outside the timed region)
             with torch.cuda.stream(self.stream):
                 res = self.ac.flush(stream=self.stream) or res
@@ -398,13 +428,22 @@ class Workload:
                                       device="cuda")
             nbytes += self.tiles_buf.numel()
             kname = "camx apply_tma_kernel + tiles_tma_kernel (K3 then K5; one-pass bytes)"
+        if self.attend:
+            # K1 + K2 + K3 with the in-pass motion counts: apply (6 B/px) + the
+            # previous frame (3 B/px) + the seam bands K1 reads
+            bands = 2 * (self.n_cams - 1) * cfg.band_width * H * 3
+            nbytes = B * (9 * self.n_cams * H * W + bands)
+            kname = "camx K1 + K2 + apply_tma_kernel<motion> (camx_correct_batch_motion)"
+            motion_call = self.motion_call()
         ev = []
         with torch.cuda.stream(stream):
             for _ in range(reps):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                if self.tiles:
+                if self.attend:
+                    motion_call()
+                elif self.tiles:
                     _lib.call("camx_correct_and_tile", self.frames.data_ptr(), self.out.data_ptr(),
                               B, self.n_cams, int(self.wrap), H, W, cfg.blocks,
                               res.gain.data_ptr(), res.offset.data_ptr(), w_dev.data_ptr(),
@@ -422,6 +461,30 @@ class Workload:
         self.k_bytes = nbytes
         self.k_name = kname
         self.k_reps = len(ev)
+
+    def motion_call(self):
+        """camx_correct_batch_motion on this workload's buffers (roofline leg):
+        fresh maps, frame 0's previous frame = the batch's last frame."""
+        import ctypes
+        from paper_1910_03517_b200 import _lib
+        from paper_1910_03517_b200.array import _MODE_CODE
+        torch, ac, cfg, B = self.torch, self.ac, self.cfg, self.B
+        buf = ac._buffers(B)
+        counts = torch.empty((B, len(ac.tile_windows(960))), dtype=torch.int64, device="cuda")
+        sc = _lib.SolveConfig(_MODE_CODE[ac.mode], ac.K, int(cfg.min_band_pixels),
+                              float(cfg.sigma_min), float(cfg.alpha),
+                              float(cfg.min_valid_fraction), 0, 0)
+        prev = self.frames[B - 1]
+        self._keep = (counts, sc)
+
+        def call():
+            _lib.call("camx_correct_batch_motion", self.frames.data_ptr(), self.out.data_ptr(),
+                      None, B, self.n_cams, int(self.wrap), self.H, self.W, cfg.band_width,
+                      cfg.t_diff, ctypes.byref(sc), None, None, buf["stats"].data_ptr(),
+                      None if buf["hist"] is None else buf["hist"].data_ptr(),
+                      buf["gain"].data_ptr(), buf["offset"].data_ptr(), buf["fit_ok"].data_ptr(),
+                      prev.data_ptr(), 960, 20, counts.data_ptr(), self.stream.cuda_stream)
+        return call
 
     def summary(self, peak, peak_kind):
         """Throughput + roofline fields (after max-over-ranks timing)."""
@@ -444,11 +507,18 @@ class Workload:
     def config(self):
         return {"workload": f"{self.name}: {self.desc}", "batch": self.B,
                 "mode": self.mode.value, "histograms": self.hist, "wrap": self.wrap,
-                "tiles_per_step": (self.tiles_buf.shape[0] if self.tiles else 0),
+                "tiles_per_step": (self.tiles_buf.shape[0] if self.tiles else
+                                   round(self.tiles_attended /
+                                         max(1, getattr(self, "frames_attended", 0)) * self.B, 2)
+                                   if self.attend else 0),
                 "cameras_per_gpu": self.count, "frame": f"{self.W}x{self.H}",
                 "step": ("K1 band stats" + (" + histograms" if self.hist else "") +
                          " + K2 seam solve + K3 apply" +
                          (" + 36 attention tiles 960->416 from the corrected frames" if self.tiles else "") +
+                         (" with the motion counts of the 36 tiling windows in the same pass, "
+                          "counts D2H; the previous batch's attention.Scheduler ticks (budget 4) "
+                          "on the host under it, then its chosen windows 960->416 "
+                          "(array.AttendPipeline)" if self.attend else "") +
                          " per array-frame"),
                 "l2": "inputs larger than L2 (batch >> 126 MB)",
                 "parallelism": f"camera-shard{self.world}" if self.world > 1 else "single",
@@ -458,7 +528,7 @@ class Workload:
                            "eager (PDL-chained)")}
 
     def free(self):
-        for k in ("frames", "out", "tiles_buf", "res", "ac"):
+        for k in ("frames", "out", "tiles_buf", "res", "ac", "_keep"):
             if hasattr(self, k):
                 delattr(self, k)
         self.torch.cuda.empty_cache()
@@ -638,7 +708,7 @@ def run_camx(args):
     # rooflined the same way (same steps / warm-up, own clocks)
     secondary = []
     if world == 1 and args.workload is None and not args.no_secondary:
-        for nm in ("config4", "config5"):
+        for nm in ("config4", "config5", "config5m"):
             w2 = Workload(nm, WORKLOADS[nm][3], args, world, rank, torch).run(
                 args.steps, args.warmup, barrier)
             w2.roofline_leg(max(3, min(args.steps, 20)))

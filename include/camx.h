@@ -180,6 +180,35 @@ int camx_correct_batch(const uint8_t *images, uint8_t *out,
                        uint32_t *hist, double *gain_out, double *offset_out,
                        uint8_t *fit_ok_out, int32_t *counters, void *stream);
 
+/* camx_correct_batch with the motion counts of the attention tick fused
+ * into K3 (replaces difference_plan's per-window count_nonzero of
+ * mask_diff, attention.py:89-103 / core.py:191-196, for every array-frame):
+ * K3 also reads the previous raw array-frame (frame b - 1 of the batch;
+ * `motion_prev` (n_cams images, may be NULL: no counts for frame 0) before
+ * frame 0) and counts, per window of the overlap-0 tiling of the
+ * (n_cams * width) x height mosaic with side win_size (row-major, nx * ny
+ * windows: camx_tiling_size), the pixels with max_c |cur - prev| > t_motion
+ * (0..255).  counts_out [n_batch][ny][nx] int64 (zeroed here).  Needs
+ * width * 3 % 16 == 0 (else CAMX_EINVAL: use camx_correct_batch +
+ * camx_window_counts). */
+int camx_correct_batch_motion(
+    const uint8_t *images, uint8_t *out, const uint8_t *prev_frame,
+    int32_t n_batch, int32_t n_cams, int32_t wrap, int32_t height,
+    int32_t width, int32_t band_width, int32_t t_diff,
+    const camx_solve_config *cfg, const double *prev_gain,
+    const double *prev_offset, camx_band_stat *stats, uint32_t *hist,
+    double *gain_out, double *offset_out, uint8_t *fit_ok_out,
+    const uint8_t *motion_prev, int32_t win_size, int32_t t_motion,
+    int64_t *counts_out, void *stream);
+/* 1 when camx_correct_batch_motion can run this geometry (16-byte aligned
+ * rows; every K3 CTA meets <= 3 x 3 windows, e.g. size >= ~700 px at
+ * 2048-px frames), else 0 (count with camx_window_counts instead). */
+int camx_motion_supported(int32_t n_batch, int32_t n_cams, int32_t height,
+                          int32_t width, int32_t blocks, int32_t size);
+/* Window grid of the overlap-0 tiling (attention.py:53-86): nx, ny. */
+int camx_tiling_size(int32_t mosaic_w, int32_t mosaic_h, int32_t size,
+                     int32_t *nx, int32_t *ny);
+
 /* ---- camera-sharded arrays (multi-GPU) ------------------------
  * One process per GPU; rank g owns the contiguous camera group
  * [begin(g), begin(g) + count(g)) of dist.camera_partition (counts differ by

@@ -93,6 +93,7 @@ class ArrayCorrector:
         self._bufs: dict = {}
         self._prev_maps = None     # (gain, offset) device [S][2][K][3]
         self._prev_frame = None    # device (N, H, W, 3), OBJECT_REMOVAL only
+        self._motion_prev = None   # device (N, H, W, 3): last frame of correct_with_motion
         self._ring = None
 
     # ------------------------------------------------------------ state
@@ -101,6 +102,7 @@ class ArrayCorrector:
         Captured CUDA graphs baked "has previous maps" in: drop them."""
         self._prev_maps = None
         self._prev_frame = None
+        self._motion_prev = None
         self._graphs = {}
 
     def set_prev_maps(self, maps: list[SeamMaps]) -> None:
@@ -570,6 +572,115 @@ class ArrayCorrector:
                           _dev.stream_handle(stream))
         return res, tiles
 
+    # ------------------------------------------------------------ attention
+    def correct_with_motion(self, frames, out=None, *, size: int = 960, t_motion: int = 20,
+                            stream=None):
+        """Correct a batch and, in the same pass over the pixels (K4 fused
+        into K3: camx_correct_batch_motion), count per array-frame the
+        motion-mask on-pixels of every window of the overlap-0 tiling - the
+        counts of difference_plan(mask_diff(prev, cur, t_motion), size)
+        (attention.py:89-103, core.py:191-196).  The previous array-frame
+        of frame 0 is the last frame of the previous call (none after
+        reset(): frame 0 then has no counts).
+
+        Returns (CorrectResult, counts int64 CUDA tensor (B, n_windows) in
+        window_origins order, has_counts list[bool] per frame)."""
+        t = _dev.require_cuda()
+        if self.cam_count != self.n_cams or self.S == 0:
+            raise ValueError("motion counts need the whole array (two or more cameras) on one GPU")
+        if not 0 <= int(t_motion) <= 255:
+            raise ValueError("t_motion must be in 0..255")
+        if frames.dim() == 4:
+            frames = frames[None]
+        B, N, H, W, C = frames.shape
+        if (N, H, W, C) != (self.n_cams, self.height, self.width, 3) or frames.dtype != t.uint8:
+            raise ValueError(f"frames must be (B, {self.n_cams}, {self.height}, {self.width}, 3) "
+                             "uint8")
+        if not frames.is_cuda or not frames.is_contiguous():
+            raise ValueError("frames must be a contiguous CUDA tensor")
+        s = min(int(size), N * W, H)
+        origins = self.tile_windows(s)
+        if out is None:
+            out = t.empty_like(frames)
+        elif out.shape != frames.shape or not out.is_contiguous():
+            raise ValueError("out must match frames")
+        buf = self._buffers(B)
+        main = stream if stream is not None else t.cuda.current_stream()
+        sh = _dev.stream_handle(main)
+        counts = t.empty((B, len(origins)), dtype=t.int64, device="cuda")
+        cfg = self.cfg
+        removal = self.mode is ExposureMode.OBJECT_REMOVAL
+        pf = self._prev_frame
+        have_prev = self._prev_maps is not None
+        sc = _lib.SolveConfig(_MODE_CODE[self.mode], self.K, int(cfg.min_band_pixels),
+                              float(cfg.sigma_min), float(cfg.alpha),
+                              float(cfg.min_valid_fraction), int(have_prev),
+                              int(removal and pf is not None))
+        pg, po = self._prev_maps if have_prev else (None, None)
+        mp = self._motion_prev
+        self.last_motion_fused = bool(_lib.load().camx_motion_supported(
+            B, self.n_cams, H, W, self.K, s))
+        if self.last_motion_fused:
+            _lib.call("camx_correct_batch_motion", frames.data_ptr(), out.data_ptr(),
+                      _dev.ptr(pf) if removal else None, B, self.n_cams, int(self.wrap), H, W,
+                      cfg.band_width, cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),
+                      buf["stats"].data_ptr(), _dev.ptr(buf["hist"]), buf["gain"].data_ptr(),
+                      buf["offset"].data_ptr(), buf["fit_ok"].data_ptr(), _dev.ptr(mp), s,
+                      int(t_motion), counts.data_ptr(), sh)
+            res = self._finish(frames, out, buf, main, removal)
+        else:  # geometry outside the fused kernel: correct, then K4 per frame
+            res = self.correct(frames, out, stream=stream)
+            org = _dev.to_device(np.asarray(origins, dtype=np.int32).reshape(-1, 2))
+            counts.zero_()
+            for b in range(B):
+                prev = frames[b - 1] if b > 0 else mp
+                if prev is None:
+                    continue
+                _lib.call("camx_window_counts", None, frames[b].data_ptr(), prev.data_ptr(),
+                          int(t_motion), N, H, W, org.data_ptr(), len(origins), s,
+                          counts[b].data_ptr(), sh)
+        has = [mp is not None] + [True] * (B - 1)
+        with t.cuda.stream(main):
+            if self._motion_prev is None:
+                self._motion_prev = t.empty_like(frames[0])
+            self._motion_prev.copy_(frames[B - 1], non_blocking=True)
+        return res, counts, has
+
+    def correct_and_attend(self, frames, scheduler, *, objects=(), frame_index: int = 0,
+                           out_size: int = 416, t_motion: int = 20, out=None, stream=None):
+        """One attention tick per array-frame (the paper's detector loop,
+        attention.py:149-186): correct the batch with the fused motion counts
+        (correct_with_motion), run `scheduler` (attention.Scheduler) on every
+        frame in order - startup sweep, expectation windows of `objects`,
+        then the difference windows ranked from the device counts, merged,
+        cut to the budget - and resample the chosen windows of the corrected
+        frames to out_size tiles (camx_tiles).
+
+        Returns (CorrectResult, requests: list per frame of AttentionRequest,
+        tiles uint8 (T, out_size, out_size, 3) in request order, counts)."""
+        t = _dev.require_cuda()
+        if tuple(scheduler.mosaic_size) != (self.n_cams * self.width, self.height):
+            raise ValueError("scheduler mosaic does not match the array")
+        size = scheduler.window_size
+        res, counts, has = self.correct_with_motion(frames, out, size=size, t_motion=t_motion,
+                                                    stream=stream)
+        host = _dev.to_host(counts)  # one D2H of B x n_windows int64 (synchronises)
+        requests, wins = [], []
+        for b in range(host.shape[0]):
+            fn = (lambda org, s, c=host[b]: c) if has[b] else None
+            reqs = scheduler.schedule(frame_index=frame_index + b, objects=objects,
+                                      window_counts_fn=fn)
+            requests.append(reqs)
+            wins += [(b, r.window.x, r.window.y) for r in reqs]
+        tiles = t.empty((len(wins), out_size, out_size, 3), dtype=t.uint8, device="cuda")
+        if wins:
+            wd = _dev.to_device(np.asarray(wins, dtype=np.int32).reshape(-1, 3))
+            _lib.call("camx_tiles", res.out.data_ptr(), self.n_cams, self.height, self.width,
+                      wd.data_ptr(), len(wins), int(size), int(out_size), tiles.data_ptr(),
+                      _dev.stream_handle(stream))
+            self._attend_wins = wd  # alive until the next call (the launch is async)
+        return res, requests, tiles, counts
+
     # ------------------------------------------------------------ results
     def maps(self, result: CorrectResult, b: int = -1, camera_ids=None) -> list[SeamMaps]:
         """Host SeamMaps of array-frame b (seam s = cameras (s, s+1 mod N))."""
@@ -664,6 +775,117 @@ class ArrayCorrector:
                     comp_done=[t.cuda.Event() for _ in range(slots)])
         self._ring = ring
         return ring
+
+
+@dataclass
+class AttendResult:
+    """One batch through the attention tick (AttendPipeline)."""
+
+    result: CorrectResult   # corrected frames and maps
+    requests: list          # per array-frame: the Scheduler's AttentionRequests
+    tiles: object           # uint8 (T, out, out, 3) CUDA tensor, request order
+    counts: np.ndarray      # int64 (B, n_windows) motion counts (host)
+    frame_index: int        # of the batch's first array-frame
+
+
+class AttendPipeline:
+    """The attention tick as a stream (the paper's detector loop: maps and
+    pixels on the GPU, the per-tick decision on the host, in parallel).
+
+    submit(batch k) launches k's correction with the fused motion counts
+    (ArrayCorrector.correct_with_motion) and an async copy of the counts to
+    pinned host memory, then finishes batch k-1: waits for its counts (its
+    kernels ran before k's), runs `scheduler` on each of its array-frames on
+    the host while the GPU corrects batch k, and launches k-1's tiles behind
+    k (camx_tiles on k-1's corrected frames).  It returns k-1's
+    AttendResult (None for the first batch); flush() returns the last one.
+    A result's buffers (frames, maps) are reused two submits later."""
+
+    def __init__(self, corrector, scheduler, *, out_size: int = 416, t_motion: int = 20):
+        if tuple(scheduler.mosaic_size) != (corrector.n_cams * corrector.width, corrector.height):
+            raise ValueError("scheduler mosaic does not match the array")
+        self.ac, self.scheduler = corrector, scheduler
+        self.out_size, self.t_motion = int(out_size), int(t_motion)
+        self._slots: dict = {}
+        self._k = 0
+        self._pending = None
+
+    def _slot(self, B: int, i: int):
+        key = (B, i)
+        sl = self._slots.get(key)
+        if sl is None:
+            t = _dev.require_cuda()
+            ac = self.ac
+            n_win = len(ac.tile_windows(self.scheduler.window_size))
+            shape = (B, ac.n_cams, ac.height, ac.width, 3)
+            mshape = (B, max(ac.S, 1), 2, ac.K, 3)
+            sl = dict(out=t.empty(shape, dtype=t.uint8, device="cuda"),
+                      gain=t.empty(mshape, dtype=t.float64, device="cuda"),
+                      offset=t.empty(mshape, dtype=t.float64, device="cuda"),
+                      fit_ok=t.empty((B, max(ac.S, 1), ac.K), dtype=t.uint8, device="cuda"),
+                      stats=t.empty((B, ac.n_cams, 2, ac.K, _lib.STAT_BYTES), dtype=t.uint8,
+                                    device="cuda"),
+                      hist=(t.empty((B, ac.n_cams, 2, ac.K, 3, 256), dtype=t.int32,
+                                    device="cuda") if ac.histograms else None),
+                      counts=t.empty((B, n_win), dtype=t.int64, pin_memory=True),
+                      event=t.cuda.Event())
+            self._slots[key] = sl
+        return sl
+
+    def submit(self, frames, *, frame_index: int, objects=(), stream=None):
+        t = _dev.require_cuda()
+        main = stream if stream is not None else t.cuda.current_stream()
+        if frames.dim() == 4:
+            frames = frames[None]
+        B = frames.shape[0]
+        sl = self._slot(B, self._k % 2)
+        res, counts, has = self.ac.correct_with_motion(
+            frames, sl["out"], size=self.scheduler.window_size, t_motion=self.t_motion,
+            stream=main)
+        S = self.ac.S
+        with t.cuda.stream(main):
+            sl["gain"][:, :S].copy_(res.gain, non_blocking=True)
+            sl["offset"][:, :S].copy_(res.offset, non_blocking=True)
+            sl["fit_ok"][:, :S].copy_(res.fit_ok, non_blocking=True)
+            sl["stats"].copy_(res.stats, non_blocking=True)
+            if sl["hist"] is not None:
+                sl["hist"].copy_(res.hist, non_blocking=True)
+            sl["counts"].copy_(counts, non_blocking=True)
+            sl["event"].record(main)
+        prev, self._pending = self._pending, (sl, B, int(frame_index), tuple(objects), has)
+        self._k += 1
+        return self._finish(prev, main) if prev is not None else None
+
+    def flush(self, stream=None):
+        t = _dev.require_cuda()
+        main = stream if stream is not None else t.cuda.current_stream()
+        prev, self._pending = self._pending, None
+        return self._finish(prev, main) if prev is not None else None
+
+    def _finish(self, pend, main) -> AttendResult:
+        t = _dev.torch()
+        sl, B, f0, objects, has = pend
+        sl["event"].synchronize()
+        host = sl["counts"].numpy().copy()
+        ac, sched = self.ac, self.scheduler
+        requests, wins = [], []
+        for b in range(B):
+            fn = (lambda org, s, c=host[b]: c) if has[b] else None
+            reqs = sched.schedule(frame_index=f0 + b, objects=objects, window_counts_fn=fn)
+            requests.append(reqs)
+            wins += [(b, r.window.x, r.window.y) for r in reqs]
+        tiles = t.empty((len(wins), self.out_size, self.out_size, 3), dtype=t.uint8,
+                        device="cuda")
+        if wins:
+            wd = _dev.to_device(np.asarray(wins, dtype=np.int32).reshape(-1, 3))
+            sl["wins"] = wd  # alive until the slot's next use (the launch is async)
+            _lib.call("camx_tiles", sl["out"].data_ptr(), ac.n_cams, ac.height, ac.width,
+                      wd.data_ptr(), len(wins), int(sched.window_size), self.out_size,
+                      tiles.data_ptr(), _dev.stream_handle(main))
+        S = ac.S
+        res = CorrectResult(sl["out"], sl["gain"][:, :S], sl["offset"][:, :S],
+                            sl["fit_ok"][:, :S], sl["stats"], sl["hist"])
+        return AttendResult(res, requests, tiles, host, f0)
 
 
 def correct_array(frames, cfg: ExposureConfig = ExposureConfig(), prev_maps=None,

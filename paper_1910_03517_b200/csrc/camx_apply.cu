@@ -20,6 +20,7 @@
 //   fma(., 256, 2^23)      = 2^23 + rint_half_even(clip(y, 0, 256))
 //   min(., 255) on the 16-bit lanes (VIMNMX.U16x2), then byte pack.
 // Since clamp bounds are integers, clip(rint(y)) == rint(clip(y)).
+#include <algorithm>
 #include <cstdlib>
 
 #include "camx_resize.cuh"
@@ -41,6 +42,13 @@ struct ApplyParams {
   // fast kernel decomposition
   int32_t chunks_per_row, col_groups, row_splits, rows_per_split;
   int32_t pdl;  // launched as a programmatic dependent of the stats/solve kernel
+  // motion counts (K3 with the in-pass K4, apply_tma_kernel<..., MOTION>):
+  // previous raw images of array-frame 0 (frames b >= 1 use frame b - 1 of
+  // the batch; NULL: no counts for frame 0), per-frame window counts of the
+  // overlap-0 tiling of the mosaic (attention.py:66-103), mask_diff threshold
+  const uint8_t *prev_first;
+  unsigned long long *counts;  // [B][ny][nx]
+  int32_t win, nx, ny, nx_reg, ny_reg, mosaic_w, t_motion;
 };
 
 // Map pointers (LEFT role = seam at the right edge, RIGHT role = seam at the
@@ -181,10 +189,37 @@ constexpr int kTmaRows = 2;  // rows per stage
 
 // MINB: CTAs per SM the register budget is sized for (0: CAMX_K3_MINB);
 // short-CTA launches use a leaner variant.
-template <int ROWS, int STAGES, int MINB = 0>
+// MOTION: the in-pass K4 (attention.py:89-103 counts of mask_diff,
+// core.py:191-196): every stage also stages the previous raw frame's rows
+// (and 16 bytes past the column group, for the pixel straddling the next
+// group) and counts, per window of the overlap-0 tiling that meets the CTA,
+// the pixels with max_c |cur - prev| > t_motion.  Per 4 bytes: VABSDIFF4,
+// a 3-op SWAR "> t" into the byte MSBs, and one IMAD gathering the 4 MSBs
+// into a nibble; a thread's 16 bytes + the next 2 (from the next chunk in
+// the ring) give an 18-bit flag mask E, and a pixel is on iff any of its 3
+// bytes is: E | E >> 1 | E >> 2 at the thread's pixel starts.
+struct MotionThr {
+  uint32_t k7;  // (127 - t') * 0x01010101, t' = t mod 128
+  bool hi;      // t >= 128
+};
+__device__ __forceinline__ uint32_t gt_nibble(uint32_t cur, uint32_t prev, const MotionThr &m) {
+  const uint32_t d = __vabsdiffu4(cur, prev);
+  const uint32_t s = (d & 0x7F7F7F7Fu) + m.k7;  // bit 7 of a byte: low7(d) > t'
+  const uint32_t f = (m.hi ? (s & d) : (s | d)) & 0x80808080u;
+  return (f * 0x00204081u) >> 28;  // byte MSBs 7, 15, 23, 31 -> bits 0..3
+}
+__device__ __forceinline__ uint32_t flags16(uint4 c, uint4 q, const MotionThr &m) {
+  return gt_nibble(c.x, q.x, m) | (gt_nibble(c.y, q.y, m) << 4) |
+         (gt_nibble(c.z, q.z, m) << 8) | (gt_nibble(c.w, q.w, m) << 12);
+}
+
+template <int ROWS, int STAGES, int MINB = 0, bool MOTION = false>
 __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
     apply_tma_kernel(const ApplyParams p) {
-  extern __shared__ __align__(128) uint4 ring[];  // [STAGES][ROWS][kApplyThreads]
+  // ring row: the 2 KB column group (MOTION: + 16 extra bytes, then the
+  // previous frame's same bytes)
+  constexpr int RS = MOTION ? 2 * (kApplyThreads + 1) : kApplyThreads;  // uint4 per ring row
+  extern __shared__ __align__(128) uint4 ring[];  // [STAGES][ROWS][RS]
   __shared__ __align__(8) uint64_t full[STAGES];
   int64_t item = blockIdx.x;
   const int cg = static_cast<int>(item % p.col_groups);
@@ -208,13 +243,30 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
   const int nrows = r1 - r0;
   const int nst = (nrows + ROWS - 1) / ROWS;
 
+  // MOTION: previous raw image rows (CTA-uniform; none -> plain K3)
+  const uint8_t *prev0 = nullptr;
+  bool extra = false;
+  if (MOTION) {
+    const int64_t bb = img / p.cam_count;
+    const int64_t cc = img - bb * p.cam_count;
+    const uint8_t *pimg = bb > 0 ? p.src + (img - p.cam_count) * p.img_bytes
+                                 : (p.prev_first ? p.prev_first + cc * p.img_bytes : nullptr);
+    if (pimg != nullptr)
+      prev0 = pimg + static_cast<int64_t>(r0) * rb + static_cast<int64_t>(cg) * kApplyThreads * 16;
+    extra = static_cast<int64_t>(cg) * kApplyThreads * 16 + seg < rb;
+  }
+  const uint32_t cseg = seg + (prev0 != nullptr && extra ? 16u : 0u);
+
   auto issue = [&](int st) {
     const int slot = st % STAGES;
     const int rr = min(ROWS, nrows - st * ROWS);
-    mbar_expect_tx(&full[slot], seg * rr);
-    for (int i = 0; i < rr; ++i)
-      bulk_g2s(ring + (slot * ROWS + i) * kApplyThreads,
-               src0 + static_cast<int64_t>(st * ROWS + i) * rb, seg, &full[slot]);
+    mbar_expect_tx(&full[slot], (prev0 != nullptr ? 2 * cseg : seg) * rr);
+    for (int i = 0; i < rr; ++i) {
+      const int64_t ro = static_cast<int64_t>(st * ROWS + i) * rb;
+      bulk_g2s(ring + (slot * ROWS + i) * RS, src0 + ro, cseg, &full[slot]);
+      if (MOTION && prev0 != nullptr)
+        bulk_g2s(ring + (slot * ROWS + i) * RS + kApplyThreads + 1, prev0 + ro, cseg, &full[slot]);
+    }
   };
 
   if (threadIdx.x == 0) {
@@ -257,16 +309,95 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
       cf.a[i] = fabsf(a[i]) < 7.7037197787136e-34f ? 0.0f : a[i] * 0.00390625f;
   }
 
+  // MOTION: the windows of the overlap-0 tiling meeting the CTA (<= 3 window
+  // columns x 3 window rows: camx_motion_supported), this thread's
+  // pixel-start bits per window column; per-window-column counts `acc` of
+  // the rows since the last change of the set of window rows containing the
+  // row, flushed (warp sum + one atomic per window) when that set changes
+  constexpr int XW = MOTION ? 3 : 1;
+  uint32_t xmask[XW], acc[XW];
+  int xwin[XW], ywin[XW], ylo[XW];
+  int nxs = 0, nys = 0, yset = 0, ynext = 0;
+  const int lane = threadIdx.x & 31;
+  MotionThr mt{};
+  auto yset_at = [&](int R, int &next) {  // window rows containing row R; next change
+    int m = 0;
+    next = r1;
+#pragma unroll
+    for (int b2 = 0; b2 < XW; ++b2)
+      if (b2 < nys) {
+        if (R >= ylo[b2] && R < ylo[b2] + p.win) {
+          m |= 1 << b2;
+          next = min(next, ylo[b2] + p.win);
+        } else if (ylo[b2] > R) {
+          next = min(next, ylo[b2]);
+        }
+      }
+    return m;
+  };
+  auto flush = [&]() {
+    const int64_t bb = img / p.cam_count;
+#pragma unroll
+    for (int a = 0; a < XW; ++a)
+      if (a < nxs) {
+        const uint32_t c = __reduce_add_sync(0xffffffffu, acc[a]);
+        if (lane == 0 && c != 0) {
+#pragma unroll
+          for (int b2 = 0; b2 < XW; ++b2)
+            if (yset & (1 << b2))
+              atomicAdd(p.counts + (bb * p.ny + ywin[b2]) * p.nx + xwin[a],
+                        static_cast<unsigned long long>(c));
+        }
+        acc[a] = 0;
+      }
+  };
+  if (MOTION && prev0 != nullptr) {
+    const int cam = p.cam_begin + static_cast<int>(img % p.cam_count);
+    const int cb0 = cg * kApplyThreads * 16;
+    const int X0 = cam * p.W + (cb0 + 2) / 3;
+    const int X1 = cam * p.W + (cb0 + static_cast<int>(seg) + 2) / 3;
+    auto wins = [](int a0, int a1, int S, int n, int nreg, int len, int *out) {
+      // <= XW by the host's geometry check (camx_motion_supported)
+      int m = 0;
+      for (int i = a0 / S; i <= (a1 - 1) / S && i < nreg && m < XW; ++i) out[m++] = i;
+      if (n > nreg && len - S < a1 && m < XW) out[m++] = n - 1;  // the clamped last window
+      return m;
+    };
+    nxs = wins(X0, X1, p.win, p.nx, p.nx_reg, p.mosaic_w, xwin);
+    nys = wins(r0, r1, p.win, p.ny, p.ny_reg, p.H, ywin);
+#pragma unroll
+    for (int a = 0; a < XW; ++a) {
+      xmask[a] = 0;
+      acc[a] = 0;
+      ylo[a] = a < nys ? (ywin[a] < p.ny_reg ? ywin[a] * p.win : p.H - p.win) : 0;
+    }
+    const int ph = (3 - j % 3) % 3;  // first pixel start in the chunk (16 j + ph = 0 mod 3)
+    for (int a = 0; a < nxs; ++a) {
+      const int wx0 = xwin[a] < p.nx_reg ? xwin[a] * p.win : p.mosaic_w - p.win;
+      for (int sb = ph; sb < 16; sb += 3) {
+        const int x = cam * p.W + (j * 16 + sb) / 3;
+        if (x >= wx0 && x < wx0 + p.win) xmask[a] |= 1u << sb;
+      }
+    }
+    yset = yset_at(r0, ynext);
+    const int t = p.t_motion;
+    mt.hi = t >= 128;
+    mt.k7 = static_cast<uint32_t>(127 - (t & 127)) * 0x01010101u;
+  }
+  // the next chunk's first 2 bytes: the next thread's chunk, or the 16
+  // extra bytes past the group; none at the row end
+  const bool has_next = threadIdx.x + 1 < chunks || extra;
+
   uint8_t *dst = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
   for (int st = 0; st < nst; ++st) {
     const int slot = st % STAGES;
     mbar_wait(&full[slot], (st / STAGES) & 1);
     const int rr = min(ROWS, nrows - st * ROWS);
+    uint4 v[ROWS];
     if (active) {
-      uint4 v[ROWS];
 #pragma unroll
       for (int i = 0; i < ROWS; ++i)
-        if (i < rr) v[i] = ring[(slot * ROWS + i) * kApplyThreads + threadIdx.x];
+        if (i < rr) v[i] = ring[(slot * ROWS + i) * RS + threadIdx.x];
 #pragma unroll
       for (int i = 0; i < ROWS; ++i)
         if (i < rr) {
@@ -274,9 +405,36 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
           st_stream_v4(dst + static_cast<int64_t>(st * ROWS + i) * rb, o);
         }
     }
+    if (MOTION && prev0 != nullptr) {
+#pragma unroll
+      for (int i = 0; i < ROWS; ++i)
+        if (i < rr) {  // CTA-uniform
+          uint32_t on = 0;
+          if (active) {
+            const uint4 *row = ring + (slot * ROWS + i) * RS;
+            uint32_t E = flags16(v[i], row[kApplyThreads + 1 + threadIdx.x], mt);
+            if (has_next) {
+              const uint32_t nc = reinterpret_cast<const uint32_t *>(row + threadIdx.x + 1)[0];
+              const uint32_t np =
+                  reinterpret_cast<const uint32_t *>(row + kApplyThreads + 2 + threadIdx.x)[0];
+              E |= (gt_nibble(nc, np, mt) & 3u) << 16;
+            }
+            on = E | (E >> 1) | (E >> 2);
+          }
+#pragma unroll
+          for (int a = 0; a < XW; ++a)
+            if (a < nxs) acc[a] += __popc(on & xmask[a]);
+          const int R1 = r0 + st * ROWS + i + 1;  // the set of window rows changes after row i?
+          if (R1 == ynext) {
+            flush();
+            yset = yset_at(R1, ynext);
+          }
+        }
+    }
     __syncthreads();  // slot consumed
     if (threadIdx.x == 0 && st + STAGES < nst) issue(st + STAGES);
   }
+  if (MOTION && prev0 != nullptr) flush();
 }
 
 // ------------------------------------------------------------- generic path
@@ -324,11 +482,11 @@ static bool plan_fast(ApplyParams &p) {
   return true;
 }
 
-template <int ROWS = kTmaRows, int STAGES = kTmaStages, int MINB = 0>
+template <int ROWS = kTmaRows, int STAGES = kTmaStages, int MINB = 0, bool MOTION = false>
 static int launch_tma(const ApplyParams &p, cudaStream_t stream) {
   const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
-  const size_t smem = STAGES * ROWS * kApplyThreads * 16;
-  cudaError_t e = cudaFuncSetAttribute(apply_tma_kernel<ROWS, STAGES, MINB>,
+  const size_t smem = STAGES * ROWS * (MOTION ? 2 * (kApplyThreads + 1) : kApplyThreads) * 16;
+  cudaError_t e = cudaFuncSetAttribute(apply_tma_kernel<ROWS, STAGES, MINB, MOTION>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
@@ -342,7 +500,7 @@ static int launch_tma(const ApplyParams &p, cudaStream_t stream) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = p.pdl ? 1 : 0;
-  e = cudaLaunchKernelEx(&lc, apply_tma_kernel<ROWS, STAGES, MINB>, p);
+  e = cudaLaunchKernelEx(&lc, apply_tma_kernel<ROWS, STAGES, MINB, MOTION>, p);
   return e == cudaSuccess ? launch_status() : static_cast<int>(e);
 }
 
@@ -550,6 +708,104 @@ extern "C" int camx_correct_batch(const uint8_t *images, uint8_t *out, const uin
                                gain_out, offset_out);
   p.pdl = 1;  // K3 is a programmatic dependent of K2
   return launch_apply(p, as_stream(stream));
+}
+
+// Origins of the overlap-0 tiling along one axis (attention.py:53-63 with
+// stride == size): `nreg` regular windows at i * size (i * size + size <
+// len), then the clamped last window at len - size (never a duplicate).
+static void tiling_axis(int len, int size, int &n, int &nreg) {
+  nreg = len > size ? (len - size + size - 1) / size : 0;
+  n = nreg + 1;
+}
+
+extern "C" int camx_tiling_size(int32_t mosaic_w, int32_t mosaic_h, int32_t size, int32_t *nx,
+                                int32_t *ny) {
+  if (size < 1 || size > mosaic_w || size > mosaic_h || nx == nullptr || ny == nullptr)
+    return CAMX_EINVAL;
+  int a, b;
+  tiling_axis(mosaic_w, size, a, b);
+  *nx = a;
+  tiling_axis(mosaic_h, size, a, b);
+  *ny = a;
+  return CAMX_OK;
+}
+
+// Windows of the overlap-0 tiling meeting [a0, a1) (regular + clamped).
+static int windows_meeting(int a0, int a1, int S, int n, int nreg, int len) {
+  int m = 0;
+  for (int i = a0 / S; i <= (a1 - 1) / S && i < nreg; ++i) ++m;
+  return m + ((n > nreg && len - S < a1) ? 1 : 0);
+}
+
+// The fused motion counts keep <= 3 x 3 windows per K3 CTA in registers:
+// the largest number of windows any CTA's columns / rows meet.
+static bool motion_fits(const ApplyParams &p, int size) {
+  int nx, nxr, ny, nyr;
+  tiling_axis(p.n_cams * p.W, size, nx, nxr);
+  tiling_axis(p.H, size, ny, nyr);
+  const int cgb = kApplyThreads * 16;
+  for (int cam = 0; cam < p.n_cams; ++cam)
+    for (int cg = 0; cg < p.col_groups; ++cg) {
+      const int cb0 = cg * cgb, seg = std::min(cgb, p.row_bytes - cb0);
+      const int X0 = cam * p.W + (cb0 + 2) / 3, X1 = cam * p.W + (cb0 + seg + 2) / 3;
+      if (windows_meeting(X0, X1, size, nx, nxr, p.n_cams * p.W) > 3) return false;
+    }
+  for (int k = 0; k < p.K; ++k)
+    for (int rs = 0; rs < p.row_splits; ++rs) {
+      const int r0 = k * p.bh + rs * p.rows_per_split;
+      const int r1 = std::min(k == p.K - 1 ? p.H : (k + 1) * p.bh, r0 + p.rows_per_split);
+      if (r0 < r1 && windows_meeting(r0, r1, size, ny, nyr, p.H) > 3) return false;
+    }
+  return true;
+}
+
+extern "C" int camx_motion_supported(int32_t n_batch, int32_t n_cams, int32_t height,
+                                     int32_t width, int32_t blocks, int32_t size) {
+  if (n_batch < 1 || n_cams < 2 || height < 1 || width < 1 || blocks < 1 || blocks > height)
+    return 0;
+  if (size < 1 || size > n_cams * width || size > height) return 0;
+  alignas(16) uint8_t dummy[16];
+  ApplyParams p = array_params(dummy, dummy, n_batch, n_cams, 0, height, width, blocks, nullptr,
+                               nullptr);
+  return plan_fast(p) && motion_fits(p, size) ? 1 : 0;
+}
+
+extern "C" int camx_correct_batch_motion(
+    const uint8_t *images, uint8_t *out, const uint8_t *prev_frame, int32_t n_batch,
+    int32_t n_cams, int32_t wrap, int32_t height, int32_t width, int32_t band_width,
+    int32_t t_diff, const camx_solve_config *cfg, const double *prev_gain,
+    const double *prev_offset, camx_band_stat *stats, uint32_t *hist, double *gain_out,
+    double *offset_out, uint8_t *fit_ok_out, const uint8_t *motion_prev, int32_t win_size,
+    int32_t t_motion, int64_t *counts_out, void *stream) {
+  if (out == nullptr || counts_out == nullptr || cfg == nullptr) return CAMX_EINVAL;
+  if (n_batch < 1 || n_cams < 2 || height < 1 || width < 1) return CAMX_EINVAL;
+  if (cfg->blocks < 1 || cfg->blocks > height) return CAMX_EINVAL;
+  if (t_motion < 0 || t_motion > 255) return CAMX_EINVAL;
+  const int32_t mw = n_cams * width;
+  if (win_size < 1 || win_size > mw || win_size > height) return CAMX_EINVAL;
+  ApplyParams p = array_params(images, out, n_batch, n_cams, wrap, height, width, cfg->blocks,
+                               gain_out, offset_out);
+  // 16-byte aligned rows and <= 3 x 3 windows per CTA (camx_motion_supported)
+  if (!plan_fast(p) || !motion_fits(p, win_size)) return CAMX_EINVAL;
+  tiling_axis(mw, win_size, p.nx, p.nx_reg);
+  tiling_axis(height, win_size, p.ny, p.ny_reg);
+  p.win = win_size;
+  p.mosaic_w = mw;
+  p.t_motion = t_motion;
+  p.prev_first = motion_prev;
+  p.counts = reinterpret_cast<unsigned long long *>(counts_out);
+  // zeroed before K1, so that K2 -> K3 stay programmatically chained
+  cudaError_t e = cudaMemsetAsync(counts_out, 0,
+                                  sizeof(int64_t) * static_cast<size_t>(n_batch) * p.nx * p.ny,
+                                  as_stream(stream));
+  if (e != cudaSuccess) return static_cast<int>(e);
+  int st = stats_and_solve(images, prev_frame, n_batch, n_cams, wrap, height, width, band_width,
+                           t_diff, cfg, prev_gain, prev_offset, stats, hist, gain_out, offset_out,
+                           fit_ok_out, stream);
+  if (st != CAMX_OK) return st;
+  p.pdl = 1;
+  // 4 stages x 2 rows x (2 KB + 16 B) x 2 frames = 33 KB per CTA, 5 CTAs/SM
+  return launch_tma<kTmaRows, 4, 5, true>(p, as_stream(stream));
 }
 
 namespace camx {

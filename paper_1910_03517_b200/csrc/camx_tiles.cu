@@ -422,7 +422,6 @@ constexpr int kBandThreads = 256;
 #define CAMX_TILES_BAND_CTAS 16
 #endif
 constexpr int kBandCtasPerTile = CAMX_TILES_BAND_CTAS;  // CTAs sharing one tile's bands
-constexpr uint32_t kTapStraddle = 0x80000000u;  // taps in two camera segments
 
 struct BandSeg {
   int x_begin, x_end;  // window-local pixel range of the segment
