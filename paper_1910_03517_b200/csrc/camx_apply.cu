@@ -198,22 +198,20 @@ constexpr int kTmaRows = 2;  // rows per stage
 // into a nibble; a thread's 16 bytes + the next 2 (from the next chunk in
 // the ring) give an 18-bit flag mask E, and a pixel is on iff any of its 3
 // bytes is: E | E >> 1 | E >> 2 at the thread's pixel starts.
-struct MotionThr {
-  uint32_t k7;  // (127 - t') * 0x01010101, t' = t mod 128
-  bool hi;      // t >= 128
-};
-__device__ __forceinline__ uint32_t gt_nibble(uint32_t cur, uint32_t prev, const MotionThr &m) {
+template <bool HI>  // t >= 128
+__device__ __forceinline__ uint32_t gt_nibble(uint32_t cur, uint32_t prev, uint32_t k7) {
   const uint32_t d = __vabsdiffu4(cur, prev);
-  const uint32_t s = (d & 0x7F7F7F7Fu) + m.k7;  // bit 7 of a byte: low7(d) > t'
-  const uint32_t f = (m.hi ? (s & d) : (s | d)) & 0x80808080u;
+  const uint32_t s = (d & 0x7F7F7F7Fu) + k7;  // bit 7 of a byte: low7(d) > t mod 128
+  const uint32_t f = (HI ? (s & d) : (s | d)) & 0x80808080u;
   return (f * 0x00204081u) >> 28;  // byte MSBs 7, 15, 23, 31 -> bits 0..3
 }
-__device__ __forceinline__ uint32_t flags16(uint4 c, uint4 q, const MotionThr &m) {
-  return gt_nibble(c.x, q.x, m) | (gt_nibble(c.y, q.y, m) << 4) |
-         (gt_nibble(c.z, q.z, m) << 8) | (gt_nibble(c.w, q.w, m) << 12);
+template <bool HI>
+__device__ __forceinline__ uint32_t flags16(uint4 c, uint4 q, uint32_t k7) {
+  return gt_nibble<HI>(c.x, q.x, k7) | (gt_nibble<HI>(c.y, q.y, k7) << 4) |
+         (gt_nibble<HI>(c.z, q.z, k7) << 8) | (gt_nibble<HI>(c.w, q.w, k7) << 12);
 }
 
-template <int ROWS, int STAGES, int MINB = 0, bool MOTION = false>
+template <int ROWS, int STAGES, int MINB = 0, bool MOTION = false, bool MHI = false>
 __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
     apply_tma_kernel(const ApplyParams p) {
   // ring row: the 2 KB column group (MOTION: + 16 extra bytes, then the
@@ -319,7 +317,7 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
   int xwin[XW], ywin[XW], ylo[XW];
   int nxs = 0, nys = 0, yset = 0, ynext = 0;
   const int lane = threadIdx.x & 31;
-  MotionThr mt{};
+  uint32_t k7 = 0;
   auto yset_at = [&](int R, int &next) {  // window rows containing row R; next change
     int m = 0;
     next = r1;
@@ -372,7 +370,7 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
       ylo[a] = a < nys ? (ywin[a] < p.ny_reg ? ywin[a] * p.win : p.H - p.win) : 0;
     }
     const int ph = (3 - j % 3) % 3;  // first pixel start in the chunk (16 j + ph = 0 mod 3)
-    for (int a = 0; a < nxs; ++a) {
+    for (int a = 0; a < nxs && active; ++a) {  // inactive threads count nothing
       const int wx0 = xwin[a] < p.nx_reg ? xwin[a] * p.win : p.mosaic_w - p.win;
       for (int sb = ph; sb < 16; sb += 3) {
         const int x = cam * p.W + (j * 16 + sb) / 3;
@@ -380,13 +378,11 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
       }
     }
     yset = yset_at(r0, ynext);
-    const int t = p.t_motion;
-    mt.hi = t >= 128;
-    mt.k7 = static_cast<uint32_t>(127 - (t & 127)) * 0x01010101u;
+    k7 = static_cast<uint32_t>(127 - (p.t_motion & 127)) * 0x01010101u;  // MHI: t >= 128
   }
   // the next chunk's first 2 bytes: the next thread's chunk, or the 16
   // extra bytes past the group; none at the row end
-  const bool has_next = threadIdx.x + 1 < chunks || extra;
+  const uint32_t next_mask = (threadIdx.x + 1 < chunks || extra) ? 3u : 0u;
 
   uint8_t *dst = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
   for (int st = 0; st < nst; ++st) {
@@ -394,10 +390,10 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
     mbar_wait(&full[slot], (st / STAGES) & 1);
     const int rr = min(ROWS, nrows - st * ROWS);
     uint4 v[ROWS];
-    if (active) {
 #pragma unroll
-      for (int i = 0; i < ROWS; ++i)
-        if (i < rr) v[i] = ring[(slot * ROWS + i) * RS + threadIdx.x];
+    for (int i = 0; i < ROWS; ++i)  // (inactive threads read ring bytes they never use)
+      if (i < rr) v[i] = ring[(slot * ROWS + i) * RS + threadIdx.x];
+    if (active) {
 #pragma unroll
       for (int i = 0; i < ROWS; ++i)
         if (i < rr) {
@@ -409,21 +405,18 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
 #pragma unroll
       for (int i = 0; i < ROWS; ++i)
         if (i < rr) {  // CTA-uniform
-          uint32_t on = 0;
-          if (active) {
-            const uint4 *row = ring + (slot * ROWS + i) * RS;
-            uint32_t E = flags16(v[i], row[kApplyThreads + 1 + threadIdx.x], mt);
-            if (has_next) {
-              const uint32_t nc = reinterpret_cast<const uint32_t *>(row + threadIdx.x + 1)[0];
-              const uint32_t np =
-                  reinterpret_cast<const uint32_t *>(row + kApplyThreads + 2 + threadIdx.x)[0];
-              E |= (gt_nibble(nc, np, mt) & 3u) << 16;
-            }
-            on = E | (E >> 1) | (E >> 2);
-          }
+          // branch-free: inactive threads have no pixel bits (xmask 0); the
+          // next chunk's word is always in the ring (the row has a spare 16
+          // bytes, the ring a spare 16 at its end), masked at the row end
+          const uint4 *row = ring + (slot * ROWS + i) * RS;
+          const uint32_t nc = reinterpret_cast<const uint32_t *>(row + threadIdx.x + 1)[0];
+          const uint32_t np =
+              reinterpret_cast<const uint32_t *>(row + kApplyThreads + 2 + threadIdx.x)[0];
+          const uint32_t E = flags16<MHI>(v[i], row[kApplyThreads + 1 + threadIdx.x], k7) |
+                             ((gt_nibble<MHI>(nc, np, k7) & next_mask) << 16);
+          const uint32_t on = E | (E >> 1) | (E >> 2);
 #pragma unroll
-          for (int a = 0; a < XW; ++a)
-            if (a < nxs) acc[a] += __popc(on & xmask[a]);
+          for (int a = 0; a < XW; ++a) acc[a] += __popc(on & xmask[a]);  // 0 past nxs
           const int R1 = r0 + st * ROWS + i + 1;  // the set of window rows changes after row i?
           if (R1 == ynext) {
             flush();
@@ -482,11 +475,13 @@ static bool plan_fast(ApplyParams &p) {
   return true;
 }
 
-template <int ROWS = kTmaRows, int STAGES = kTmaStages, int MINB = 0, bool MOTION = false>
+template <int ROWS = kTmaRows, int STAGES = kTmaStages, int MINB = 0, bool MOTION = false,
+          bool MHI = false>
 static int launch_tma(const ApplyParams &p, cudaStream_t stream) {
   const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
-  const size_t smem = STAGES * ROWS * (MOTION ? 2 * (kApplyThreads + 1) : kApplyThreads) * 16;
-  cudaError_t e = cudaFuncSetAttribute(apply_tma_kernel<ROWS, STAGES, MINB, MOTION>,
+  const size_t smem = STAGES * ROWS * (MOTION ? 2 * (kApplyThreads + 1) : kApplyThreads) * 16 +
+                      (MOTION ? 16 : 0);  // MOTION: the last row's next-word read
+  cudaError_t e = cudaFuncSetAttribute(apply_tma_kernel<ROWS, STAGES, MINB, MOTION, MHI>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
@@ -500,7 +495,7 @@ static int launch_tma(const ApplyParams &p, cudaStream_t stream) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = p.pdl ? 1 : 0;
-  e = cudaLaunchKernelEx(&lc, apply_tma_kernel<ROWS, STAGES, MINB, MOTION>, p);
+  e = cudaLaunchKernelEx(&lc, apply_tma_kernel<ROWS, STAGES, MINB, MOTION, MHI>, p);
   return e == cudaSuccess ? launch_status() : static_cast<int>(e);
 }
 
@@ -805,7 +800,8 @@ extern "C" int camx_correct_batch_motion(
   if (st != CAMX_OK) return st;
   p.pdl = 1;
   // 4 stages x 2 rows x (2 KB + 16 B) x 2 frames = 33 KB per CTA, 5 CTAs/SM
-  return launch_tma<kTmaRows, 4, 5, true>(p, as_stream(stream));
+  if (t_motion >= 128) return launch_tma<kTmaRows, 4, 5, true, true>(p, as_stream(stream));
+  return launch_tma<kTmaRows, 4, 5, true, false>(p, as_stream(stream));
 }
 
 namespace camx {
