@@ -75,15 +75,17 @@ def test_camx_arm_json_line_on_gpu():
 
 @pytest.mark.gpu
 def test_camx_arm_secondary_workloads_on_gpu():
-    """The default N=1 line also carries config4 and config5, each with its
-    own roofline and clocks."""
+    """The default N=1 line also carries config4, config5 and config5m (the
+    attention tick with the in-pass motion counts), each with its own
+    roofline and clocks."""
     r = _run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"], timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip()][-1])
     sec = {x["workload"].split(":")[0]: x for x in d["secondary"]}
-    assert set(sec) == {"config4", "config5"}
+    assert set(sec) == {"config4", "config5", "config5m"}
     for x in sec.values():
         assert x["value"] > 0 and x["roofline"]["bound"] == "hbm" and "clocks" in x
         assert 0 < x["roofline"]["frac"] <= 1.2 and x["gpu_launches"] >= 3 * x["steps"]
     assert sec["config4"]["config"]["wrap"] and sec["config4"]["config"]["batch"] == 64
     assert sec["config5"]["config"]["tiles_per_step"] == 36 * 30
+    assert 0 < sec["config5m"]["config"]["tiles_per_step"] <= 4 * 30  # Scheduler budget 4
