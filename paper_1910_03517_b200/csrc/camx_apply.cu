@@ -470,6 +470,12 @@ static bool plan_fast(ApplyParams &p) {
   int splits = 1;
   const int64_t target = static_cast<int64_t>(sm_count()) * 8;
   while (base * splits < target && (max_rows + splits) / (splits + 1) >= 16) ++splits;
+  // under ~4 waves of 96-row CTAs (a camera shard's group): halve the CTAs,
+  // which then run 7 per SM - the partial last wave and the ramp/drain
+  // shrink (one camera x 30 frames: 103.8 -> 96.9 us; profiles/r02)
+  if (splits == 1 && base < 4 * static_cast<int64_t>(sm_count()) * CAMX_K3_MINB &&
+      (max_rows + 1) / 2 >= 16)
+    splits = 2;
   p.row_splits = splits;
   p.rows_per_split = (max_rows + splits - 1) / splits;
   return true;
