@@ -346,17 +346,13 @@ int camx_tiles_shard(const uint8_t *images, int32_t n_cams, int32_t height,
                      const int32_t *windows, int32_t n_tiles, int32_t size,
                      int32_t out_size, uint8_t *tiles_out, void *stream);
 
-/* Stage 3 + 4b (config 5): apply the array correction AND cut the tiles
- * from the corrected pixels.  When the geometry allows (aligned rows, at
- * most 64 windows per array-frame, out_size <= 3*size) this is ONE pass
- * over the raw frames: the apply kernel resamples every tile row whose
- * source rows it holds in shared memory, and a small fix-up kernel
- * completes the outputs whose taps straddle two CTAs from the corrected
- * frame.  Otherwise apply, then camx_tiles on `out`.  windows: device int32
- * [n_tiles][3] (batch index, x, y) GROUPED BY batch index; frame_off:
- * device int32 [n_batch+1] first tile of each array-frame (NULL disables
- * fusion); max_tiles_per_frame: the largest group.  Maps as
- * camx_apply_array (cam_begin = 0, cam_count = n_cams). */
+/* Stage 3 + 4b (config 5): apply the array correction, then cut the tiles
+ * from the corrected frames with camx_tiles' TMA-staged resample (the tile
+ * kernel reads each output row's two tap rows of `out`).  windows: device
+ * int32 [n_tiles][3] (batch index, x, y); frame_off (device int32
+ * [n_batch+1], first tile of each array-frame) and max_tiles_per_frame
+ * describe their grouping by array-frame (ABI v1 arguments, may be NULL /
+ * 0).  Maps as camx_apply_array (cam_begin = 0, cam_count = n_cams). */
 int camx_correct_and_tile(const uint8_t *images, uint8_t *out,
                           int32_t n_batch, int32_t n_cams, int32_t wrap,
                           int32_t height, int32_t width, int32_t blocks,
@@ -366,7 +362,7 @@ int camx_correct_and_tile(const uint8_t *images, uint8_t *out,
                           int32_t size, int32_t out_size, uint8_t *tiles_out,
                           void *stream);
 
-/* camx_correct_batch + tiles: K1, K2 (PDL), fused apply+tiles (PDL). */
+/* camx_correct_batch + tiles: K1, K2 (PDL), K3 (PDL), tiles (camx_tiles). */
 int camx_correct_batch_tiles(
     const uint8_t *images, uint8_t *out, const uint8_t *prev_frame,
     int32_t n_batch, int32_t n_cams, int32_t wrap, int32_t height,

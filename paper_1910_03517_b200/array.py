@@ -455,11 +455,9 @@ class ArrayCorrector:
         full_ptr = stats.data_ptr() + lo * rec_bytes
         if self.exchange is not None:
             # Python exchange (any torch.distributed backend): host-synchronous
-            # on both sides.  Gloo's CUDA all-gather does not reliably order
-            # its device copies against a caller stream it did not create
-            # (K2 was measured reading the records before they landed), and
-            # this path exists for portability, not speed - the NCCL path is
-            # the stream-ordered camx_correct_batch_sharded.
+            # on both sides (for gloo the records go through host copies:
+            # dist._gather).  This path exists for portability, not speed -
+            # the NCCL path is the stream-ordered camx_correct_batch_sharded.
             t = _dev.torch()
             ext = t.cuda.ExternalStream(sh)
             ext.synchronize()
@@ -470,6 +468,7 @@ class ArrayCorrector:
                     buf["full"] = t.empty((buf["stats"].shape[0], self.n_cams, *full.shape[2:]),
                                           dtype=full.dtype, device=full.device)
                 buf["full"][lo:hi].copy_(full)
+            t.cuda.synchronize()  # the records are in place before K2 is enqueued
             full_ptr = buf["full"][lo].data_ptr()
         have_prev = prev_maps is not None
         sc = _lib.SolveConfig(_MODE_CODE[self.mode], self.K, int(cfg.min_band_pixels),

@@ -59,9 +59,7 @@ def make_stats_exchange(n_cams: int, group=None):
             chunks = list(recv.unbind(0))
         else:
             chunks = [t.empty_like(send) for _ in range(world)]
-            _host_sync(nccl, send)
-            dist.all_gather(chunks, send, group=group)
-            _host_sync(nccl, send)
+            _gather(chunks, send, nccl, group)
         return t.cat([chunks[g][:, :c] for g, (_, c) in enumerate(parts)], dim=1).contiguous()
 
     return exchange
@@ -188,18 +186,38 @@ def sharded_window_counts(origins, size: int, *, cur=None, prev=None, mask=None,
     part = t.as_tensor(np.asarray(counts_fn(local, size), dtype=np.int64))
     if dist.get_backend(group) == "nccl":
         part = part.cuda()
-    else:
-        _host_sync(False, cur if cur is not None else mask)
-    dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+    _reduce_sum(part, dist.get_backend(group) == "nccl", group)
     return part.cpu().numpy()
 
 
-def _host_sync(nccl: bool, x) -> None:
-    """Non-NCCL backends on CUDA tensors: finish the device work on both
-    sides of the collective (gloo does not reliably order its copies
-    against the caller's stream; see ArrayCorrector._stats_solve)."""
-    if not nccl and getattr(x, "is_cuda", False):
-        _dev.torch().cuda.synchronize()
+def _gather(outs, x, nccl: bool, group=None) -> None:
+    """all_gather of `x` into `outs`.  NCCL: on the device, stream-ordered.
+    Other backends (gloo): through host copies - gloo's CUDA collectives do
+    not reliably order their device copies against the caller's stream (a
+    K2 launched after the exchange was measured reading records that had
+    not landed), so the device tensors are copied to the host (synchronous),
+    gathered there, and copied back (stream-ordered before later kernels)."""
+    import torch.distributed as dist
+    if nccl:
+        dist.all_gather(outs, x, group=group)
+        return
+    xc = x.cpu()
+    hs = [_dev.torch().empty_like(xc) for _ in outs]
+    dist.all_gather(hs, xc, group=group)
+    for o, h in zip(outs, hs):
+        o.copy_(h)
+
+
+def _reduce_sum(x, nccl: bool, group=None):
+    """all_reduce(SUM) of `x` (host copies for non-NCCL backends; see _gather)."""
+    import torch.distributed as dist
+    if nccl or not getattr(x, "is_cuda", False):
+        dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group)
+        return x
+    xc = x.cpu()
+    dist.all_reduce(xc, op=dist.ReduceOp.SUM, group=group)
+    x.copy_(xc)
+    return x
 
 
 def tile_homes(windows, size: int, n_cams: int, width: int, world: int):
@@ -255,9 +273,7 @@ def sharded_tiles(out_local, windows, *, size: int = 960, out_size: int = 416, n
     # (1) halo: every rank's first corrected column
     first = out_local[:, 0, :, 0, :].contiguous()  # (B, H, 3)
     cols = [t.empty_like(first) for _ in range(world)]
-    _host_sync(nccl, first)
-    dist.all_gather(cols, first, group=group)
-    _host_sync(nccl, first)
+    _gather(cols, first, nccl, group)
     halo = cols[rank + 1] if rank + 1 < world else None
 
     if tiles_fn is None:
@@ -286,13 +302,9 @@ def sharded_tiles(out_local, windows, *, size: int = 960, out_size: int = 416, n
         part[t.as_tensor(mine, device=dev)] = sub
     if strad:
         if not nccl and part.dtype == t.uint8:  # gloo sums int32
-            acc = part.to(t.int32)
-            _host_sync(nccl, acc)
-            dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
-            _host_sync(nccl, acc)
-            part = acc.to(t.uint8)
+            part = _reduce_sum(part.to(t.int32), nccl, group).to(t.uint8)
         else:
-            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+            _reduce_sum(part, nccl, group)
 
     ids = sorted(own + [i for i in strad if homes[i][0] == rank])
     pos_own = {i: k for k, i in enumerate(own)}
