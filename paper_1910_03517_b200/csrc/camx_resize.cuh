@@ -46,12 +46,13 @@ template <int J>
 __device__ __forceinline__ void resample_row_lanes(const uint8_t *ra, const uint8_t *rb,
                                                    const uint32_t (&off)[J],
                                                    const uint32_t (&wt)[J], uint32_t wy1,
-                                                   uint8_t *orow, int out, int lane) {
+                                                   uint8_t *orow, int out, int lane,
+                                                   int ox_lo = 0, int ox_hi = 1 << 30) {
   const uint32_t wy0 = 256u - wy1;
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int ox = lane + 32 * j;
-    if (ox < out) {
+    if (ox < out && ox >= ox_lo && ox < ox_hi) {
       const uint32_t la = off[j];
       const uint32_t sh = la * 8u;  // funnel shifts use the low 5 bits
       const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
@@ -73,13 +74,13 @@ __device__ __forceinline__ void resample_row_lanes(const uint8_t *ra, const uint
 // Per-lane column taps of resample_row_lanes (lane l: columns l + 32 j).
 template <int J>
 __device__ __forceinline__ void lane_taps(int lane, int out, float scale, int size, int head,
-                                          uint32_t (&off)[J], uint32_t (&wt)[J]) {
+                                          uint32_t (&off)[J], uint32_t (&wt)[J], int shift = 0) {
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int ox = lane + 32 * j;
     int a = 0, c, w1 = 0;
     if (ox < out) src_coord_w(ox, scale, size, a, c, w1);
-    off[j] = static_cast<uint32_t>(head + 3 * a);
+    off[j] = static_cast<uint32_t>(head + 3 * (a + shift));  // (unused when not owned)
     wt[j] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
   }
 }

@@ -228,9 +228,19 @@ __host__ __device__ __forceinline__ size_t tma_tile_smem(const TmaTileGeom &g) {
   return static_cast<size_t>(kTmaTileWarps) * kTmaTileSlots * (2 * g.pitch + g.opitch);
 }
 
+// Camera shard (camx_tiles_shard): this GPU holds mosaic columns
+// [col_begin, col_begin + local_cols); it stages the window's local columns
+// (+ the halo pixel: the next rank's first column) and writes the output
+// columns whose first tap is local, leaving the others untouched.
+struct TileShard {
+  int32_t col_begin, local_cols;
+  const uint8_t *halo;  // [B][H][3] or nullptr
+};
+
 template <int J>
 __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const TileParams p,
-                                                                       const TmaTileGeom g) {
+                                                                       const TmaTileGeom g,
+                                                                       const TileShard sd) {
   extern __shared__ __align__(128) uint8_t tts[];
   __shared__ __align__(8) uint64_t full[kTmaTileWarps][kTmaTileSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -238,21 +248,44 @@ __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const Til
   const int64_t b = p.wins[3 * t];
   const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
   const int out = p.out, O3 = out * 3;
+  // the window's local pixels [ps, pe) (the whole window without a shard)
+  const int lx0 = x0 - sd.col_begin;
+  const int ps = max(lx0, 0), pe = min(lx0 + p.size, sd.local_cols);
+  if (ps >= pe) return;  // no local column (CTA-uniform)
+  const bool halo = sd.halo != nullptr && lx0 + p.size > sd.local_cols;
   const int64_t rowbytes = static_cast<int64_t>(p.W) * 3;
   const int64_t img_bytes = static_cast<int64_t>(p.H) * rowbytes;
-  const int cam0 = x0 / p.W, cam1 = (x0 + p.size - 1) / p.W;
-  const int sb = (x0 - cam0 * p.W) * 3;                          // first wanted byte (cam0 row)
+  const int cam0 = ps / p.W, cam1 = (pe - 1) / p.W;
+  const int sb = (ps - cam0 * p.W) * 3;                          // first wanted byte (cam0 row)
   const int head = sb & 15;
-  const int eb = ((x0 + p.size - cam1 * p.W) * 3 + 15) & ~15;    // staged end (cam1 row)
+  const int eb = ((pe - cam1 * p.W) * 3 + 15) & ~15;             // staged end (cam1 row)
   const uint32_t n_first = static_cast<uint32_t>((cam0 == cam1 ? eb : rowbytes) - (sb - head));
   const uint32_t row_tx = cam0 == cam1 ? n_first
       : n_first + static_cast<uint32_t>((cam1 - cam0 - 1) * rowbytes + eb);
   const uint8_t *frame = p.img + b * p.n_cams * img_bytes;
   const int slot_bytes = 2 * g.pitch + g.opitch;
   uint8_t *wbase = tts + warp * kTmaTileSlots * slot_bytes;
+  // owned output columns: first tap lx0 + i0(ox) in [0, local_cols)
+  // (a contiguous range: i0 is nondecreasing)
+  int ox_lo = 0, ox_hi = out;
+  if (lx0 < 0 || lx0 + p.size > sd.local_cols) {
+    auto first = [&](int lim) {  // first ox with lx0 + i0(ox) >= lim
+      int lo = 0, hi = out;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        int a, c, w;
+        src_coord_w(mid, p.scale, p.size, a, c, w);
+        if (lx0 + a >= lim) hi = mid; else lo = mid + 1;
+      }
+      return lo;
+    };
+    ox_lo = first(0);
+    ox_hi = first(sd.local_cols);
+  }
+  const bool bulk = g.bulk_out && ox_lo == 0 && ox_hi == out;  // whole rows are ours
 
   uint32_t off[J], wt[J];
-  lane_taps<J>(lane, out, p.scale, p.size, head, off, wt);
+  lane_taps<J>(lane, out, p.scale, p.size, head, off, wt, lx0 - ps);
   const int oy0 = blockIdx.x * g.rows_per_cta;
   const int oy1 = min(out, oy0 + g.rows_per_cta);
   const int n_rows = oy1 - oy0 > warp ? (oy1 - oy0 - warp + kTmaTileWarps - 1) / kTmaTileWarps : 0;
@@ -286,17 +319,28 @@ __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const Til
     for (int i = 0; i < min(kTmaTileSlots, n_rows); ++i) issue(i);
 
   uint8_t *tile = p.tiles + static_cast<int64_t>(t) * out * O3;
+  // the halo pixel sits right after the shard's last pixel (the staged
+  // bytes end at that camera's row end, 16-byte aligned)
+  const int halo_off = head + 3 * (sd.local_cols - ps);
   for (int i = 0; i < n_rows; ++i) {
     const int slot = i % kTmaTileSlots;
     const int oy = oy0 + warp + i * kTmaTileWarps;
     int ya, yb, w1y;
     src_coord_w(oy, p.scale, p.size, ya, yb, w1y);
-    const uint8_t *ra = wbase + slot * slot_bytes;
+    uint8_t *ra = wbase + slot * slot_bytes;
     uint8_t *ob = wbase + slot * slot_bytes + 2 * g.pitch;
-    uint8_t *orow = g.bulk_out ? ob : tile + static_cast<int64_t>(oy) * O3;
+    uint8_t *orow = bulk ? ob : tile + static_cast<int64_t>(oy) * O3;
     mbar_wait(&full[warp][slot], (i / kTmaTileSlots) & 1);
-    resample_row_lanes<J>(ra, ra + g.pitch, off, wt, static_cast<uint32_t>(w1y), orow, out, lane);
-    if (g.bulk_out) {
+    if (halo) {
+      if (lane < 6) {
+        const int r = lane / 3, ch = lane - 3 * r;
+        ra[r * g.pitch + halo_off + ch] = sd.halo[(b * p.H + y0 + (r ? yb : ya)) * 3 + ch];
+      }
+      __syncwarp();
+    }
+    resample_row_lanes<J>(ra, ra + g.pitch, off, wt, static_cast<uint32_t>(w1y), orow, out, lane,
+                          ox_lo, ox_hi);
+    if (bulk) {
       fence_proxy_async_smem();  // this lane's row bytes before the bulk store reads them
       __syncwarp();
       if (lane == 0) {
@@ -306,16 +350,20 @@ __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const Til
     }
     __syncwarp();  // every lane is done with the slot's source rows
     if (lane == 0) {
-      if (i + kTmaTileSlots < n_rows) issue(i + kTmaTileSlots);
+      if (i + kTmaTileSlots < n_rows) {
+        if (halo) fence_proxy_async_smem();  // the halo bytes (generic) before the refill
+        issue(i + kTmaTileSlots);
+      }
       // the next row writes the output buffer last read by row i + 1 - slots
-      if (g.bulk_out) bulk_wait_read<kTmaTileSlots - 1>();
+      if (bulk) bulk_wait_read<kTmaTileSlots - 1>();
     }
     __syncwarp();
   }
-  if (g.bulk_out && lane == 0) bulk_wait<0>();
+  if (bulk && lane == 0) bulk_wait<0>();
 }
 
-static int launch_tiles_tma(const TileParams &p, int32_t n_tiles, cudaStream_t s) {
+static int launch_tiles_tma(const TileParams &p, int32_t n_tiles, cudaStream_t s,
+                            const TileShard &sd) {
   const int J = (p.out + 31) / 32;
   TmaTileGeom g{};
   g.pitch = tma_tile_pitch(p.size);
@@ -333,7 +381,7 @@ static int launch_tiles_tma(const TileParams &p, int32_t n_tiles, cudaStream_t s
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return static_cast<int>(e);
-    kern<<<grid, kTmaTileWarps * 32, smem, s>>>(p, g);
+    kern<<<grid, kTmaTileWarps * 32, smem, s>>>(p, g, sd);
     return launch_status();
   };
   if (J <= 2) return go(tiles_tma_kernel<2>);
@@ -356,7 +404,8 @@ static bool tiles_tma_ok(const TileParams &p) {
 // may be the first column of the next rank, supplied as `halo` (B, H, 3) -
 // the 1-pixel corrected halo column.  Output pixels of other ranks' columns
 // are left untouched (the caller zero-fills and sums the partials).
-// Per-pixel gather: this path runs only for windows that touch a shard.
+// The TMA-staged kernel (tiles_tma_kernel with a TileShard) serves aligned
+// geometries; this per-pixel gather the rest.
 struct ShardTileParams {
   TileParams t;
   int32_t col_begin;    // global mosaic column of local column 0
@@ -396,217 +445,6 @@ __global__ void tiles_shard_kernel(const ShardTileParams p) {
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
       dst[3 * q + ch] = static_cast<uint8_t>(bilerp_fx(a[ch], bb[ch], c[ch], d[ch], wx, wy));
-  }
-}
-
-// 16-byte global -> shared copies without a register round trip
-// (cp.async.cg: every copy of a band in flight at once, instead of one
-// load -> store latency per element of the staging loop).
-__device__ __forceinline__ void stage16(void *smem_dst, const void *gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gsrc)
-               : "memory");
-}
-__device__ __forceinline__ void stage_wait() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-// Band-staging constants and segment records (camera-shard tile kernel).
-#ifndef CAMX_TILES_BAND_ROWS
-#define CAMX_TILES_BAND_ROWS 4
-#endif
-constexpr int kBandRows = CAMX_TILES_BAND_ROWS;
-constexpr int kBandThreads = 256;
-#ifndef CAMX_TILES_BAND_CTAS
-#define CAMX_TILES_BAND_CTAS 16
-#endif
-constexpr int kBandCtasPerTile = CAMX_TILES_BAND_CTAS;  // CTAs sharing one tile's bands
-
-struct BandSeg {
-  int x_begin, x_end;  // window-local pixel range of the segment
-  int cam;             // camera of the segment
-  int head;            // first wanted byte inside the staged 16-byte superset
-  int nvec;            // 16-byte vectors staged per row
-  int off;             // smem byte offset of the superset in a staged row
-};
-
-__device__ __forceinline__ int band_byte(const BandSeg &s0, const BandSeg &s1, int x) {
-  return x < s0.x_end ? s0.off + s0.head + 3 * x : s1.off + s1.head + 3 * (x - s1.x_begin);
-}
-
-// Band-staged kernel for a camera shard (camx_tiles_shard): as
-// tiles_band_kernel, but only the window's columns on this shard are staged
-// and only the output columns this shard owns (first tap on the shard,
-// contiguous [ox_lo, ox_hi) since i0 increases) are computed and stored; a
-// second tap on the next shard's first column comes from the halo.
-constexpr uint32_t kTapSeam = 0x40000000u;  // second tap = first pixel of segment 1
-constexpr uint32_t kTapHalo = 0x20000000u;  // second tap = the halo column
-constexpr uint32_t kTapFlags = kTapSeam | kTapHalo;
-
-__global__ void __launch_bounds__(kBandThreads) tiles_band_shard_kernel(const ShardTileParams sp,
-                                                                         int pitch,
-                                                                         int bands_per_cta) {
-  const TileParams &p = sp.t;
-  extern __shared__ __align__(16) uint8_t bsm[];
-  const int t = blockIdx.y;
-  const int64_t b = p.wins[3 * t];
-  const int x0 = p.wins[3 * t + 1], y0 = p.wins[3 * t + 2];
-  const int out = p.out;
-  const int O3 = out * 3;
-  // the window's columns on this shard, in local mosaic columns
-  const int lx0 = max(x0, sp.col_begin) - sp.col_begin;
-  const int lx1 = min(x0 + p.size, sp.col_begin + sp.local_cols) - sp.col_begin;
-  if (lx1 <= lx0) return;  // CTA-uniform: nothing here
-  uint2 *tap = reinterpret_cast<uint2 *>(bsm);
-  uint8_t *rows = bsm + ((out * 8 + 15) & ~15);
-  uint8_t *orow = rows + 2 * kBandRows * pitch;
-  __shared__ uint32_t wy_s[kBandRows];
-  __shared__ int srow_s[2 * kBandRows];
-  __shared__ const uint8_t *src0_s[2 * kBandRows], *src1_s[2 * kBandRows];
-  __shared__ int ox_lo_s, ox_hi_s;
-  // segments of the staged span [lx0, lx1) over this shard's cameras
-  BandSeg sg[2];
-  {
-    int x = lx0, off = 0;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int cam = min(x / p.W, p.n_cams - 1);
-      const int xe = min(lx1, (cam + 1) * p.W);
-      sg[i].x_begin = x - lx0;
-      sg[i].x_end = xe - lx0;
-      sg[i].cam = cam;
-      sg[i].head = ((x - cam * p.W) * 3) & 15;
-      sg[i].nvec = xe > x ? (sg[i].head + (xe - x) * 3 + 15) >> 4 : 0;
-      sg[i].off = off;
-      off += sg[i].nvec * 16;
-      x = xe;
-    }
-  }
-  if (threadIdx.x == 0) {
-    ox_lo_s = out;
-    ox_hi_s = 0;
-  }
-  __syncthreads();
-  const int span0 = x0 - sp.col_begin - lx0;  // window-local column a -> staged index a + span0
-  for (int ox = threadIdx.x; ox < out; ox += blockDim.x) {
-    int a, c, w1;
-    src_coord_w(ox, p.scale, p.size, a, c, w1);
-    const int sa = a + span0, sc = c + span0;  // indices in the staged span
-    uint32_t o = 0;
-    if (sa >= 0 && a + x0 - sp.col_begin < sp.local_cols) {  // first tap here: owned
-      o = static_cast<uint32_t>(band_byte(sg[0], sg[1], sa));
-      const bool halo = sc >= lx1 - lx0;  // second tap = the next shard's first column
-      if (halo) o |= kTapHalo;
-      else if (sa < sg[0].x_end && sc >= sg[0].x_end) o |= kTapSeam;
-      atomicMin(&ox_lo_s, ox);
-      atomicMax(&ox_hi_s, ox + 1);
-    }
-    tap[ox] = make_uint2(o, static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16));
-  }
-  __syncthreads();
-  const int ox_lo = ox_lo_s, ox_hi = ox_hi_s;
-  if (ox_hi <= ox_lo) return;  // CTA-uniform
-  const int width = ox_hi - ox_lo;
-  const int64_t rowbytes = static_cast<int64_t>(p.W) * 3;
-  const int64_t img_bytes = static_cast<int64_t>(p.H) * rowbytes;
-  const uint8_t *seg0 = p.img + (b * p.n_cams + sg[0].cam) * img_bytes +
-                        (lx0 + sg[0].x_begin - sg[0].cam * p.W) * 3 - sg[0].head;
-  const uint8_t *seg1 = p.img + (b * p.n_cams + sg[1].cam) * img_bytes +
-                        (lx0 + sg[1].x_begin - sg[1].cam * p.W) * 3 - sg[1].head;
-  const int nv0 = sg[0].nvec, nv = nv0 + sg[1].nvec;
-  const int off1 = sg[1].off;
-  const uint32_t a1_seg1 = static_cast<uint32_t>(sg[1].off + sg[1].head);
-  const int band0 = blockIdx.x * bands_per_cta;
-  for (int band = band0; band < band0 + bands_per_cta; ++band) {
-    const int oy0 = band * kBandRows;
-    if (oy0 >= out) break;
-    const int nr = min(kBandRows, out - oy0);
-    __syncthreads();
-    if (threadIdx.x < nr) {
-      int a, c, w1;
-      src_coord_w(oy0 + threadIdx.x, p.scale, p.size, a, c, w1);
-      wy_s[threadIdx.x] = static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16);
-      srow_s[2 * threadIdx.x] = y0 + a;
-      srow_s[2 * threadIdx.x + 1] = y0 + c;
-      src0_s[2 * threadIdx.x] = seg0 + (y0 + a) * rowbytes;
-      src0_s[2 * threadIdx.x + 1] = seg0 + (y0 + c) * rowbytes;
-      src1_s[2 * threadIdx.x] = seg1 + (y0 + a) * rowbytes;
-      src1_s[2 * threadIdx.x + 1] = seg1 + (y0 + c) * rowbytes;
-    }
-    __syncthreads();
-    {
-      int r = threadIdx.x / nv, v = threadIdx.x - r * nv;
-      const int step_r = blockDim.x / nv, step_v = blockDim.x - step_r * nv;
-      while (r < 2 * nr) {
-        const bool first = v < nv0;
-        const uint4 *src = reinterpret_cast<const uint4 *>(first ? src0_s[r] : src1_s[r]) +
-                           (first ? v : v - nv0);
-        stage16(rows + r * pitch + (first ? v * 16 : off1 + (v - nv0) * 16), src);
-        r += step_r;
-        v += step_v;
-        if (v >= nv) {
-          v -= nv;
-          ++r;
-        }
-      }
-      stage_wait();
-    }
-    __syncthreads();
-    // warp per (row, column half of the owned range), lanes stride the columns
-    {
-      constexpr int kUnitsPerRow = (kBandThreads / 32) / kBandRows > 0 ? (kBandThreads / 32) / kBandRows : 1;
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      for (int u = warp; u < nr * kUnitsPerRow; u += kBandThreads / 32) {
-        const int ol = u / kUnitsPerRow, part = u - ol * kUnitsPerRow;
-        const int c0 = part * width / kUnitsPerRow, c1 = (part + 1) * width / kUnitsPerRow;
-        const uint32_t wyp = wy_s[ol];
-        const uint32_t wy0 = wyp & 0xFFFFu, wy1 = wyp >> 16;
-        const uint8_t *ra = rows + (2 * ol) * pitch;
-        const uint8_t *rb = ra + pitch;
-        for (int ox = c0 + lane; ox < c1; ox += 32) {
-          const int gox = ox_lo + ox;
-          const uint2 tv = tap[gox];
-          uint8_t *o = orow + ol * O3 + 3 * gox;
-          if (!(tv.x & kTapFlags)) {
-            const uint32_t la = tv.x;
-            const uint32_t sh = la * 8u;
-            const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
-            const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
-            const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
-            const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-              const uint32_t sel = 0x0030u + 0x0011u * ch;
-              const uint32_t v0 = __dp2a_lo(tv.y, __byte_perm(alo, ahi, sel), 0u);
-              const uint32_t v1 = __dp2a_lo(tv.y, __byte_perm(blo, bhi, sel), 0u);
-              o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
-            }
-          } else {
-            const uint32_t a0 = tv.x & ~kTapFlags;
-            const uint32_t w1 = tv.y >> 16;
-            const bool use_halo = (tv.x & kTapHalo) != 0;
-            const uint8_t *ha = sp.halo + (b * p.H + srow_s[2 * ol]) * 3;
-            const uint8_t *hb = sp.halo + (b * p.H + srow_s[2 * ol + 1]) * 3;
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-              const uint32_t A = ra[a0 + ch], C = rb[a0 + ch];
-              const uint32_t Bv = use_halo ? ha[ch] : ra[a1_seg1 + ch];
-              const uint32_t D = use_halo ? hb[ch] : rb[a1_seg1 + ch];
-              o[ch] = static_cast<uint8_t>(bilerp_fx(A, Bv, C, D, w1, wy1));
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // store the owned byte range of every output row of the band
-    const int obytes = 3 * width;
-    for (int rr = 0; rr < nr; ++rr) {
-      uint8_t *drow = p.tiles + (static_cast<int64_t>(t) * out + oy0 + rr) * O3 + 3 * ox_lo;
-      const uint8_t *srow = orow + rr * O3 + 3 * ox_lo;
-      for (int c3 = threadIdx.x; c3 < obytes; c3 += blockDim.x) drow[c3] = srow[c3];
-    }
   }
 }
 
@@ -735,7 +573,7 @@ static int launch_tiles(const uint8_t *images, int32_t n_cams, int32_t height, i
     tiles_kernel<<<dim3(static_cast<unsigned>(bx), n_tiles), 256, 0, s>>>(p);
     return launch_status();
   }
-  if (tiles_tma_ok(p)) return launch_tiles_tma(p, n_tiles, s);
+  if (tiles_tma_ok(p)) return launch_tiles_tma(p, n_tiles, s, TileShard{0, n_cams * width, nullptr});
   if (size > width) {  // a window row spans > 2 cameras: per-pixel gather kernel
     const int64_t npx = static_cast<int64_t>(out_size) * out_size;
     int64_t bx = (npx + 255) / 256;
@@ -821,25 +659,9 @@ static int tiles_shard_launch(const uint8_t *images, int32_t n_cams, int32_t hei
   p.col_begin = col_begin;
   p.local_cols = n_cams * width;
   p.halo = halo;
-  if (out_size < size && size <= width && (width * 3) % 16 == 0 &&
-      reinterpret_cast<uintptr_t>(images) % 16 == 0) {
-    const int pitch = ((size * 3 + 15) & ~15) + 64;
-    const size_t smem = ((out_size * 8 + 15) & ~15) + 2 * kBandRows * pitch +
-                        static_cast<size_t>(kBandRows) * out_size * 3;
-    if (smem <= 200 * 1024) {
-      if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(tiles_band_shard_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return static_cast<int>(e);
-      }
-      const int nbands = (out_size + kBandRows - 1) / kBandRows;
-      const int bpc = (nbands + kBandCtasPerTile - 1) / kBandCtasPerTile;
-      dim3 grid((nbands + bpc - 1) / bpc, n_tiles);
-      tiles_band_shard_kernel<<<grid, kBandThreads, smem, as_stream(stream)>>>(p, pitch, bpc);
-      return launch_status();
-    }
-  }
+  if (out_size != size && tiles_tma_ok(p.t))  // TMA-staged, warp per output row
+    return launch_tiles_tma(p.t, n_tiles, as_stream(stream),
+                            TileShard{col_begin, n_cams * width, halo});
   const int64_t npx = static_cast<int64_t>(out_size) * out_size;
   int64_t bx = (npx + 255) / 256;
   if (bx > 128) bx = 128;
