@@ -431,27 +431,40 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
 }
 
 // ------------------------------------------------------------- generic path
-// Any width / alignment: one thread per pixel, coefficients per pixel.
-__global__ void apply_generic_kernel(const ApplyParams p) {
-  const int64_t npx = static_cast<int64_t>(p.n_img) * p.H * p.W;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < npx;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int col = static_cast<int>(t % p.W);
-    const int64_t rest = t / p.W;
-    const int row = static_cast<int>(rest % p.H);
-    const int64_t img = rest / p.H;
-    const int k = min(row / p.bh, p.K - 1);
-    const double *gl, *bl, *gr, *br;
-    map_ptrs(p, img, gl, bl, gr, br);
-    const int64_t off = img * p.img_bytes + static_cast<int64_t>(row) * p.row_bytes + col * 3;
+// Any width / alignment (rows not 16-byte multiples): thread = one pixel
+// column of one row block (split) of one image; the three channels' float32
+// (M, A) are made once and the block's rows are streamed with byte loads and
+// stores (a warp covers 96 contiguous bytes of a row).  Same float32 chain
+// as the reference: rn(p * M), + A, rint, clip.
+constexpr int kColThreads = 128;
+__global__ void __launch_bounds__(kColThreads) apply_cols_kernel(const ApplyParams p,
+                                                                 int64_t img0) {
+  const int col = blockIdx.x * kColThreads + threadIdx.x;
+  if (col >= p.W) return;
+  const int k = static_cast<int>(blockIdx.y) / p.row_splits;
+  const int rs = static_cast<int>(blockIdx.y) - k * p.row_splits;
+  const int64_t img = img0 + blockIdx.z;
+  const int blk_r0 = k * p.bh;
+  const int blk_r1 = (k == p.K - 1) ? p.H : blk_r0 + p.bh;
+  const int r0 = blk_r0 + rs * p.rows_per_split;
+  const int r1 = min(blk_r1, r0 + p.rows_per_split);
+  if (r0 >= r1) return;
+  const double *gl, *bl, *gr, *br;
+  map_ptrs(p, img, gl, bl, gr, br);
+  float m[3], a[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) coef_f32(col, ch, k, p.W, gl, bl, gr, br, m[ch], a[ch]);
+  const int64_t off = img * p.img_bytes + static_cast<int64_t>(r0) * p.row_bytes + col * 3;
+  const uint8_t *s = p.src + off;
+  uint8_t *d = p.dst + off;
+  for (int r = r0; r < r1; ++r, s += p.row_bytes, d += p.row_bytes) {
+    const uint32_t v0 = s[0], v1 = s[1], v2 = s[2];
+    const uint32_t v[3] = {v0, v1, v2};
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      float m, a;
-      coef_f32(col, ch, k, p.W, gl, bl, gr, br, m, a);
-      float y = __fadd_rn(__fmul_rn(static_cast<float>(p.src[off + ch]), m), a);
-      y = rintf(y);
-      y = fminf(fmaxf(y, 0.0f), 255.0f);
-      p.dst[off + ch] = static_cast<uint8_t>(y);
+      float y = __fadd_rn(__fmul_rn(static_cast<float>(v[ch]), m[ch]), a[ch]);
+      y = fminf(fmaxf(rintf(y), 0.0f), 255.0f);
+      d[ch] = static_cast<uint8_t>(y);
     }
   }
 }
@@ -515,12 +528,26 @@ static int launch_apply(ApplyParams &p, cudaStream_t stream) {
     if (p.rows_per_split <= 48) return launch_tma<kTmaRows, kTmaStages, 7>(p, stream);
     return launch_tma<>(p, stream);
   }
-  const int64_t npx = static_cast<int64_t>(p.n_img) * p.H * p.W;
-  int64_t blocks = (npx + 255) / 256;
-  const int64_t cap = static_cast<int64_t>(sm_count()) * 16;
-  if (blocks > cap) blocks = cap;
-  apply_generic_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(p);
-  return launch_status();
+  // unaligned rows: column-per-thread kernel, rows split until the grid has
+  // ~8 CTAs per SM
+  const int max_rows = p.H - (p.K - 1) * p.bh;
+  const int64_t gx = (p.W + kColThreads - 1) / kColThreads;
+  const int64_t base = static_cast<int64_t>(p.n_img) * p.K * gx;
+  int splits = 1;
+  while (base * splits < static_cast<int64_t>(sm_count()) * 8 &&
+         (max_rows + splits) / (splits + 1) >= 8)
+    ++splits;
+  p.row_splits = splits;
+  p.rows_per_split = (max_rows + splits - 1) / splits;
+  for (int64_t i0 = 0; i0 < p.n_img; i0 += 65535) {  // images ride on gridDim.z
+    const int64_t n = std::min<int64_t>(65535, p.n_img - i0);
+    const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(p.K * splits),
+                    static_cast<unsigned>(n));
+    apply_cols_kernel<<<grid, kColThreads, 0, stream>>>(p, i0);
+    const int st = launch_status();
+    if (st != CAMX_OK) return st;
+  }
+  return CAMX_OK;
 }
 
 }  // namespace camx
