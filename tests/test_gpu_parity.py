@@ -792,7 +792,7 @@ def test_window_counts_on_a_camera_shard():
     np.testing.assert_array_equal(total, want)
 
 
-@pytest.mark.parametrize("W", [100, 128])  # 3W % 16 == 0: the band-staged shard kernel
+@pytest.mark.parametrize("W", [100, 128])  # 3W % 16 == 0: the TMA-staged kernel (+ halo); else the gather
 @pytest.mark.parametrize("world,n_cams,size,out", [(2, 4, 96, 40), (3, 5, 96, 96), (4, 8, 150, 64),
                                                    (3, 6, 120, 77)])
 def test_tiles_on_camera_shards_sum_to_array_tiles(world, n_cams, size, out, W):
