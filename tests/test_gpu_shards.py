@@ -280,3 +280,52 @@ def test_two_process_gloo_sharded_path_on_gpu():
         assert all(ok), (rank, ok)
     homed = sorted(i for _, _, ids, _ in res for i in ids)
     assert homed == list(range(res[0][3]))
+
+
+def _nccl_one_rank_worker(port, q):
+    """One process, torch.distributed over NCCL with world 1: dist.NcclComm
+    (the unique id broadcast over NCCL, camx_comm_init) and the sharded entry
+    points with a real one-rank NCCL all-gather, against ArrayCorrector."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_1910_03517_b200.dist import NcclComm
+        N, H, W, K, B = 4, 96, 160, 4, 3
+        cfg = xp.ExposureConfig(band_width=16, blocks=K)
+        frames = np.stack([O.synthetic_array(N, H, W, seed=31, objects=2, frame_index=t)
+                           for t in range(2 * B)])
+        d = torch.from_numpy(frames).cuda()
+        ok = []
+        comm = NcclComm()
+        for mode in MODES:
+            want = whole_array(d, [(0, B), (B, 2 * B)], N, H, W, cfg, mode, False)
+            ac = ArrayCorrector(N, H, W, cfg, mode, histograms=True, cam_begin=0, cam_count=N,
+                                comm=comm)
+            got = [keep(ac.correct(d[lo:hi].contiguous())) for lo, hi in ((0, B), (B, 2 * B))]
+            ap = ArrayCorrector(N, H, W, cfg, mode, histograms=True, cam_begin=0, cam_count=N,
+                                comm=comm)
+            piped = [ap.submit(d[:B].contiguous())]
+            piped = [keep(ap.submit(d[B:].contiguous())), keep(ap.flush())]
+            for g, w in list(zip(got, want)) + list(zip(piped, want)):
+                ok.append(all(torch.equal(g[k], w[k]) for k in
+                              ("out", "gain", "offset", "fit_ok", "stats", "hist")))
+        comm.close()
+        torch.cuda.synchronize()
+        q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_comm_one_rank_sharded_entry_points():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_one_rank_worker, args=(_free_port(), q))
+    p.start()
+    ok = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert ok and all(ok), ok
