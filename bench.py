@@ -100,24 +100,32 @@ class ClockSampler:
         except Exception:
             self.nv = None
 
-    def _run(self):
+    def _sample(self):
         nv = self.nv
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            self._stop.wait(0.005)
+            self._sample()
+            self._stop.wait(0.002)
 
     def __enter__(self):
         if self.nv is not None:
             self._th = threading.Thread(target=self._run, daemon=True)
             self._th.start()
         return self
+
+    def mark(self):
+        """One synchronous sample (the GPU is busy with the timed work)."""
+        if self.nv is not None:
+            self._sample()
 
     def __exit__(self, *a):
         self._stop.set()
@@ -387,6 +395,7 @@ class Workload:
                     for _ in range(steps):
                         res = self.step()
                 stop.record(self.stream)
+                clk.mark()  # the queued steps are running: sample under load
                 stop.synchronize()
                 barrier()
         finally:
