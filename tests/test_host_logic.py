@@ -295,3 +295,17 @@ class TestStatsTable:                 # band-statistics export
         text = xp.write_stats_table(rec).splitlines()
         with pytest.raises(ValueError):
             xp.read_stats_table("\n".join(text[:-1]) + "\n")  # a record missing
+
+
+@given(st.lists(st.tuples(st.integers(0, 400), st.integers(0, 400), st.integers(20, 200)),
+                min_size=0, max_size=40),
+       st.integers(1, 8), st.floats(0.0, 1.0))
+def test_merge_with_budget_cut_is_exact(wins, budget, merge_iou):
+    """Scheduler cuts the merged list to its budget with an early exit
+    (_merge_duplicates(..., limit)): identical to merging everything and
+    slicing, as in attention.py:149-186."""
+    reqs = [at.AttentionRequest(DetectorWindow(x, y, s), at.Mechanism.DIFFERENCE, i)
+            for i, (x, y, s) in enumerate(wins)]
+    full = at._merge_duplicates(reqs, merge_iou)[:budget]
+    cut = at._merge_duplicates(reqs, merge_iou, budget)
+    assert [r.priority for r in cut] == [r.priority for r in full]
