@@ -193,3 +193,30 @@ def test_attend_pipeline_matches_sequential_ticks():
         assert [[(r.window.x, r.window.y, r.mechanism) for r in f] for f in g_reqs] == \
                [[(r.window.x, r.window.y, r.mechanism) for r in f] for f in reqs]
         assert torch.equal(g_tiles, tiles)
+
+
+@pytest.mark.parametrize("mode", [xp.ExposureMode.OBJECT_REMOVAL, xp.ExposureMode.SMOOTHING],
+                         ids=lambda m: m.value)
+def test_motion_counts_with_wrap_and_stateful_modes(mode):
+    """The in-pass counts on a 360-degree array (wrap seam) in the stateful
+    modes: counts bit-exact; frames, maps and histograms identical to
+    correct() across two calls (the OBJECT_REMOVAL previous frame and the
+    smoothing state carry exactly as without the counts)."""
+    N, H, W, S = 3, 96, 128, 64
+    frames = moving_batch(4, N, H, W, seed=77)
+    d = torch.from_numpy(frames).cuda()
+    cfg = xp.ExposureConfig(band_width=16, blocks=4)
+    ac = ArrayCorrector(N, H, W, cfg, mode, wrap=True, histograms=True)
+    ref = ArrayCorrector(N, H, W, cfg, mode, wrap=True, histograms=True)
+    c = []
+    for lo, hi in ((0, 2), (2, 4)):
+        got, counts, _ = ac.correct_with_motion(d[lo:hi], size=S)
+        assert ac.last_motion_fused
+        want = ref.correct(d[lo:hi])
+        assert torch.equal(got.out, want.out) and torch.equal(got.gain, want.gain)
+        assert torch.equal(got.offset, want.offset) and torch.equal(got.hist, want.hist)
+        c.append(counts.cpu().numpy())
+    c = np.concatenate(c)
+    for b in range(1, 4):
+        _, want_c = oracle_counts(frames[b - 1], frames[b], S, 20)
+        np.testing.assert_array_equal(c[b], want_c)
