@@ -832,9 +832,19 @@ extern "C" int camx_correct_batch_motion(
                            fit_ok_out, stream);
   if (st != CAMX_OK) return st;
   p.pdl = 1;
-  // 4 stages x 2 rows x (2 KB + 16 B) x 2 frames = 33 KB per CTA, 5 CTAs/SM
-  if (t_motion >= 128) return launch_tma<kTmaRows, 4, 5, true, true>(p, as_stream(stream));
-  return launch_tma<kTmaRows, 4, 5, true, false>(p, as_stream(stream));
+  // 5 stages x 2 rows x (2 KB + 16 B) x 2 frames = 41 KB per CTA, 5 CTAs/SM
+  // (96 registers): 1.12 ms per 30 config-2 frames incl. K1 + K2, vs 1.19 at
+  // 4 stages, 1.26 at 6 x 4 CTAs, 1.23-1.31 at 6 CTAs/SM (80 registers,
+  // spills); profiles/r02/SUMMARY.md.  Build knobs for A/B runs.
+#ifndef CAMX_K3M_STAGES
+#define CAMX_K3M_STAGES 5
+#endif
+#ifndef CAMX_K3M_MINB
+#define CAMX_K3M_MINB 5
+#endif
+  constexpr int kS = CAMX_K3M_STAGES, kB = CAMX_K3M_MINB;
+  if (t_motion >= 128) return launch_tma<kTmaRows, kS, kB, true, true>(p, as_stream(stream));
+  return launch_tma<kTmaRows, kS, kB, true, false>(p, as_stream(stream));
 }
 
 namespace camx {
