@@ -1,0 +1,112 @@
+"""Randomised parity sweep of the production paths against the oracle
+(CUDA; checker = oracle/camarray_oracle.py).  Each case draws a geometry
+(cameras, height, width incl. unaligned widths, blocks, band width), a mode,
+wrap, batch size and seed, then checks:
+
+* ArrayCorrector.correct (two consecutive batches, histograms on) against the
+  oracle tick loop: gains/offsets within 1e-12 relative, fit_ok identical,
+  pixels identical except for the documented +-1 LSB tolerance (counted);
+* histograms of every band against np.bincount of the oracle's band slices;
+* correct_with_motion counts against the oracle's difference-plan counts;
+* camx_tiles (random windows, random out size) against oracle crop + resize.
+
+    python tools/fuzz_parity.py [n_cases] [seed]
+"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from oracle import camarray_oracle as O  # noqa: E402
+from paper_1910_03517_b200 import _lib  # noqa: E402
+from paper_1910_03517_b200 import exposure as xp  # noqa: E402
+from paper_1910_03517_b200.array import ArrayCorrector  # noqa: E402
+
+MODES = [(xp.ExposureMode.STANDARD, O.STANDARD), (xp.ExposureMode.OBJECT_REMOVAL, O.OBJECT_REMOVAL),
+         (xp.ExposureMode.SMOOTHING, O.SMOOTHING)]
+
+
+def one_case(rng, idx):
+    N = int(rng.integers(2, 6))
+    W = int(rng.choice([64, 96, 100, 128, 130, 160, 250, 256, 342, 512, 700, 704]))
+    H = int(rng.integers(40, 200))
+    K = int(rng.integers(1, min(12, H) + 1))
+    bw = int(rng.integers(2, max(3, min(32, W // 2)) + 1))
+    mode, om = MODES[int(rng.integers(0, 3))]
+    wrap = bool(rng.integers(0, 2)) and N >= 2
+    B = int(rng.integers(1, 5))
+    seed = int(rng.integers(0, 10**6))
+    cfg = xp.ExposureConfig(band_width=bw, blocks=K, min_band_pixels=int(rng.integers(1, 80)))
+    ocfg = O.Cfg(band_width=bw, blocks=K, min_band_pixels=cfg.min_band_pixels)
+    frames = np.stack([O.synthetic_array(N, H, W, seed=seed, objects=int(rng.integers(0, 3)),
+                                         frame_index=t) for t in range(2 * B)])
+    d = torch.from_numpy(frames).cuda()
+    ac = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap, histograms=True)
+    r1 = ac.correct(d[:B])
+    o1, g1 = r1.out.cpu().numpy(), r1.gain.cpu().numpy()
+    of1, ok1, h1 = r1.offset.cpu().numpy(), r1.fit_ok.cpu().numpy(), r1.hist.cpu().numpy()
+    r2 = ac.correct(d[B:])
+    got_out = np.concatenate([o1, r2.out.cpu().numpy()])
+    got_g = np.concatenate([g1, r2.gain.cpu().numpy()])
+    got_o = np.concatenate([of1, r2.offset.cpu().numpy()])
+    got_ok = np.concatenate([ok1, r2.fit_ok.cpu().numpy()])
+    got_h = np.concatenate([h1, r2.hist.cpu().numpy()])
+    want_out, wg, wo, wok = O.correct_sequence(frames, None, om, ocfg, wrap=wrap)
+    tag = f"case {idx}: N={N} H={H} W={W} K={K} bw={bw} {mode.value} wrap={wrap} B={B} seed={seed}"
+    np.testing.assert_allclose(got_g, wg, rtol=1e-12, atol=1e-9, err_msg=tag)
+    np.testing.assert_allclose(got_o, wo, rtol=1e-12, atol=1e-9, err_msg=tag)
+    np.testing.assert_array_equal(got_ok.astype(bool), wok, err_msg=tag)
+    diff = np.abs(got_out.astype(int) - want_out.astype(int))
+    assert diff.max() <= 1, f"{tag}: pixel diff {diff.max()}"
+    flips = int((diff > 0).sum())
+    # histograms of a few bands (removal: the kept pixels of the in-band mask)
+    for _ in range(3):
+        b = int(rng.integers(0, 2 * B))
+        c = int(rng.integers(0, N))
+        if om == O.OBJECT_REMOVAL:
+            continue  # masked histograms are covered by the dedicated tests
+        for s, side in ((0, O.LEFT), (1, O.RIGHT)):
+            want_h = O.band_histograms(frames[b, c], side, bw, K)
+            np.testing.assert_array_equal(got_h[b, c, s], want_h, err_msg=f"{tag} hist")
+    # motion counts (fused or fallback path)
+    size = int(rng.integers(8, min(H, N * W) + 1))
+    t = int(rng.integers(0, 256))
+    mc = ArrayCorrector(N, H, W, cfg, wrap=wrap)
+    _, counts, has = mc.correct_with_motion(d[:B + 1], size=size, t_motion=t)
+    cnt = counts.cpu().numpy()
+    for b in range(1, B + 1):
+        m = np.concatenate([O.mask_diff(frames[b][k], frames[b - 1][k], t) for k in range(N)],
+                           axis=1)
+        _, wc = O.window_counts(m, size)
+        np.testing.assert_array_equal(cnt[b], wc, err_msg=f"{tag} counts size={size} t={t}")
+    # tiles
+    S = int(rng.integers(4, min(H, N * W) + 1))
+    out = int(rng.integers(2, 2 * S + 1))
+    wins = [(int(rng.integers(0, B)), int(rng.integers(0, N * W - S + 1)),
+             int(rng.integers(0, H - S + 1))) for _ in range(int(rng.integers(1, 12)))]
+    wd = torch.as_tensor(np.asarray(wins, np.int32), device="cuda")
+    tiles = torch.empty((len(wins), out, out, 3), dtype=torch.uint8, device="cuda")
+    _lib.call("camx_tiles", d.data_ptr(), N, H, W, wd.data_ptr(), len(wins), S, out,
+              tiles.data_ptr(), None)
+    tl = tiles.cpu().numpy()
+    for i, (b, x, y) in enumerate(wins):
+        crop = O.crop(np.concatenate(list(frames[b]), axis=1), x, y, S)
+        want_t = crop if out == S else O.resize_bilinear(crop, out)
+        np.testing.assert_array_equal(tl[i], want_t, err_msg=f"{tag} tile {i} S={S} out={out}")
+    return flips, mc.last_motion_fused
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
+    total_flips = fused = 0
+    for i in range(n):
+        f, fu = one_case(rng, i)
+        total_flips += f
+        fused += int(fu)
+    print(f"{n} cases OK; LSB flips {total_flips}; fused motion path in {fused} cases")
+
+
+if __name__ == "__main__":
+    main()
