@@ -97,6 +97,105 @@ def one_case(rng, idx):
     return flips, mc.last_motion_fused
 
 
+def shard_case(rng, idx):
+    """The camera-sharded native path at world 2..min(N, 4) with the loopback
+    communicator (one thread + stream per rank): every rank's frames, maps,
+    records and histograms byte-identical to the whole-array corrector over
+    two batches (correct and submit/flush alternately); sharded tiles summed
+    over the ranks identical to camx_tiles."""
+    import threading
+    from paper_1910_03517_b200.dist import camera_partition, loopback_comms
+    N = int(rng.integers(2, 7))
+    world = int(rng.integers(2, min(N, 4) + 1))
+    W = int(rng.choice([96, 128, 160, 256, 342]))
+    H = int(rng.integers(48, 160))
+    K = int(rng.integers(1, min(8, H) + 1))
+    bw = int(rng.integers(2, min(24, W // 2) + 1))
+    mode = MODES[int(rng.integers(0, 3))][0]
+    wrap = bool(rng.integers(0, 2))
+    B = int(rng.integers(1, 4))
+    piped = bool(rng.integers(0, 2))
+    seed = int(rng.integers(0, 10**6))
+    cfg = xp.ExposureConfig(band_width=bw, blocks=K)
+    frames = np.stack([O.synthetic_array(N, H, W, seed=seed, objects=2, frame_index=t)
+                       for t in range(2 * B)])
+    d = torch.from_numpy(frames).cuda()
+    tag = (f"shard case {idx}: N={N} world={world} H={H} W={W} K={K} bw={bw} {mode.value} "
+           f"wrap={wrap} B={B} piped={piped} seed={seed}")
+    whole = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap, histograms=True)
+    keys = ("out", "gain", "offset", "fit_ok", "stats", "hist")
+    want = []
+    for lo, hi in ((0, B), (B, 2 * B)):
+        r = whole.correct(d[lo:hi])
+        want.append({k: getattr(r, k).clone() for k in keys})
+    comms = loopback_comms(world)
+    parts = camera_partition(N, world)
+    got, errs = [None] * world, []
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            b0, c = parts[r]
+            ac = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap, histograms=True, cam_begin=b0,
+                                cam_count=c, comm=comms[r])
+            st = torch.cuda.Stream()
+            res = []
+            with torch.cuda.stream(st):
+                locs = [d[lo:hi, b0:b0 + c].contiguous() for lo, hi in ((0, B), (B, 2 * B))]
+                if piped:
+                    ac.submit(locs[0], stream=st)
+                    outs = [ac.submit(locs[1], stream=st), ac.flush(stream=st)]
+                    for o in outs:
+                        res.append({k: getattr(o, k).clone() for k in keys})
+                        st.synchronize()
+                else:
+                    for loc in locs:
+                        o = ac.correct(loc, stream=st)
+                        res.append({k: getattr(o, k).clone() for k in keys})
+            st.synchronize()
+            got[r] = res
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    ths = [threading.Thread(target=rank, args=(r,), daemon=True) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(240)
+    for c in comms:
+        c.close()
+    if errs:
+        raise errs[0]
+    for r, (b0, c) in enumerate(parts):
+        for i in range(2):
+            g, w = got[r][i], want[i]
+            for k in ("gain", "offset", "fit_ok", "stats"):
+                assert torch.equal(g[k], w[k]), f"{tag} rank {r} batch {i} {k}"
+            for k in ("out", "hist"):
+                assert torch.equal(g[k], w[k][:, b0:b0 + c]), f"{tag} rank {r} batch {i} {k}"
+    # sharded tiles: disjoint owned columns summing to the whole-array tiles
+    S = int(rng.integers(4, min(H, N * W) + 1))
+    out = int(rng.integers(2, 2 * S + 1))
+    wins = [(int(rng.integers(0, B)), int(rng.integers(0, N * W - S + 1)),
+             int(rng.integers(0, H - S + 1))) for _ in range(int(rng.integers(1, 10)))]
+    wd = torch.as_tensor(np.asarray(wins, np.int32), device="cuda")
+    full = want[0]["out"]
+    ref = torch.empty((len(wins), out, out, 3), dtype=torch.uint8, device="cuda")
+    _lib.call("camx_tiles", full.data_ptr(), N, H, W, wd.data_ptr(), len(wins), S, out,
+              ref.data_ptr(), None)
+    acc = torch.zeros((len(wins), out, out, 3), dtype=torch.int32, device="cuda")
+    for g, (b0, c) in enumerate(parts):
+        local = full[:, b0:b0 + c].contiguous()
+        halo = full[:, b0 + c, :, 0, :].contiguous() if g + 1 < world else None
+        part = torch.zeros_like(ref)
+        _lib.call("camx_tiles_shard", local.data_ptr(), c, H, W, b0 * W,
+                  0 if halo is None else halo.data_ptr(), wd.data_ptr(), len(wins), S, out,
+                  part.data_ptr(), None)
+        acc += part.to(torch.int32)
+    torch.cuda.synchronize()
+    assert torch.equal(acc.to(torch.uint8), ref), f"{tag} sharded tiles S={S} out={out}"
+
+
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 50
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
@@ -106,6 +205,10 @@ def main():
         total_flips += f
         fused += int(fu)
     print(f"{n} cases OK; LSB flips {total_flips}; fused motion path in {fused} cases")
+    ns = max(1, n // 4)
+    for i in range(ns):
+        shard_case(rng, i)
+    print(f"{ns} camera-shard cases OK (loopback world 2..4, correct and submit/flush, tiles)")
 
 
 if __name__ == "__main__":
