@@ -6,7 +6,8 @@ wrap, batch size and seed, then checks:
 * ArrayCorrector.correct (two consecutive batches, histograms on) against the
   oracle tick loop: gains/offsets within 1e-12 relative, fit_ok identical,
   pixels identical except for the documented +-1 LSB tolerance (counted);
-* histograms of every band against np.bincount of the oracle's band slices;
+* histograms of sampled bands against np.bincount of the oracle's band slices
+  (OBJECT_REMOVAL: of the pixels its in-band mask_diff keeps);
 * correct_with_motion counts against the oracle's difference-plan counts;
 * camx_tiles (random windows, random out size) against oracle crop + resize.
 
@@ -60,15 +61,17 @@ def one_case(rng, idx):
     diff = np.abs(got_out.astype(int) - want_out.astype(int))
     assert diff.max() <= 1, f"{tag}: pixel diff {diff.max()}"
     flips = int((diff > 0).sum())
-    # histograms of a few bands (removal: the kept pixels of the in-band mask)
+    # histograms of a few bands (OBJECT_REMOVAL: the pixels kept by the
+    # in-band mask_diff against the previous array-frame; frame 0 unmasked)
     for _ in range(3):
         b = int(rng.integers(0, 2 * B))
         c = int(rng.integers(0, N))
-        if om == O.OBJECT_REMOVAL:
-            continue  # masked histograms are covered by the dedicated tests
+        mask = None
+        if om == O.OBJECT_REMOVAL and b > 0:
+            mask = O.mask_diff(frames[b, c], frames[b - 1, c], cfg.t_diff)
         for s, side in ((0, O.LEFT), (1, O.RIGHT)):
-            want_h = O.band_histograms(frames[b, c], side, bw, K)
-            np.testing.assert_array_equal(got_h[b, c, s], want_h, err_msg=f"{tag} hist")
+            want_h = O.band_histograms(frames[b, c], side, bw, K, mask)
+            np.testing.assert_array_equal(got_h[b, c, s], want_h, err_msg=f"{tag} hist b={b}")
     # motion counts (fused or fallback path)
     size = int(rng.integers(8, min(H, N * W) + 1))
     t = int(rng.integers(0, 256))
