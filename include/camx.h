@@ -200,11 +200,14 @@ int camx_correct_batch_motion(
     double *gain_out, double *offset_out, uint8_t *fit_ok_out,
     const uint8_t *motion_prev, int32_t win_size, int32_t t_motion,
     int64_t *counts_out, void *stream);
-/* 1 when camx_correct_batch_motion can run this geometry (16-byte aligned
- * rows; every K3 CTA meets <= 3 x 3 windows, e.g. size >= ~700 px at
- * 2048-px frames), else 0 (count with camx_window_counts instead). */
-int camx_motion_supported(int32_t n_batch, int32_t n_cams, int32_t height,
-                          int32_t width, int32_t blocks, int32_t size);
+/* 1 when camx_correct_batch_motion (cam_count = n_cams) or
+ * camx_correct_batch_sharded_motion (this rank's cam_count cameras) can run
+ * this geometry (16-byte aligned rows; every K3 CTA meets <= 3 x 3 windows,
+ * e.g. size >= ~700 px at 2048-px frames), else 0 (count with
+ * camx_window_counts instead). */
+int camx_motion_supported(int32_t n_batch, int32_t n_cams, int32_t cam_count,
+                          int32_t height, int32_t width, int32_t blocks,
+                          int32_t size);
 /* Window grid of the overlap-0 tiling (attention.py:53-86): nx, ny. */
 int camx_tiling_size(int32_t mosaic_w, int32_t mosaic_h, int32_t size,
                      int32_t *nx, int32_t *ny);
@@ -275,6 +278,24 @@ int camx_correct_batch_sharded(const uint8_t *images, uint8_t *out,
  * apply_images == NULL: no back half (first step).  The caller double-buffers
  * the maps / records between consecutive steps.  One pipelined sequence per
  * (device, communicator) at a time. */
+/* camx_correct_batch_sharded with the attention tick's motion counts fused
+ * into this rank's K3 (as camx_correct_batch_motion; n_chunks = 1):
+ * motion_prev = this rank's cameras of the array-frame before frame 0 (may
+ * be NULL).  Each rank counts the pixels of its cameras into its slot of
+ * counts_all [world][n_batch][ny][nx] int64, the slots are all-gathered
+ * through `comm` and summed: counts_out [n_batch][ny][nx] holds the whole
+ * array's counts on every rank. */
+int camx_correct_batch_sharded_motion(
+    const uint8_t *images, uint8_t *out, const uint8_t *prev_frame,
+    int32_t n_batch, int32_t n_cams, int32_t cam_begin, int32_t cam_count,
+    int32_t world, int32_t wrap, int32_t height, int32_t width,
+    int32_t band_width, int32_t t_diff, const camx_solve_config *cfg,
+    const double *prev_gain, const double *prev_offset,
+    camx_band_stat *stats_local, camx_band_stat *stats_all, uint32_t *hist,
+    double *gain_out, double *offset_out, uint8_t *fit_ok_out,
+    const uint8_t *motion_prev, int32_t win_size, int32_t t_motion,
+    int64_t *counts_all, int64_t *counts_out, void *comm, void *stream);
+
 int camx_correct_batch_sharded_step(
     const uint8_t *images, const uint8_t *prev_frame, int32_t n_batch,
     int32_t n_cams, int32_t cam_begin, int32_t cam_count, int32_t world,

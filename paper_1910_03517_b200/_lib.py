@@ -91,7 +91,10 @@ SIGNATURES = {
     "camx_correct_batch_motion": [P, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P,
                                   P, P, P, I32, I32, P, P],
     "camx_tiling_size": [I32, I32, I32, P, P],
-    "camx_motion_supported": [I32, I32, I32, I32, I32, I32],
+    "camx_motion_supported": [I32, I32, I32, I32, I32, I32, I32],
+    "camx_correct_batch_sharded_motion": [P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32,
+                                          I32, P, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P,
+                                          P],
     "camx_seam_cost": [P, P, I64, I32, I32, I32, I32, P, P],
     "camx_blob_components": [P, I32, I32, I32, I32, I32, I32, P, P, I32, P, P],
 }

@@ -239,9 +239,30 @@ class ArrayCorrector:
     def _correct_sharded(self, frames, out, buf, sh, pf):
         """camx_correct_batch_sharded: K1 on this rank's cameras, NCCL
         all-gather of the records, K2 for all seams, K3 (one C call)."""
-        t = _dev.torch()
         cfg = self.cfg
         B = frames.shape[0]
+        world = self.comm.world
+        self._shard_bufs(buf, B)
+        removal = self.mode is ExposureMode.OBJECT_REMOVAL
+        have_prev = self._prev_maps is not None
+        sc = _lib.SolveConfig(_MODE_CODE[self.mode], self.K, int(cfg.min_band_pixels),
+                              float(cfg.sigma_min), float(cfg.alpha),
+                              float(cfg.min_valid_fraction), int(have_prev),
+                              int(removal and pf is not None))
+        pg, po = self._prev_maps if have_prev else (None, None)
+        _lib.call("camx_correct_batch_sharded", frames.data_ptr(), out.data_ptr(),
+                  _dev.ptr(pf) if removal else None, B, self.n_cams, self.cam_begin,
+                  self.cam_count, world, int(self.wrap), self.height, self.width, cfg.band_width,
+                  cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),
+                  buf["stats_local"].data_ptr(), buf["stats_all"].data_ptr(),
+                  _dev.ptr(buf["hist"]), buf["gain"].data_ptr(), buf["offset"].data_ptr(),
+                  buf["fit_ok"].data_ptr(), min(self.shard_chunks(world), B), self.comm.handle,
+                  sh)
+
+    def _shard_bufs(self, buf, B):
+        """Record buffers of the sharded entry points: local records, the
+        rank-major gathered records and their camera-order index."""
+        t = _dev.torch()
         world = self.comm.world
         cmax = -(-self.n_cams // world)
         if "stats_all" not in buf:
@@ -260,21 +281,6 @@ class ArrayCorrector:
                 idx += [world * cmax * lo + (g * (hi - lo) + (b - lo)) * cmax + l
                         for b in range(lo, hi) for g, (_, c) in enumerate(parts) for l in range(c)]
             buf["gather_index"] = t.as_tensor(idx, dtype=t.int64, device="cuda")
-        removal = self.mode is ExposureMode.OBJECT_REMOVAL
-        have_prev = self._prev_maps is not None
-        sc = _lib.SolveConfig(_MODE_CODE[self.mode], self.K, int(cfg.min_band_pixels),
-                              float(cfg.sigma_min), float(cfg.alpha),
-                              float(cfg.min_valid_fraction), int(have_prev),
-                              int(removal and pf is not None))
-        pg, po = self._prev_maps if have_prev else (None, None)
-        _lib.call("camx_correct_batch_sharded", frames.data_ptr(), out.data_ptr(),
-                  _dev.ptr(pf) if removal else None, B, self.n_cams, self.cam_begin,
-                  self.cam_count, world, int(self.wrap), self.height, self.width, cfg.band_width,
-                  cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),
-                  buf["stats_local"].data_ptr(), buf["stats_all"].data_ptr(),
-                  _dev.ptr(buf["hist"]), buf["gain"].data_ptr(), buf["offset"].data_ptr(),
-                  buf["fit_ok"].data_ptr(), min(self.shard_chunks(world), B), self.comm.handle,
-                  sh)
 
     # ------------------------------------------------------------ pipelined stream
     def submit(self, frames, out=None, *, stream=None) -> CorrectResult | None:
@@ -585,19 +591,22 @@ class ArrayCorrector:
         Returns (CorrectResult, counts int64 CUDA tensor (B, n_windows) in
         window_origins order, has_counts list[bool] per frame)."""
         t = _dev.require_cuda()
-        if self.cam_count != self.n_cams or self.S == 0:
-            raise ValueError("motion counts need the whole array (two or more cameras) on one GPU")
+        sharded = self.cam_count != self.n_cams
+        if self.S == 0:
+            raise ValueError("motion counts need an array of two or more cameras")
+        if sharded and self.comm is None:
+            raise ValueError("motion counts on a camera shard go through comm= (dist.NcclComm)")
         if not 0 <= int(t_motion) <= 255:
             raise ValueError("t_motion must be in 0..255")
         if frames.dim() == 4:
             frames = frames[None]
         B, N, H, W, C = frames.shape
-        if (N, H, W, C) != (self.n_cams, self.height, self.width, 3) or frames.dtype != t.uint8:
-            raise ValueError(f"frames must be (B, {self.n_cams}, {self.height}, {self.width}, 3) "
-                             "uint8")
+        if (N, H, W, C) != (self.cam_count, self.height, self.width, 3) or frames.dtype != t.uint8:
+            raise ValueError(f"frames must be (B, {self.cam_count}, {self.height}, {self.width}, "
+                             "3) uint8")
         if not frames.is_cuda or not frames.is_contiguous():
             raise ValueError("frames must be a contiguous CUDA tensor")
-        s = min(int(size), N * W, H)
+        s = min(int(size), self.n_cams * W, H)  # the windows tile the whole mosaic
         origins = self.tile_windows(s)
         if out is None:
             out = t.empty_like(frames)
@@ -618,8 +627,29 @@ class ArrayCorrector:
         pg, po = self._prev_maps if have_prev else (None, None)
         mp = self._motion_prev
         self.last_motion_fused = bool(_lib.load().camx_motion_supported(
-            B, self.n_cams, H, W, self.K, s))
-        if self.last_motion_fused:
+            B, self.n_cams, self.cam_count, H, W, self.K, s))
+        if sharded:
+            # this rank's K3 counts its cameras' pixels; the ranks' counts are
+            # all-gathered through comm and summed (identical on every rank)
+            if not self.last_motion_fused or self.shard_chunks(self.comm.world) != 1:
+                raise ValueError(f"window size {s} is too small for the fused counts on a "
+                                 "camera shard: use dist.sharded_window_counts")
+            self._shard_bufs(buf, B)
+            key = ("counts_all", B, len(origins))
+            call = self._bufs.get(key)
+            if call is None:
+                call = t.empty((self.comm.world, B, len(origins)), dtype=t.int64, device="cuda")
+                self._bufs[key] = call
+            _lib.call("camx_correct_batch_sharded_motion", frames.data_ptr(), out.data_ptr(),
+                      _dev.ptr(pf) if removal else None, B, self.n_cams, self.cam_begin,
+                      self.cam_count, self.comm.world, int(self.wrap), H, W, cfg.band_width,
+                      cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),
+                      buf["stats_local"].data_ptr(), buf["stats_all"].data_ptr(),
+                      _dev.ptr(buf["hist"]), buf["gain"].data_ptr(), buf["offset"].data_ptr(),
+                      buf["fit_ok"].data_ptr(), _dev.ptr(mp), s, int(t_motion), call.data_ptr(),
+                      counts.data_ptr(), self.comm.handle, sh)
+            res = self._finish(frames, out, buf, main, removal)
+        elif self.last_motion_fused:
             _lib.call("camx_correct_batch_motion", frames.data_ptr(), out.data_ptr(),
                       _dev.ptr(pf) if removal else None, B, self.n_cams, int(self.wrap), H, W,
                       cfg.band_width, cfg.t_diff, ctypes.byref(sc), _dev.ptr(pg), _dev.ptr(po),

@@ -787,16 +787,68 @@ static bool motion_fits(const ApplyParams &p, int size) {
   return true;
 }
 
-extern "C" int camx_motion_supported(int32_t n_batch, int32_t n_cams, int32_t height,
-                                     int32_t width, int32_t blocks, int32_t size) {
+// K3 with the motion counts needs 16-byte aligned rows and <= 3 x 3 windows
+// per CTA for this launch's decomposition.
+static bool motion_plan(ApplyParams &p, int size) { return plan_fast(p) && motion_fits(p, size); }
+
+extern "C" int camx_motion_supported(int32_t n_batch, int32_t n_cams, int32_t cam_count,
+                                     int32_t height, int32_t width, int32_t blocks,
+                                     int32_t size) {
   if (n_batch < 1 || n_cams < 2 || height < 1 || width < 1 || blocks < 1 || blocks > height)
     return 0;
+  if (cam_count < 1 || cam_count > n_cams) return 0;
   if (size < 1 || size > n_cams * width || size > height) return 0;
   alignas(16) uint8_t dummy[16];
-  ApplyParams p = array_params(dummy, dummy, n_batch, n_cams, 0, height, width, blocks, nullptr,
-                               nullptr);
-  return plan_fast(p) && motion_fits(p, size) ? 1 : 0;
+  ApplyParams p = array_params(dummy, dummy, n_batch, cam_count, 0, height, width, blocks,
+                               nullptr, nullptr);
+  p.n_cams = n_cams;
+  return motion_plan(p, size) ? 1 : 0;
 }
+
+#ifndef CAMX_K3M_STAGES
+#define CAMX_K3M_STAGES 5
+#endif
+#ifndef CAMX_K3M_MINB
+#define CAMX_K3M_MINB 5
+#endif
+
+namespace camx {
+// Motion fields of p (planned by motion_plan) and the K3 <MOTION> launch:
+// 5 stages x 2 rows x (2 KB + 16 B) x 2 frames = 41 KB per CTA, 5 CTAs/SM
+// (96 registers): 1.12 ms per 30 config-2 frames incl. K1 + K2, vs 1.19 at 4
+// stages, 1.26 at 6 x 4 CTAs, 1.23-1.31 at 6 CTAs/SM (80 registers, spills);
+// profiles/r02/SUMMARY.md.  Counts accumulate (atomics) into `counts`.
+int launch_motion_apply(ApplyParams &p, const uint8_t *motion_prev, int32_t win_size,
+                        int32_t t_motion, int64_t *counts, cudaStream_t stream) {
+  const int32_t mw = p.n_cams * p.W;
+  tiling_axis(mw, win_size, p.nx, p.nx_reg);
+  tiling_axis(p.H, win_size, p.ny, p.ny_reg);
+  p.win = win_size;
+  p.mosaic_w = mw;
+  p.t_motion = t_motion;
+  p.prev_first = motion_prev;
+  p.counts = reinterpret_cast<unsigned long long *>(counts);
+  constexpr int kS = CAMX_K3M_STAGES, kB = CAMX_K3M_MINB;
+  if (t_motion >= 128) return launch_tma<kTmaRows, kS, kB, true, true>(p, stream);
+  return launch_tma<kTmaRows, kS, kB, true, false>(p, stream);
+}
+
+// The sharded K3 with counts (camx_shard.cu): this rank's cameras, counts of
+// its pixels only (the ranks' counts sum to the array's).
+int apply_camera_group_motion(const uint8_t *images, uint8_t *out, int nb, int cam_begin,
+                              int cam_count, int n_cams, int wrap, int height, int width,
+                              int blocks, const double *gain, const double *offset,
+                              const uint8_t *motion_prev, int32_t win_size, int32_t t_motion,
+                              int64_t *counts, cudaStream_t s) {
+  ApplyParams p = array_params(images, out, nb, cam_count, wrap, height, width, blocks, gain,
+                               offset);
+  p.cam_begin = cam_begin;
+  p.n_cams = n_cams;
+  p.S = wrap ? n_cams : n_cams - 1;
+  if (!motion_plan(p, win_size)) return CAMX_EINVAL;
+  return launch_motion_apply(p, motion_prev, win_size, t_motion, counts, s);
+}
+}  // namespace camx
 
 extern "C" int camx_correct_batch_motion(
     const uint8_t *images, uint8_t *out, const uint8_t *prev_frame, int32_t n_batch,
@@ -814,17 +866,13 @@ extern "C" int camx_correct_batch_motion(
   ApplyParams p = array_params(images, out, n_batch, n_cams, wrap, height, width, cfg->blocks,
                                gain_out, offset_out);
   // 16-byte aligned rows and <= 3 x 3 windows per CTA (camx_motion_supported)
-  if (!plan_fast(p) || !motion_fits(p, win_size)) return CAMX_EINVAL;
-  tiling_axis(mw, win_size, p.nx, p.nx_reg);
-  tiling_axis(height, win_size, p.ny, p.ny_reg);
-  p.win = win_size;
-  p.mosaic_w = mw;
-  p.t_motion = t_motion;
-  p.prev_first = motion_prev;
-  p.counts = reinterpret_cast<unsigned long long *>(counts_out);
+  if (!motion_plan(p, win_size)) return CAMX_EINVAL;
+  int nx, nxr, ny, nyr;
+  tiling_axis(mw, win_size, nx, nxr);
+  tiling_axis(height, win_size, ny, nyr);
   // zeroed before K1, so that K2 -> K3 stay programmatically chained
   cudaError_t e = cudaMemsetAsync(counts_out, 0,
-                                  sizeof(int64_t) * static_cast<size_t>(n_batch) * p.nx * p.ny,
+                                  sizeof(int64_t) * static_cast<size_t>(n_batch) * nx * ny,
                                   as_stream(stream));
   if (e != cudaSuccess) return static_cast<int>(e);
   int st = stats_and_solve(images, prev_frame, n_batch, n_cams, wrap, height, width, band_width,
@@ -832,19 +880,7 @@ extern "C" int camx_correct_batch_motion(
                            fit_ok_out, stream);
   if (st != CAMX_OK) return st;
   p.pdl = 1;
-  // 5 stages x 2 rows x (2 KB + 16 B) x 2 frames = 41 KB per CTA, 5 CTAs/SM
-  // (96 registers): 1.12 ms per 30 config-2 frames incl. K1 + K2, vs 1.19 at
-  // 4 stages, 1.26 at 6 x 4 CTAs, 1.23-1.31 at 6 CTAs/SM (80 registers,
-  // spills); profiles/r02/SUMMARY.md.  Build knobs for A/B runs.
-#ifndef CAMX_K3M_STAGES
-#define CAMX_K3M_STAGES 5
-#endif
-#ifndef CAMX_K3M_MINB
-#define CAMX_K3M_MINB 5
-#endif
-  constexpr int kS = CAMX_K3M_STAGES, kB = CAMX_K3M_MINB;
-  if (t_motion >= 128) return launch_tma<kTmaRows, kS, kB, true, true>(p, as_stream(stream));
-  return launch_tma<kTmaRows, kS, kB, true, false>(p, as_stream(stream));
+  return launch_motion_apply(p, motion_prev, win_size, t_motion, counts_out, as_stream(stream));
 }
 
 namespace camx {

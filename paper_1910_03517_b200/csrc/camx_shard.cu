@@ -14,6 +14,8 @@
 #include <mutex>
 #include <utility>
 
+#include <algorithm>
+
 #include "camx_common.cuh"
 
 namespace camx {
@@ -27,6 +29,11 @@ int launch_seam_solve(const camx_band_stat *stats, int32_t n_batch, int32_t n_ca
                       const double *prev_offset, double *gain_out, double *offset_out,
                       uint8_t *fit_ok_out, cudaStream_t stream, bool pdl, int32_t world,
                       int32_t cmax);
+int apply_camera_group_motion(const uint8_t *images, uint8_t *out, int nb, int cam_begin,
+                              int cam_count, int n_cams, int wrap, int height, int width,
+                              int blocks, const double *gain, const double *offset,
+                              const uint8_t *motion_prev, int32_t win_size, int32_t t_motion,
+                              int64_t *counts, cudaStream_t s);
 int apply_camera_group(const uint8_t *images, uint8_t *out, int nb, int cam_begin, int cam_count,
                        int n_cams, int wrap, int height, int width, int blocks,
                        const double *gain, const double *offset, bool pdl, cudaStream_t s);
@@ -205,6 +212,59 @@ extern "C" int camx_correct_batch_sharded(
     if (st != CAMX_OK) return st;
   }
   return CAMX_OK;
+}
+
+// counts_out[i] = sum over ranks of counts_all[w][i]
+__global__ void sum_ranks_kernel(const int64_t *all, int64_t *out, int64_t n, int world) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t v = 0;
+    for (int w = 0; w < world; ++w) v += all[w * n + i];
+    out[i] = v;
+  }
+}
+
+extern "C" int camx_correct_batch_sharded_motion(
+    const uint8_t *images, uint8_t *out, const uint8_t *prev_frame, int32_t n_batch,
+    int32_t n_cams, int32_t cam_begin, int32_t cam_count, int32_t world, int32_t wrap,
+    int32_t height, int32_t width, int32_t band_width, int32_t t_diff, const camx_solve_config *cfg,
+    const double *prev_gain, const double *prev_offset, camx_band_stat *stats_local,
+    camx_band_stat *stats_all, uint32_t *hist, double *gain_out, double *offset_out,
+    uint8_t *fit_ok_out, const uint8_t *motion_prev, int32_t win_size, int32_t t_motion,
+    int64_t *counts_all, int64_t *counts_out, void *comm, void *stream) {
+  if (!images || !out || !stats_local || !stats_all || !gain_out || !offset_out || !fit_ok_out ||
+      !counts_all || !counts_out)
+    return CAMX_EINVAL;
+  if (n_batch < 1 || t_motion < 0 || t_motion > 255) return CAMX_EINVAL;
+  if (win_size < 1 || win_size > n_cams * width || win_size > height) return CAMX_EINVAL;
+  ShardGeom g;
+  int st = shard_geom(g, n_cams, cam_begin, cam_count, world, wrap, height, width, band_width,
+                      t_diff, cfg, prev_gain, prev_offset, comm);
+  if (st != CAMX_OK) return st;
+  int32_t nx = 0, ny = 0;
+  st = camx_tiling_size(n_cams * width, height, win_size, &nx, &ny);
+  if (st != CAMX_OK) return st;
+  const int64_t n = static_cast<int64_t>(n_batch) * nx * ny;
+  int64_t *mine = counts_all + g.rank * n;  // this rank's slot (in-place all-gather)
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(mine, 0, sizeof(int64_t) * n, s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  st = shard_front(g, images, prev_frame, n_batch, cfg, prev_gain, prev_offset, stats_local,
+                   stats_all, hist, gain_out, offset_out, fit_ok_out, comm, s);
+  if (st != CAMX_OK) return st;
+  st = apply_camera_group_motion(images, out, n_batch, g.cam_begin, g.cam_count, g.n_cams,
+                                 g.wrap, g.H, g.W, cfg->blocks, gain_out, offset_out, motion_prev,
+                                 win_size, t_motion, mine, s);
+  if (st != CAMX_OK) return st;
+  if (g.world > 1 || comm != nullptr) {
+    st = comm_all_gather(mine, counts_all, sizeof(int64_t) * n, comm, s);
+    if (st != CAMX_OK) return st;
+  }
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, 1024);
+  sum_ranks_kernel<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), threads, 0, s>>>(
+      counts_all, counts_out, n, g.world);
+  return launch_status();
 }
 
 extern "C" int camx_correct_batch_sharded_step(

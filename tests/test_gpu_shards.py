@@ -329,3 +329,54 @@ def test_nccl_comm_one_rank_sharded_entry_points():
     p.join(timeout=60)
     assert p.exitcode == 0
     assert ok and all(ok), ok
+
+
+@pytest.mark.parametrize("mode", [xp.ExposureMode.STANDARD, xp.ExposureMode.OBJECT_REMOVAL],
+                         ids=lambda m: m.value)
+@pytest.mark.parametrize("N,world,wrap", [(5, 2, False), (6, 3, True), (4, 4, False)])
+def test_sharded_motion_counts_world_gt1(N, world, wrap, mode):
+    """correct_with_motion on camera shards (camx_correct_batch_sharded_motion,
+    loopback communicator): every rank's counts are the whole array's
+    difference-plan counts (the ranks' K3 counts all-gathered and summed),
+    and its frames / maps / histograms equal the whole-array corrector's."""
+    H, W, K, S = 128, 128, 4, 128
+    cfg = xp.ExposureConfig(band_width=16, blocks=K)
+    frames = np.stack([O.synthetic_array(N, H, W, seed=57, objects=3, frame_index=t)
+                       for t in range(5)])
+    d = torch.from_numpy(frames).cuda()
+    batches = [(0, 2), (2, 5)]
+    want = whole_array(d, batches, N, H, W, cfg, mode, wrap)
+    comms = loopback_comms(world)
+    parts = camera_partition(N, world)
+
+    def rank_fn(r):
+        begin, count = parts[r]
+        ac = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap, histograms=True, cam_begin=begin,
+                            cam_count=count, comm=comms[r])
+        s = torch.cuda.Stream()
+        out, cnt, has = [], [], []
+        with torch.cuda.stream(s):
+            for lo, hi in batches:
+                loc = d[lo:hi, begin:begin + count].contiguous()
+                res, c, h = ac.correct_with_motion(loc, size=S, stream=s)
+                assert ac.last_motion_fused
+                out.append(keep(res))
+                cnt.append(c.clone())
+                has += h
+        s.synchronize()
+        return out, torch.cat(cnt).cpu().numpy(), has
+
+    try:
+        got = run_ranks(world, rank_fn)
+    finally:
+        for c in comms:
+            c.close()
+    for r, (begin, count) in enumerate(parts):
+        res, cnt, has = got[r]
+        assert_rank_matches(res, want, begin, count, f"rank {r}/{world}")
+        assert has == [False, True, True, True, True]
+        for b in range(1, 5):
+            m = np.concatenate([O.mask_diff(frames[b][c], frames[b - 1][c], 20)
+                                for c in range(N)], axis=1)
+            _, wc = O.window_counts(m, S)
+            np.testing.assert_array_equal(cnt[b], wc, f"rank {r} frame {b}")
