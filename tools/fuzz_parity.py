@@ -176,6 +176,44 @@ def shard_case(rng, idx):
                 assert torch.equal(g[k], w[k]), f"{tag} rank {r} batch {i} {k}"
             for k in ("out", "hist"):
                 assert torch.equal(g[k], w[k][:, b0:b0 + c]), f"{tag} rank {r} batch {i} {k}"
+    # sharded attention-tick counts (when the geometry takes the fused path)
+    size = int(rng.integers(max(8, min(H, N * W) // 2), min(H, N * W) + 1))
+    tm = int(rng.integers(0, 256))
+    motion = all(_lib.load().camx_motion_supported(B + 1, N, c, H, W, K, size) for _, c in parts)
+    if motion:
+        comms = loopback_comms(world)
+        cnts = [None] * world
+
+        def rank_m(r):
+            try:
+                torch.cuda.set_device(0)
+                b0, c = parts[r]
+                ac = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap, cam_begin=b0, cam_count=c,
+                                    comm=comms[r])
+                st = torch.cuda.Stream()
+                with torch.cuda.stream(st):
+                    _, cc, _ = ac.correct_with_motion(d[:B + 1, b0:b0 + c].contiguous(), size=size,
+                                                      t_motion=tm, stream=st)
+                    cnts[r] = cc.cpu().numpy()
+            except BaseException as e:  # noqa: BLE001
+                errs.append(e)
+
+        ths = [threading.Thread(target=rank_m, args=(r,), daemon=True) for r in range(world)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join(240)
+        for c in comms:
+            c.close()
+        if errs:
+            raise errs[0]
+        for b in range(1, B + 1):
+            m = np.concatenate([O.mask_diff(frames[b][k], frames[b - 1][k], tm) for k in range(N)],
+                               axis=1)
+            _, wc = O.window_counts(m, size)
+            for r in range(world):
+                np.testing.assert_array_equal(cnts[r][b], wc,
+                                              err_msg=f"{tag} rank {r} counts size={size} t={tm}")
     # sharded tiles: disjoint owned columns summing to the whole-array tiles
     S = int(rng.integers(4, min(H, N * W) + 1))
     out = int(rng.integers(2, 2 * S + 1))
@@ -197,6 +235,7 @@ def shard_case(rng, idx):
         acc += part.to(torch.int32)
     torch.cuda.synchronize()
     assert torch.equal(acc.to(torch.uint8), ref), f"{tag} sharded tiles S={S} out={out}"
+    return motion
 
 
 def main():
@@ -209,9 +248,9 @@ def main():
         fused += int(fu)
     print(f"{n} cases OK; LSB flips {total_flips}; fused motion path in {fused} cases")
     ns = max(1, n // 4)
-    for i in range(ns):
-        shard_case(rng, i)
-    print(f"{ns} camera-shard cases OK (loopback world 2..4, correct and submit/flush, tiles)")
+    nm = sum(bool(shard_case(rng, i)) for i in range(ns))
+    print(f"{ns} camera-shard cases OK (loopback world 2..4, correct and submit/flush, tiles; "
+          f"sharded motion counts in {nm})")
 
 
 if __name__ == "__main__":
