@@ -586,7 +586,10 @@ class ArrayCorrector:
         counts of difference_plan(mask_diff(prev, cur, t_motion), size)
         (attention.py:89-103, core.py:191-196).  The previous array-frame
         of frame 0 is the last frame of the previous call (none after
-        reset(): frame 0 then has no counts).
+        reset(): frame 0 then has no counts).  On a camera shard
+        (comm=) each rank's K3 counts its cameras' pixels and the ranks'
+        counts are all-gathered and summed (camx_correct_batch_sharded_motion):
+        every rank returns the whole array's counts.
 
         Returns (CorrectResult, counts int64 CUDA tensor (B, n_windows) in
         window_origins order, has_counts list[bool] per frame)."""
@@ -660,7 +663,9 @@ class ArrayCorrector:
         else:  # geometry outside the fused kernel: correct, then K4 per frame
             res = self.correct(frames, out, stream=stream)
             org = _dev.to_device(np.asarray(origins, dtype=np.int32).reshape(-1, 2))
-            counts.zero_()
+            self._motion_org = org  # alive until the next call (the launches are async)
+            with t.cuda.stream(main):
+                counts.zero_()
             for b in range(B):
                 prev = frames[b - 1] if b > 0 else mp
                 if prev is None:
