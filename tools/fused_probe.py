@@ -1,4 +1,4 @@
-"""Config-5 fused K3+K5 alone (maps given): camx_correct_and_tile over a
+"""Config-5 K3 + K5 alone (maps given; camx_correct_and_tile: K3 then the tile kernel) over a
 config-2 batch with the 36-window sliding plan per array-frame.
 
     python tools/fused_probe.py [B] [reps]      # ms per call, GB/s on algorithmic bytes
