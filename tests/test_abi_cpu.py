@@ -61,6 +61,21 @@ def test_invalid_arguments_are_rejected_before_any_launch(lib):
     g = np.ones(3)
     assert lib.camx_apply_map(rec.ctypes.data, rec.ctypes.data, 1, 4, 4, 7, 1, g.ctypes.data,
                               g.ctypes.data, None) == _lib.CAMX_EINVAL
+    # the round-2 entry points: window grid / support queries and argument checks
+    import ctypes
+    nx, ny = ctypes.c_int32(), ctypes.c_int32()
+    assert lib.camx_tiling_size(16384, 1536, 960, ctypes.byref(nx), ctypes.byref(ny)) == 0
+    assert (nx.value, ny.value) == (18, 2)  # the 36-window config-2 plan
+    assert lib.camx_tiling_size(100, 50, 60, ctypes.byref(nx), ctypes.byref(ny)) == _lib.CAMX_EINVAL
+    assert lib.camx_motion_supported(30, 8, 8, 1536, 2048, 16, 960) == 1
+    assert lib.camx_motion_supported(30, 8, 8, 1536, 2046, 16, 960) == 0  # unaligned rows
+    assert lib.camx_motion_supported(30, 8, 8, 1536, 2048, 16, 64) == 0   # > 3 x 3 per CTA
+    cnt = np.zeros(64, np.int64)
+    sc = _lib.SolveConfig(0, 4, 64, 1e-3, 0.05, 0.5, 0, 0)
+    args = [rec.ctypes.data, rec.ctypes.data, None, 1, 2, 0, 8, 16, 4, 20, ctypes.byref(sc), None,
+            None, rec.ctypes.data, None, rec.ctypes.data, rec.ctypes.data, rec.ctypes.data, None]
+    assert lib.camx_correct_batch_motion(*args, 8, 256, cnt.ctypes.data, None) == _lib.CAMX_EINVAL
+    assert lib.camx_correct_batch_motion(*args, 99, 20, cnt.ctypes.data, None) == _lib.CAMX_EINVAL
     with pytest.raises(ValueError):
         _lib.check(_lib.CAMX_EINVAL, "x")
     with pytest.raises(RuntimeError):
