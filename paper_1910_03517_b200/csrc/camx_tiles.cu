@@ -315,6 +315,9 @@ __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const Til
       }
     }
   };
+  // launched as a programmatic dependent of K3 (config 5): the corrected
+  // frames are complete only past this point (a no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (lane == 0)
     for (int i = 0; i < min(kTmaTileSlots, n_rows); ++i) issue(i);
 
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const Til
 }
 
 static int launch_tiles_tma(const TileParams &p, int32_t n_tiles, cudaStream_t s,
-                            const TileShard &sd) {
+                            const TileShard &sd, bool pdl = false) {
   const int J = (p.out + 31) / 32;
   TmaTileGeom g{};
   g.pitch = tma_tile_pitch(p.size);
@@ -381,8 +384,18 @@ static int launch_tiles_tma(const TileParams &p, int32_t n_tiles, cudaStream_t s
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return static_cast<int>(e);
-    kern<<<grid, kTmaTileWarps * 32, smem, s>>>(p, g, sd);
-    return launch_status();
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(kTmaTileWarps * 32);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    e = cudaLaunchKernelEx(&lc, kern, p, g, sd);
+    return e == cudaSuccess ? launch_status() : static_cast<int>(e);
   };
   if (J <= 2) return go(tiles_tma_kernel<2>);
   if (J <= 4) return go(tiles_tma_kernel<4>);
@@ -623,6 +636,30 @@ extern "C" int camx_tiles(const uint8_t *images, int32_t n_cams, int32_t height,
   }
   return CAMX_OK;
 }
+
+namespace camx {
+// camx_tiles right behind K3 (config 5): the TMA tile kernel as a
+// programmatic dependent, so its prologue overlaps K3's last wave.
+int tiles_after_apply(const uint8_t *images, int32_t n_cams, int32_t height, int32_t width,
+                      const int32_t *windows, int32_t n_tiles, int32_t size, int32_t out_size,
+                      uint8_t *tiles_out, void *stream) {
+  TileParams p{};
+  p.img = images;
+  p.n_cams = n_cams;
+  p.H = height;
+  p.W = width;
+  p.size = size;
+  p.out = out_size;
+  p.wins = windows;
+  p.tiles = tiles_out;
+  p.scale = static_cast<float>(size) / static_cast<float>(out_size);
+  if (out_size == size || n_tiles > 65535 || !tiles_tma_ok(p))
+    return camx_tiles(images, n_cams, height, width, windows, n_tiles, size, out_size, tiles_out,
+                      stream);
+  return launch_tiles_tma(p, n_tiles, as_stream(stream), TileShard{0, n_cams * width, nullptr},
+                          true);
+}
+}  // namespace camx
 
 extern "C" int camx_seam_cost(const uint8_t *left, const uint8_t *right, int64_t n_pairs,
                               int32_t height, int32_t left_width, int32_t right_width,
