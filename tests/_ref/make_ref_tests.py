@@ -4,7 +4,7 @@
     python tests/_ref/make_ref_tests.py        # needs /root/reference (this container)
 
 Copies, byte for byte apart from a provenance comment on top:
-  tests/   conftest.py, test_exposure.py, test_attention.py, test_core.py
+  tests/   conftest.py, test_exposure.py, test_attention.py, test_core.py, test_detect.py
   src/     scenegen.py, world3d.py, tracker.py, imgio.py  -> tests/_ref/camarray/
 The test modules run UNMODIFIED against this repository's package: the
 `camarray` package beside them (tests/_ref/camarray/__init__.py, written by
@@ -31,7 +31,7 @@ from pathlib import Path
 REF = Path("/root/reference/pkg")
 HERE = Path(__file__).resolve().parent
 
-TESTS = ["conftest.py", "test_exposure.py", "test_attention.py", "test_core.py"]
+TESTS = ["conftest.py", "test_exposure.py", "test_attention.py", "test_core.py", "test_detect.py"]
 FIXTURE_SRC = ["scenegen.py", "world3d.py", "tracker.py", "imgio.py"]
 
 

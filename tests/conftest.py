@@ -17,6 +17,10 @@ def pytest_collection_modifyitems(config, items):
     # CUDA path, so they belong to the GPU tier
     import pytest
     ref = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref") + os.sep
+    oracle_skip = pytest.mark.skip(reason="OracleDetector (ground truth from world3d/scenegen) "
+                                          "is out of scope, SURVEY 2")
     for item in items:
         if str(item.fspath).startswith(ref):
             item.add_marker(pytest.mark.gpu)
+            if "TestOracleDetector" in item.nodeid:
+                item.add_marker(oracle_skip)
