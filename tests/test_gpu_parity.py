@@ -1215,3 +1215,33 @@ def test_stats_table_export_of_a_corrected_batch():
                 r = rec[b, c, s]
                 np.testing.assert_array_equal(r["valid"], valid)
                 np.testing.assert_allclose(r["sum"] / r["valid"][:, None], m, rtol=1e-14)
+
+
+@pytest.mark.parametrize("wrap", [False, True])
+def test_checkpoint_resume_through_the_maps_table(wrap):
+    """Checkpoint / resume of a stateful stream (SMOOTHING): two batches,
+    the last array-frame's maps written as the reference's text table
+    (write_maps_table, exposure.py:448-493), read back into a fresh
+    corrector (set_prev_maps), two more batches - frames and maps identical
+    to the uninterrupted stream."""
+    N, H, W = 4, 96, 128
+    cfg = xp.ExposureConfig(band_width=16, blocks=4)
+    mode = xp.ExposureMode.SMOOTHING
+    frames = np.stack([O.synthetic_array(N, H, W, seed=303, objects=2, frame_index=t)
+                       for t in range(8)])
+    d = torch.from_numpy(frames).cuda()
+    batches = [(0, 2), (2, 4), (4, 6), (6, 8)]
+    full = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap)
+    want = []
+    for lo, hi in batches:
+        r = full.correct(d[lo:hi])
+        want.append((r.out.clone(), r.gain.clone()))
+    first = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap)
+    for lo, hi in batches[:2]:
+        r = first.correct(d[lo:hi])
+    text = xp.write_maps_table(first.maps(r))  # the checkpoint
+    resumed = ArrayCorrector(N, H, W, cfg, mode, wrap=wrap)
+    resumed.set_prev_maps(xp.read_maps_table(text))
+    for (lo, hi), (w_out, w_gain) in zip(batches[2:], want[2:]):
+        r = resumed.correct(d[lo:hi])
+        assert torch.equal(r.out, w_out) and torch.equal(r.gain, w_gain)
