@@ -717,7 +717,7 @@ def run_camx(args):
     # rooflined the same way (same steps / warm-up, own clocks)
     secondary = []
     if world == 1 and args.workload is None and not args.no_secondary:
-        for nm in ("config4", "config5", "config5m"):
+        for nm in ("config5", "config5m", "config4"):  # the long, hot 4K run last
             w2 = Workload(nm, WORKLOADS[nm][3], args, world, rank, torch).run(
                 args.steps, args.warmup, barrier)
             w2.roofline_leg(max(3, min(args.steps, 20)))
