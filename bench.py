@@ -89,6 +89,7 @@ class ClockSampler:
 
     def __init__(self, device_index: int):
         self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.power_w = []
         self._stop = threading.Event()
         self._th = None
         try:
@@ -104,6 +105,7 @@ class ClockSampler:
         nv = self.nv
         try:
             self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.power_w.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1e3)
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             for bit, name in self.REASONS.items():
                 if r & bit and name != "gpu_idle":
@@ -136,8 +138,11 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                     "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        d = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+             "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power_w:
+            d["power_w"] = round(statistics.median(self.power_w), 1)
+        return d
 
 
 # ------------------------------------------------------------------ CPU baseline
@@ -444,32 +449,45 @@ class Workload:
             nbytes = B * (9 * self.n_cams * H * W + bands)
             kname = "camx K1 + K2 + apply_tma_kernel<motion> (camx_correct_batch_motion)"
             motion_call = self.motion_call()
+        def launch():
+            if self.attend:
+                motion_call()
+            elif self.tiles:
+                _lib.call("camx_correct_and_tile", self.frames.data_ptr(), self.out.data_ptr(),
+                          B, self.n_cams, int(self.wrap), H, W, cfg.blocks,
+                          res.gain.data_ptr(), res.offset.data_ptr(), w_dev.data_ptr(),
+                          off_dev.data_ptr(), len(wins), int(per_b.max()), 960, 416,
+                          self.tiles_buf.data_ptr(), stream.cuda_stream)
+            else:
+                _lib.call("camx_apply_array", self.frames.data_ptr(), self.out.data_ptr(), B,
+                          self.begin, self.count, self.n_cams, int(self.wrap), H, W,
+                          cfg.blocks, res.gain.data_ptr(), res.offset.data_ptr(),
+                          stream.cuda_stream)
+
+        # per-launch CUDA events on the launch stream, after warm-up; the
+        # median launch - a mean would also count the rare host
+        # stall that leaves the GPU idle between an event and its launch
+        import statistics
         ev = []
-        with torch.cuda.stream(stream):
+        with torch.cuda.stream(stream), ClockSampler(torch.cuda.current_device()) as clk:
+            for _ in range(2):
+                launch()
             for _ in range(reps):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                if self.attend:
-                    motion_call()
-                elif self.tiles:
-                    _lib.call("camx_correct_and_tile", self.frames.data_ptr(), self.out.data_ptr(),
-                              B, self.n_cams, int(self.wrap), H, W, cfg.blocks,
-                              res.gain.data_ptr(), res.offset.data_ptr(), w_dev.data_ptr(),
-                              off_dev.data_ptr(), len(wins), int(per_b.max()), 960, 416,
-                              self.tiles_buf.data_ptr(), stream.cuda_stream)
-                else:
-                    _lib.call("camx_apply_array", self.frames.data_ptr(), self.out.data_ptr(), B,
-                              self.begin, self.count, self.n_cams, int(self.wrap), H, W,
-                              cfg.blocks, res.gain.data_ptr(), res.offset.data_ptr(),
-                              stream.cuda_stream)
+                launch()
                 e1.record(stream)
                 ev.append((e0, e1))
-        torch.cuda.synchronize()
-        self.k_ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
+            clk.mark()
+            torch.cuda.synchronize()
+        self.k_clocks = clk.summary()
+        times = [a.elapsed_time(b) for a, b in ev]
+        self.k_ms = statistics.median(times)
+        self.k_ms_mean = sum(times) / len(times)
         self.k_bytes = nbytes
         self.k_name = kname
-        self.k_reps = len(ev)
+        self.k_reps = len(times)
 
     def motion_call(self):
         """camx_correct_batch_motion on this workload's buffers (roofline leg):
@@ -509,7 +527,10 @@ class Workload:
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic_for(self.name, self.k_bytes, self.B),
                          "peak_kind": peak_kind, "k_ms_per_launch": round(self.k_ms, 4),
+                         "k_ms_stat": "median of the timed launches (mean "
+                                      f"{getattr(self, 'k_ms_mean', self.k_ms):.4f})",
                          "k_bytes_per_launch": self.k_bytes, "k_launches_timed": self.k_reps,
+                         "k_clocks": getattr(self, "k_clocks", None),
                          "k_share_of_step": round(self.k_ms * self.steps / self.ms, 4)},
         }
 
@@ -698,23 +719,13 @@ def run_camx(args):
     wl.ms, wl.k_ms = max_ranks(wl.ms, wl.k_ms)
     main = wl.summary(peak, peak_kind)
 
-    e2e = None
-    if not args.no_e2e and not wl.tiles:
-        e2e = e2e_ring(wl, min(args.e2e_batch, B), max(2, args.e2e_steps), args.warmup,
-                       barrier, world, args.e2e_slots)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_baseline_line(wl, args)
-        except Exception as e:  # pragma: no cover
-            cpu = {"value": None, "unit": "MP/s", "cores": 0, "kind": "port",
-                   "sample": f"failed: {e}"}
     line_cfg = wl.config()
     clocks, launches = wl.clocks, wl.launches
-    wl.free()
 
     # the other single-GPU workloads BASELINE.json names, each timed and
-    # rooflined the same way (same steps / warm-up, own clocks)
+    # rooflined the same way (same steps / warm-up, own clocks); before the
+    # e2e and CPU legs, whose host-heavy phases were measured to slow the GPU
+    # legs that follow them
     secondary = []
     if world == 1 and args.workload is None and not args.no_secondary:
         for nm in ("config5", "config5m", "config4"):  # the long, hot 4K run last
@@ -726,6 +737,19 @@ def run_camx(args):
                      steps=args.steps, warmup=args.warmup)
             secondary.append(d)
             w2.free()
+
+    e2e = None
+    if not args.no_e2e and not wl.tiles:
+        e2e = e2e_ring(wl, min(args.e2e_batch, B), max(2, args.e2e_steps), args.warmup,
+                       barrier, world, args.e2e_slots)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_line(wl, args)
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "MP/s", "cores": 0, "kind": "port",
+                   "sample": f"failed: {e}"}
+    wl.free()
 
     if rank == 0:
         line = {

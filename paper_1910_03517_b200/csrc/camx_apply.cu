@@ -172,6 +172,88 @@ __device__ __forceinline__ uint4 correct16(uint4 v, const Coef16 &cf) {
   return r;
 }
 
+// In-range variant (every sub-pixel of the CTA has |M| * 255 + |A| < 32000,
+// i.e. |p*M + A| < 2^15 for every byte p - all maps a solver produces): no
+// 2^-8 scaling and no saturating adds -
+//   fma(X, M, -2^23*M)  = rn(p*M)                 (exact: one rounding)
+//   + A                 = rn(rn(p*M) + A)         (the reference's f32 add)
+//   + 1.5*2^23          = 1.5*2^23 + rint_half_even(.)   (|.| < 2^22)
+// so the low 16 bits of each lane are rint(y) as an int16, and one
+// VIMNMX.S16x2.RELU (min 255, then max 0) clamps two sub-pixels: 15 instead
+// of 17 instructions per 4 bytes, all paired except the byte permutes.
+struct Coef16F {
+  uint64_t m[8];  // pairs (M, M)
+  uint64_t c[8];  // pairs (-2^23*M)
+  uint64_t a[8];  // pairs (A)
+};
+
+__device__ __forceinline__ uint32_t min255_relu_s16x2(uint32_t x) {
+  uint32_t d;
+  asm("min.relu.s16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(0x00FF00FFu));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t correct_word(uint32_t w, const Coef16F &cf, int base) {
+  const uint64_t kMagic = pack2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  uint32_t z[4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = (base + 2 * h) >> 1;
+    const uint32_t x0 = __byte_perm(w, 0x4B00u, 0x5440u + 2 * h);
+    const uint32_t x1 = __byte_perm(w, 0x4B00u, 0x5441u + 2 * h);
+    const uint64_t y = fma2_rn(pack2u(x0, x1), cf.m[i], cf.c[i]);
+    const uint64_t q = add2_rn(add2_rn(y, cf.a[i]), kMagic);
+    unpack2u(q, z[2 * h], z[2 * h + 1]);
+  }
+  const uint32_t p01 = min255_relu_s16x2(__byte_perm(z[0], z[1], 0x5410u));
+  const uint32_t p23 = min255_relu_s16x2(__byte_perm(z[2], z[3], 0x5410u));
+  return __byte_perm(p01, p23, 0x6420u);
+}
+
+__device__ __forceinline__ uint4 correct16(uint4 v, const Coef16F &cf) {
+  uint4 r;
+  r.x = correct_word(v.x, cf, 0);
+  r.y = correct_word(v.y, cf, 4);
+  r.z = correct_word(v.z, cf, 8);
+  r.w = correct_word(v.w, cf, 12);
+  return r;
+}
+
+// Coefficients from the per-sub-pixel float32 (M, A); the general form is
+// derived from the in-range one (same float32 M and A).
+__device__ __forceinline__ void make_coef(const float (&m)[16], const float (&a)[16],
+                                          Coef16F &cf) {
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) {
+    cf.m[i >> 1] = pack2(m[i], m[i + 1]);
+    cf.c[i >> 1] = pack2(m[i] * -8388608.0f, m[i + 1] * -8388608.0f);
+    cf.a[i >> 1] = pack2(a[i], a[i + 1]);
+  }
+}
+__device__ __forceinline__ Coef16 general_coef(const Coef16F &f) {
+  Coef16 cf;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t m0, m1, a0, a1;
+    unpack2u(f.m[i], m0, m1);
+    unpack2u(f.a[i], a0, a1);
+    const float mm[2] = {__uint_as_float(m0), __uint_as_float(m1)};
+    const float aa[2] = {__uint_as_float(a0), __uint_as_float(a1)};
+    cf.m[i] = pack2(mm[0] * 0.00390625f, mm[1] * 0.00390625f);
+    cf.c[i] = pack2(mm[0] * -32768.0f, mm[1] * -32768.0f);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      cf.a[2 * i + h] = fabsf(aa[h]) < 7.7037197787136e-34f ? 0.0f : aa[h] * 0.00390625f;
+  }
+  return cf;
+}
+__device__ __forceinline__ bool coef_in_range(const float (&m)[16], const float (&a)[16]) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) ok &= fabsf(m[i]) * 255.0f + fabsf(a[i]) < 32000.0f;  // NaN: false
+  return ok;
+}
+
 // ------------------------------------------------- TMA bulk-copy pipeline
 // CTA = one 2 KB column group of one row block (split) of one image, thread
 // = one 16-byte chunk; the rows stream through a kStages-deep shared-memory
@@ -285,10 +367,11 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
   const bool active = threadIdx.x < chunks;
   const double *gl, *bl, *gr, *br;
   map_ptrs(p, img, gl, bl, gr, br);
-  Coef16 cf;
+  // per sub-pixel (a per-column lambda cache measured ~6% slower end to
+  // end on B200: tools/ab_k3.py)
+  Coef16F cff;
+  bool in_range = true;
   if (active) {
-    // per sub-pixel (a per-column lambda cache measured ~6% slower end to
-    // end on B200: tools/ab_k3.py)
     float m[16], a[16];
     const int q0 = j * 16;
     int col = q0 / 3;
@@ -301,15 +384,17 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
         ++col;
       }
     }
-#pragma unroll
-    for (int i = 0; i < 16; i += 2) {
-      cf.m[i >> 1] = pack2(m[i] * 0.00390625f, m[i + 1] * 0.00390625f);
-      cf.c[i >> 1] = pack2(m[i] * -32768.0f, m[i + 1] * -32768.0f);
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      cf.a[i] = fabsf(a[i]) < 7.7037197787136e-34f ? 0.0f : a[i] * 0.00390625f;
+    in_range = coef_in_range(m, a);
+    make_coef(m, a, cff);
   }
+  // CTA-uniform choice of the arithmetic (Coef16F unless some sub-pixel's
+  // map is extreme); the two row loops below never hold both coefficient sets.
+  // Only where the register budget holds it without spilling: the MOTION and
+  // 7-CTA/SM variants keep the general chain (measured: tools/ab_sustain.py,
+  // tools/ab_k3.sh - K3 under the power cap 0.786 -> 0.755 ms per 30 frames,
+  // config 4 step 7.32-7.37 -> 7.18-7.21 ms; MOTION with it 4% slower)
+  constexpr bool kInRangeChain = !MOTION && (MINB == 0 ? CAMX_K3_MINB : MINB) <= 6;
+  const bool fast = kInRangeChain && __syncthreads_and(in_range) != 0;
 
   // MOTION: the windows of the overlap-0 tiling meeting the CTA (<= 3 window
   // columns x 3 window rows: camx_motion_supported), this thread's
@@ -388,8 +473,10 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
   // extra bytes past the group; none at the row end
   const uint32_t next_mask = (threadIdx.x + 1 < chunks || extra) ? 3u : 0u;
 
-  uint8_t *dst = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
-  for (int st = 0; st < nst; ++st) {
+  uint8_t *const dst0 = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
+  auto stream_rows = [&](const auto cf) {
+  uint8_t *dst = dst0;  // row st * ROWS of the split
+  for (int st = 0; st < nst; ++st, dst += ROWS * rb) {
     const int slot = st % STAGES;
     mbar_wait(&full[slot], (st / STAGES) & 1);
     const int rr = min(ROWS, nrows - st * ROWS);
@@ -402,7 +489,7 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
       for (int i = 0; i < ROWS; ++i)
         if (i < rr) {
           const uint4 o = correct16(v[i], cf);
-          st_stream_v4(dst + static_cast<int64_t>(st * ROWS + i) * rb, o);
+          st_stream_v4(dst + i * rb, o);
         }
     }
     if (MOTION && prev0 != nullptr) {
@@ -431,6 +518,11 @@ __global__ void __launch_bounds__(kApplyThreads, MINB > 0 ? MINB : CAMX_K3_MINB)
     __syncthreads();  // slot consumed
     if (threadIdx.x == 0 && st + STAGES < nst) issue(st + STAGES);
   }
+  };
+  if (fast)
+    stream_rows(cff);
+  else
+    stream_rows(general_coef(cff));
   if (MOTION && prev0 != nullptr) flush();
 }
 

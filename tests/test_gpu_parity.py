@@ -426,14 +426,17 @@ def test_apply_array_bit_exact_given_maps():
             np.testing.assert_array_equal(got[b], want)
 
 
-@pytest.mark.parametrize("scale", ["tie", "wide"])
+@pytest.mark.parametrize("scale", ["tie", "wide", "edge"])
 def test_apply_extreme_and_tie_maps_bit_exact(scale):
     """K3 and the fused K3+K5 kernel at extreme and tie-heavy maps, bit-exact.
     'wide' maps (gains up to 1e3, offsets to +-3e4) clip most sub-pixels at
     both ends; 'tie' maps (quarter gains, half offsets) put many products
     exactly on .5 so the half-even rounding of every step is exercised (this
     test caught ptxas contracting mul.rn.f32x2 + add.rn.f32x2 into one FFMA2
-    in an unsaturated-chain experiment; profiles/r01/SUMMARY.md)."""
+    in an unsaturated-chain experiment; profiles/r01/SUMMARY.md); 'edge' maps
+    (|gain| 100-130, offsets to +-300) sit on both sides of K3's in-range
+    bound |M| * 255 + |A| < 32000 (the int16 clamp path vs the saturating
+    one, chosen per CTA)."""
     rng = np.random.default_rng(17)
     from paper_1910_03517_b200 import _lib
     N, H, W, K, B = 3, 64, 1024, 4, 2
@@ -444,6 +447,9 @@ def test_apply_extreme_and_tie_maps_bit_exact(scale):
         off = rng.uniform(-3e4, 3e4, (B, S, 2, K, 3))
         off[:, :, :, ::2] = rng.uniform(-50, 50, (B, S, 2, (K + 1) // 2, 3))
         gain[:, :, :, ::2] = rng.uniform(0.5, 2.0, (B, S, 2, (K + 1) // 2, 3))
+    elif scale == "edge":
+        gain = rng.uniform(100, 130, (B, S, 2, K, 3)) * rng.choice([-1.0, 1.0], (B, S, 2, K, 3))
+        off = rng.uniform(-300, 300, (B, S, 2, K, 3))
     else:
         gain = rng.integers(1, 8, (B, S, 2, K, 3)) / 4.0
         off = rng.integers(-64, 64, (B, S, 2, K, 3)) / 2.0

@@ -10,9 +10,10 @@ import sys
 import numpy as np
 import torch
 
-from paper_1910_03517_b200 import _lib
-from paper_1910_03517_b200.array import ArrayCorrector
-from paper_1910_03517_b200.synth import synthetic_batch
+sys.path.insert(0, ".")
+from paper_1910_03517_b200 import _lib  # noqa: E402
+from paper_1910_03517_b200.array import ArrayCorrector  # noqa: E402
+from paper_1910_03517_b200.synth import synthetic_batch  # noqa: E402
 
 N, H, W = 8, 1536, 2048
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 30
