@@ -614,408 +614,6 @@ static int launch_tma(const ApplyParams &p, cudaStream_t stream) {
   return e == cudaSuccess ? launch_status() : static_cast<int>(e);
 }
 
-// ------------------------------------------------ config 5 in one pass (K3 + K5)
-// apply_tiles_kernel: K3's CTA (one 2 KB column group of one row block of one
-// image) also cuts the detector tiles from the rows it has just corrected, so
-// each frame makes one HBM round trip (north_star; the two-pass K3 -> K5 path
-// re-reads the tiles' tap rows).  Ownership: output pixel (t, oy, ox) is
-// computed by the CTA holding the first byte of its first tap pixel (mosaic
-// column x0 + j0(ox)) in the row of its first tap (y0 + i0(oy)).  Its other
-// taps are the next pixel - at most 5 bytes past the group: the CTA also stages
-// the next 16-byte chunk (of the same row, or of the next camera's row for a
-// camera's last group) and 16 lanes of warp 3 correct it byte-wise - and the
-// next row: for the CTA's last row that is the first row of the next CTA,
-// staged as one more stage and corrected with its own block's maps (not
-// stored).  Corrected rows are written back into the ring and a slot is
-// refilled one stage late, so both tap rows of an output row are resident when
-// its second tap row lands.  Per CTA a schedule of (window, output row)
-// entries, counting-sorted by the stage of their second tap row, is built
-// once; per stage each warp takes every 4th due entry and resamples the row's
-// owned column range, lane l producing columns ox_lo + l + 32 m with the
-// camx_resize.cuh arithmetic (bit-identical to tiles_tma_kernel).
-constexpr int kOpStages = 6;
-constexpr int kOpRows = 2;
-constexpr int kOpRB = kApplyThreads * 16 + 32;  // ring row: group + halo chunk + slack
-
-struct OnePassParams {
-  ApplyParams a;
-  const int32_t *wins;       // [n][3] (b, x, y), grouped by array-frame
-  const int32_t *frame_off;  // [B + 1]
-  uint8_t *tiles;
-  int32_t size, out;
-  float scale;
-  int32_t win_cap;    // windows of one frame (smem list capacity)
-  int32_t ent_cap;    // schedule entries of one CTA
-  int32_t stage_cap;  // stages of one CTA (+ the halo stage)
-};
-
-struct OpWin {  // a window meeting the CTA
-  int32_t base;   // ring-row byte offset of the window's tap pixel j0 = 0: 3 (x0 - cam W) - G0
-  int32_t t;      // tile index
-  int32_t y0;
-  int16_t ox_lo, ox_hi, oy_lo, oy_hi;  // owned output columns / rows
-};
-
-__device__ __forceinline__ int op_lower_bound(const uint2 *tab, int n, int v) {
-  int lo = 0, hi = n;  // first o with tab[o].x >= v (tab[].x nondecreasing)
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (static_cast<int>(tab[mid].x) >= v) hi = mid; else lo = mid + 1;
-  }
-  return lo;
-}
-
-// Exact float32 (M, A) of one sub-pixel (column col of image img, block kk).
-__device__ __forceinline__ void op_coef(const ApplyParams &p, int64_t img, int col, int ch,
-                                        int kk, float &m, float &a) {
-  const double *gl, *bl, *gr, *br;
-  map_ptrs(p, img, gl, bl, gr, br);
-  coef_f32(col, ch, kk, p.W, gl, bl, gr, br, m, a);
-}
-
-__device__ __forceinline__ uint8_t op_correct_byte(uint32_t v, float m, float a) {
-  float y = __fadd_rn(__fmul_rn(static_cast<float>(v), m), a);
-  y = fminf(fmaxf(rintf(y), 0.0f), 255.0f);
-  return static_cast<uint8_t>(y);
-}
-
-template <int MINB>
-__global__ void __launch_bounds__(kApplyThreads, MINB) apply_tiles_kernel(const OnePassParams q) {
-  const ApplyParams &p = q.a;
-  extern __shared__ __align__(128) uint8_t op_sm[];
-  uint8_t *ring = op_sm;  // [kOpStages][kOpRows][kOpRB]
-  uint2 *tab = reinterpret_cast<uint2 *>(op_sm + kOpStages * kOpRows * kOpRB);  // [out]
-  OpWin *wl = reinterpret_cast<OpWin *>(tab + q.out);                           // [win_cap]
-  uint2 *ent = reinterpret_cast<uint2 *>(wl + q.win_cap);                       // [ent_cap]
-  int *scnt = reinterpret_cast<int *>(ent + q.ent_cap);                         // [stage_cap]
-  __shared__ __align__(8) uint64_t full[kOpStages];
-  __shared__ int n_win;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  int64_t item = blockIdx.x;
-  const int cg = static_cast<int>(item % p.col_groups);
-  item /= p.col_groups;
-  const int rs = static_cast<int>(item % p.row_splits);
-  item /= p.row_splits;
-  const int k = static_cast<int>(item % p.K);
-  const int64_t img = item / p.K;
-  const int blk_r0 = k * p.bh;
-  const int blk_r1 = (k == p.K - 1) ? p.H : blk_r0 + p.bh;
-  const int r0 = blk_r0 + rs * p.rows_per_split;
-  const int r1 = min(blk_r1, r0 + p.rows_per_split);
-  if (r0 >= r1) return;  // CTA-uniform
-  const int chunks = min(kApplyThreads, p.chunks_per_row - cg * kApplyThreads);
-  const uint32_t seg = static_cast<uint32_t>(chunks) * 16u;
-  const int j = cg * kApplyThreads + tid;
-  const int64_t rb = p.row_bytes;
-  const int G0 = cg * kApplyThreads * 16;
-  const int64_t b = img / p.cam_count;
-  const int cam = static_cast<int>(img - b * p.cam_count);
-  const uint8_t *src_img = p.src + img * p.img_bytes;
-  const int nrows = r1 - r0;
-  const int nst_own = (nrows + kOpRows - 1) / kOpRows;
-  const bool hrow = r1 < p.H;  // the next CTA's first row (second taps of the last row)
-  const int nst = nst_own + (hrow ? 1 : 0);
-  // halo chunk: the 16 bytes after the group (same row), or the next camera's
-  // first 16 bytes for a camera's last group; none past the mosaic's end
-  int64_t halo_off = -1;  // from the image base + R * rb
-  if (G0 + static_cast<int64_t>(seg) < rb)
-    halo_off = G0 + seg;
-  else if (cam + 1 < p.n_cams)
-    halo_off = p.img_bytes;  // image img + 1, same row
-  const uint32_t row_tx = seg + (halo_off >= 0 ? 16u : 0u);
-
-  auto row_of = [&](int i) { return i < nrows ? r0 + i : r1; };  // CTA row index -> frame row
-  auto ring_row = [&](int i) {  // CTA row index (nrows = the halo row) -> its ring row
-    const int st = i < nrows ? i / kOpRows : nst_own;
-    const int sub = i < nrows ? i - (i / kOpRows) * kOpRows : 0;
-    return ring + ((st % kOpStages) * kOpRows + sub) * kOpRB;
-  };
-  auto issue = [&](int st) {
-    const int slot = st % kOpStages;
-    const int rr = st < nst_own ? min(kOpRows, nrows - st * kOpRows) : 1;
-    mbar_expect_tx(&full[slot], row_tx * rr);
-    for (int i = 0; i < rr; ++i) {
-      const int R = st < nst_own ? r0 + st * kOpRows + i : r1;
-      const uint8_t *srow = src_img + static_cast<int64_t>(R) * rb;
-      uint8_t *d = ring + (slot * kOpRows + i) * kOpRB;
-      bulk_g2s(d, srow + G0, seg, &full[slot]);
-      if (halo_off >= 0) bulk_g2s(d + seg, srow + halo_off, 16u, &full[slot]);
-    }
-  };
-  if (tid == 0) {
-    for (int i = 0; i < kOpStages; ++i) mbar_init(&full[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int st = 0; st < min(kOpStages, nst); ++st) issue(st);
-    n_win = 0;
-  }
-  // tap table (shared by rows and columns: every window has the same size)
-  for (int o = tid; o < q.out; o += kApplyThreads) {
-    int i0, i1, w1;
-    src_coord_w(o, q.scale, q.size, i0, i1, w1);
-    tab[o] = make_uint2(static_cast<uint32_t>(i0),
-                        static_cast<uint32_t>(256 - w1) | (static_cast<uint32_t>(w1) << 16));
-  }
-  for (int s = tid; s < q.stage_cap; s += kApplyThreads) scnt[s] = 0;
-  __syncthreads();
-  // the frame's windows meeting this CTA: owned columns [P0, P1) of the mosaic
-  // (pixels whose first byte is in the group), owned rows [r0, r1)
-  {
-    const int camW = cam * p.W;
-    const int P0 = camW + (G0 + 2) / 3, P1 = camW + (G0 + static_cast<int>(seg) + 2) / 3;
-    const int f0 = q.frame_off[b], f1 = q.frame_off[b + 1];
-    for (int w = f0 + tid; w < f1; w += kApplyThreads) {
-      const int x0 = q.wins[3 * w + 1], y0 = q.wins[3 * w + 2];
-      const int oxl = op_lower_bound(tab, q.out, P0 - x0), oxh = op_lower_bound(tab, q.out, P1 - x0);
-      const int oyl = op_lower_bound(tab, q.out, r0 - y0), oyh = op_lower_bound(tab, q.out, r1 - y0);
-      if (oxl < oxh && oyl < oyh) {
-        const int s = atomicAdd(&n_win, 1);
-        OpWin v;
-        v.base = 3 * (x0 - camW) - G0;
-        v.t = w;
-        v.y0 = y0;
-        v.ox_lo = static_cast<int16_t>(oxl);
-        v.ox_hi = static_cast<int16_t>(oxh);
-        v.oy_lo = static_cast<int16_t>(oyl);
-        v.oy_hi = static_cast<int16_t>(oyh);
-        wl[s] = v;
-      }
-    }
-  }
-  __syncthreads();
-  const int nw = n_win;
-  // schedule: entries (window, output row) counting-sorted by the stage of
-  // the second tap row; scnt[s] ends as the end of stage s's entries
-  auto stage_of_b = [&](const OpWin &v, int oy) {
-    const int i0 = static_cast<int>(tab[oy].x);
-    const int ib = v.y0 + min(i0 + 1, q.size - 1) - r0;  // <= nrows
-    return ib < nrows ? ib / kOpRows : nst_own;
-  };
-  for (int w = 0; w < nw; ++w) {
-    const OpWin v = wl[w];
-    for (int oy = v.oy_lo + tid; oy < v.oy_hi; oy += kApplyThreads) atomicAdd(&scnt[stage_of_b(v, oy)], 1);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    for (int s = 0; s < nst; ++s) {
-      const int c = scnt[s];
-      scnt[s] = acc;
-      acc += c;
-    }
-  }
-  __syncthreads();
-  for (int w = 0; w < nw; ++w) {
-    const OpWin v = wl[w];
-    for (int oy = v.oy_lo + tid; oy < v.oy_hi; oy += kApplyThreads) {
-      const uint2 e = tab[oy];
-      const int i0 = static_cast<int>(e.x);
-      const int ia = v.y0 + i0 - r0;
-      const int ib = v.y0 + min(i0 + 1, q.size - 1) - r0;
-      const int pos = atomicAdd(&scnt[ib < nrows ? ib / kOpRows : nst_own], 1);
-      ent[pos] = make_uint2(static_cast<uint32_t>(ia) | (static_cast<uint32_t>(ib) << 16),
-                            static_cast<uint32_t>(oy) | ((e.y >> 16) << 9) |
-                                (static_cast<uint32_t>(w) << 18));
-    }
-  }
-  (void)stage_of_b;
-
-  // maps come from the preceding solve grid (programmatic dependent launch)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-
-  const bool active = tid < chunks;
-  const double *gl, *bl, *gr, *br;
-  map_ptrs(p, img, gl, bl, gr, br);
-  Coef16F cff;
-  bool in_range = true;
-  if (active) {
-    float m[16], a[16];
-    const int q0 = j * 16;
-    int col = q0 / 3;
-    int ch = q0 - col * 3;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      coef_f32(col, ch, k, p.W, gl, bl, gr, br, m[i], a[i]);
-      if (++ch == 3) {
-        ch = 0;
-        ++col;
-      }
-    }
-    in_range = coef_in_range(m, a);
-    make_coef(m, a, cff);
-  }
-  // halo-chunk lanes: warp 3 lanes 0-15, one sub-pixel each
-  const bool hl = halo_off >= 0 && warp == 3 && lane < 16;
-  const int64_t h_img = halo_off == p.img_bytes ? img + 1 : img;
-  const int h_q = halo_off == p.img_bytes ? lane : (G0 + static_cast<int>(seg)) + lane;
-  float hm = 1.0f, ha = 0.0f;
-  if (hl) op_coef(p, h_img, h_q / 3, h_q % 3, k, hm, ha);
-  const bool fast = __syncthreads_and(in_range) != 0;  // (also: the schedule is complete)
-
-  uint8_t *const dst0 = p.dst + img * p.img_bytes + static_cast<int64_t>(r0) * rb + j * 16;
-  const int O3 = 3 * q.out;
-
-  auto resample = [&](int st) {  // the output rows whose second tap row is in stage st
-    const int e1 = scnt[st];
-    const int e0 = st == 0 ? 0 : scnt[st - 1];
-    for (int e = e0 + warp; e < e1; e += kApplyThreads / 32) {
-      const uint2 E = ent[e];
-      const int oy = static_cast<int>(E.y & 511u);
-      const uint32_t wy1 = (E.y >> 9) & 511u, wy0 = 256u - wy1;
-      const OpWin v = wl[E.y >> 18];
-      const uint8_t *ra = ring_row(static_cast<int>(E.x & 0xffffu));
-      const uint8_t *rb2 = ring_row(static_cast<int>(E.x >> 16));
-      uint8_t *orow = q.tiles + (static_cast<int64_t>(v.t) * q.out + oy) * O3;
-      for (int ox = v.ox_lo + lane; ox < v.ox_hi; ox += 32) {
-        const uint2 c = tab[ox];
-        const uint32_t la = static_cast<uint32_t>(v.base + 3 * static_cast<int>(c.x));
-        const uint32_t sh = la * 8u;  // funnel shifts use the low 5 bits
-        const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
-        const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb2 + (la & ~3u));
-        const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
-        const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
-        uint8_t *o = orow + 3 * ox;
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)
-          const uint32_t v0 = __dp2a_lo(c.y, __byte_perm(alo, ahi, sel), 0u);
-          const uint32_t v1 = __dp2a_lo(c.y, __byte_perm(blo, bhi, sel), 0u);
-          o[ch] = static_cast<uint8_t>((v0 * wy0 + v1 * wy1 + 32768u) >> 16);
-        }
-      }
-    }
-  };
-  auto halo_bytes = [&](uint8_t *row) {  // warp 3 lanes 0-15: the halo chunk, byte-wise
-    if (hl) row[seg + lane] = op_correct_byte(row[seg + lane], hm, ha);
-  };
-  auto end_stage = [&](int st) {
-    fence_proxy_async_smem();  // ring write-backs (generic) before the refill (async)
-    __syncthreads();
-    resample(st);
-    __syncthreads();  // slot of stage st - 1 consumed
-    if (tid == 0 && st >= 1 && st - 1 + kOpStages < nst) issue(st - 1 + kOpStages);
-  };
-
-  auto stream_rows = [&](const auto cf) {
-    uint8_t *dst = dst0;
-    for (int st = 0; st < nst_own; ++st, dst += kOpRows * rb) {
-      const int slot = st % kOpStages;
-      mbar_wait(&full[slot], (st / kOpStages) & 1);
-      const int rr = min(kOpRows, nrows - st * kOpRows);
-#pragma unroll
-      for (int i = 0; i < kOpRows; ++i)
-        if (i < rr) {
-          uint8_t *row = ring + (slot * kOpRows + i) * kOpRB;
-          if (active) {
-            uint4 *rv = reinterpret_cast<uint4 *>(row) + tid;
-            const uint4 o = correct16(*rv, cf);
-            st_stream_v4(dst + i * rb, o);
-            *rv = o;
-          }
-          halo_bytes(row);
-        }
-      end_stage(st);
-    }
-  };
-  if (fast)
-    stream_rows(cff);
-  else
-    stream_rows(general_coef(cff));
-
-  if (hrow) {  // the next CTA's first row: its block's maps, corrected into the ring only
-    const int kh = min(r1 / p.bh, p.K - 1);
-    const int st = nst_own, slot = st % kOpStages;
-    Coef16 ch16;
-    if (active) {
-      float m[16], a[16];
-      const int q0 = j * 16;
-      int col = q0 / 3;
-      int c3 = q0 - col * 3;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        coef_f32(col, c3, kh, p.W, gl, bl, gr, br, m[i], a[i]);
-        if (++c3 == 3) {
-          c3 = 0;
-          ++col;
-        }
-      }
-      Coef16F f;
-      make_coef(m, a, f);
-      ch16 = general_coef(f);
-    }
-    if (hl) op_coef(p, h_img, h_q / 3, h_q % 3, kh, hm, ha);
-    mbar_wait(&full[slot], (st / kOpStages) & 1);
-    uint8_t *row = ring + slot * kOpRows * kOpRB;
-    if (active) {
-      uint4 *rv = reinterpret_cast<uint4 *>(row) + tid;
-      *rv = correct16(*rv, ch16);
-    }
-    halo_bytes(row);
-    __syncthreads();
-    resample(st);
-  }
-  (void)row_of;
-}
-
-// Whether the one-pass kernel serves this launch, and its shared memory.
-static size_t onepass_smem(const OnePassParams &q) {
-  return static_cast<size_t>(kOpStages) * kOpRows * kOpRB + static_cast<size_t>(q.out) * 8 +
-         static_cast<size_t>(q.win_cap) * sizeof(OpWin) + static_cast<size_t>(q.ent_cap) * 8 +
-         static_cast<size_t>(q.stage_cap) * 4;
-}
-
-static int launch_onepass(OnePassParams &q, cudaStream_t stream) {
-  ApplyParams &p = q.a;
-  const int64_t grid = static_cast<int64_t>(p.n_img) * p.K * p.col_groups * p.row_splits;
-  const size_t smem = onepass_smem(q);
-  auto kern = apply_tiles_kernel<5>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return static_cast<int>(e);
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(static_cast<unsigned>(grid));
-  lc.blockDim = dim3(kApplyThreads);
-  lc.dynamicSmemBytes = smem;
-  lc.stream = stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  lc.attrs = at;
-  lc.numAttrs = p.pdl ? 1 : 0;
-  e = cudaLaunchKernelEx(&lc, kern, q);
-  return e == cudaSuccess ? launch_status() : static_cast<int>(e);
-}
-
-// Config 5 through the one-pass kernel when the geometry allows it: aligned
-// rows (K3's fast path), the whole array, a downscale to <= 511 px, at most
-// 256 windows per frame and a schedule that fits shared memory.  Returns 1
-// when it did not apply (the caller runs K3 then K5).
-static int try_onepass(ApplyParams &p, const int32_t *windows, const int32_t *frame_off,
-                       int32_t n_tiles, int32_t max_tiles_per_frame, int32_t size,
-                       int32_t out_size, uint8_t *tiles_out, cudaStream_t stream) {
-  static const bool off = getenv("CAMX_ONEPASS") && getenv("CAMX_ONEPASS")[0] == '0';
-  if (off || frame_off == nullptr || n_tiles <= 0 || out_size >= size || out_size > 511 ||
-      max_tiles_per_frame < 1 || max_tiles_per_frame > 256 || p.cam_count != p.n_cams)
-    return 1;
-  if (!plan_fast(p)) return 1;
-  if (p.rows_per_split + 2 > 65535) return 1;
-  OnePassParams q{};
-  q.a = p;
-  q.wins = windows;
-  q.frame_off = frame_off;
-  q.tiles = tiles_out;
-  q.size = size;
-  q.out = out_size;
-  q.scale = static_cast<float>(size) / static_cast<float>(out_size);
-  q.win_cap = max_tiles_per_frame;
-  // owned output rows of one window in one CTA: rows_per_split * out / size + 2
-  const int64_t rows_w = static_cast<int64_t>(p.rows_per_split) * out_size / size + 2;
-  q.ent_cap = static_cast<int32_t>(std::min<int64_t>(rows_w * max_tiles_per_frame, 1 << 20));
-  q.stage_cap = (p.rows_per_split + kOpRows - 1) / kOpRows + 1;
-  if (onepass_smem(q) > 200 * 1024) return 1;
-  return launch_onepass(q, stream);
-}
-
 static int launch_apply(ApplyParams &p, cudaStream_t stream) {
   if (p.n_img <= 0 || p.H <= 0 || p.W <= 0) return CAMX_OK;
   if (plan_fast(p)) {
@@ -1206,15 +804,11 @@ int tiles_after_apply(const uint8_t *images, int32_t n_cams, int32_t height, int
 static int apply_and_tile(ApplyParams &p, const int32_t *windows, const int32_t *frame_off,
                           int32_t n_tiles, int32_t max_tiles_per_frame, int32_t size,
                           int32_t out_size, uint8_t *tiles_out, void *stream) {
+  (void)frame_off;
+  (void)max_tiles_per_frame;
   if (n_tiles < 0 || size < 1 || out_size < 1 || size > p.H || size > p.n_cams * p.W)
     return CAMX_EINVAL;
   if (n_tiles > 0 && (windows == nullptr || tiles_out == nullptr)) return CAMX_EINVAL;
-  if (n_tiles > 0 && p.n_img > 0) {
-    ApplyParams q = p;
-    const int st = try_onepass(q, windows, frame_off, n_tiles, max_tiles_per_frame, size,
-                               out_size, tiles_out, as_stream(stream));
-    if (st != 1) return st;
-  }
   int st = launch_apply(p, as_stream(stream));
   if (st != CAMX_OK || n_tiles == 0) return st;
   return tiles_after_apply(p.dst, p.n_cams, p.H, p.W, windows, n_tiles, size, out_size,
