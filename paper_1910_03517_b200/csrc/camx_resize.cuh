@@ -42,24 +42,27 @@ __device__ __forceinline__ uint32_t bilerp_fx(uint32_t a, uint32_t b, uint32_t c
 // (256 - w1) | w1 << 16.  Per pixel: 3 aligned words per row + funnel shift
 // (the 8 bytes from the tap pair on), channel pairs by PRMT, horizontal
 // blend by dp2a, vertical by IMAD (bilerp_fx arithmetic, bit-identical).
-template <int J>
+template <int J, bool RANGE = false, bool EXACT = false>
 __device__ __forceinline__ void resample_row_lanes(const uint8_t *ra, const uint8_t *rb,
                                                    const uint32_t (&off)[J],
                                                    const uint32_t (&wt)[J], uint32_t wy1,
                                                    uint8_t *orow, int out, int lane,
                                                    int ox_lo = 0, int ox_hi = 1 << 30) {
   const uint32_t wy0 = 256u - wy1;
+  uint8_t *const ol = orow + 3 * lane;  // column l + 32 j at ol + 96 j (immediate offsets)
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int ox = lane + 32 * j;
-    if (ox < out && ox >= ox_lo && ox < ox_hi) {
+    // EXACT: J = ceil(out / 32), so only the last j can run past `out`;
+    // RANGE: a camera shard's owned columns [ox_lo, ox_hi)
+    if (((EXACT && j < J - 1) || ox < out) && (!RANGE || (ox >= ox_lo && ox < ox_hi))) {
       const uint32_t la = off[j];
       const uint32_t sh = la * 8u;  // funnel shifts use the low 5 bits
       const uint32_t *wa = reinterpret_cast<const uint32_t *>(ra + (la & ~3u));
       const uint32_t *wb = reinterpret_cast<const uint32_t *>(rb + (la & ~3u));
       const uint32_t alo = __funnelshift_r(wa[0], wa[1], sh), ahi = __funnelshift_r(wa[1], wa[2], sh);
       const uint32_t blo = __funnelshift_r(wb[0], wb[1], sh), bhi = __funnelshift_r(wb[1], wb[2], sh);
-      uint8_t *o = orow + 3 * ox;
+      uint8_t *o = ol + 96 * j;
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
         const uint32_t sel = 0x0030u + 0x0011u * ch;  // bytes (ch, ch + 3)

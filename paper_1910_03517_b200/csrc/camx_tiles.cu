@@ -237,7 +237,7 @@ struct TileShard {
   const uint8_t *halo;  // [B][H][3] or nullptr
 };
 
-template <int J>
+template <int J, bool EXACT>
 __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const TileParams p,
                                                                        const TmaTileGeom g,
                                                                        const TileShard sd) {
@@ -341,8 +341,15 @@ __global__ void __launch_bounds__(kTmaTileWarps * 32) tiles_tma_kernel(const Til
       }
       __syncwarp();
     }
-    resample_row_lanes<J>(ra, ra + g.pitch, off, wt, static_cast<uint32_t>(w1y), orow, out, lane,
-                          ox_lo, ox_hi);
+    // (the output row buffer is shared memory on the bulk path: 32-bit
+    // addresses, byte stores at immediate offsets; a shard's partial row
+    // goes straight to global memory)
+    if (bulk)
+      resample_row_lanes<J, false, EXACT>(ra, ra + g.pitch, off, wt, static_cast<uint32_t>(w1y), ob,
+                                          out, lane);
+    else
+      resample_row_lanes<J, true>(ra, ra + g.pitch, off, wt, static_cast<uint32_t>(w1y), orow, out,
+                                  lane, ox_lo, ox_hi);
     if (bulk) {
       fence_proxy_async_smem();  // this lane's row bytes before the bulk store reads them
       __syncwarp();
@@ -397,11 +404,12 @@ static int launch_tiles_tma(const TileParams &p, int32_t n_tiles, cudaStream_t s
     e = cudaLaunchKernelEx(&lc, kern, p, g, sd);
     return e == cudaSuccess ? launch_status() : static_cast<int>(e);
   };
-  if (J <= 2) return go(tiles_tma_kernel<2>);
-  if (J <= 4) return go(tiles_tma_kernel<4>);
-  if (J <= 8) return go(tiles_tma_kernel<8>);
-  if (J <= 13) return go(tiles_tma_kernel<13>);
-  return go(tiles_tma_kernel<16>);
+  // EXACT instantiations where J = ceil(out / 32) (416 -> 13)
+  if (J == 2) return go(tiles_tma_kernel<2, true>);
+  if (J <= 4) return J == 4 ? go(tiles_tma_kernel<4, true>) : go(tiles_tma_kernel<4, false>);
+  if (J <= 8) return J == 8 ? go(tiles_tma_kernel<8, true>) : go(tiles_tma_kernel<8, false>);
+  if (J <= 13) return J == 13 ? go(tiles_tma_kernel<13, true>) : go(tiles_tma_kernel<13, false>);
+  return J == 16 ? go(tiles_tma_kernel<16, true>) : go(tiles_tma_kernel<16, false>);
 }
 
 static bool tiles_tma_ok(const TileParams &p) {
