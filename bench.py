@@ -236,7 +236,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    name = args.workload or "config2"
+    # the GPU arm's workload at this N (config 3 = config 2's array sharded
+    # over the ranks; the same frames - the CPU reference has no shards)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    name = args.workload or ("config3" if world > 1 else "config2")
     n_cams, H, W, _, desc = WORKLOADS[name]
     frames = bench_frames(name, 2, "cpu").numpy()
     threads = os.cpu_count() or 1
