@@ -1,6 +1,7 @@
 """Where the N=8 sharded step loses time (one GPU, stand-in one-rank comm):
-K3 alone on one camera vs the pipelined submit() step, at B = 30."""
+K3 alone on one camera vs the pipelined submit() step, at B = 30 (WEAK=1: B = 30 N)."""
 import ctypes
+import os
 import sys
 
 import torch
@@ -31,7 +32,10 @@ def timeit(fn, steps=40):
     return e0.elapsed_time(e1) / steps
 
 
+B0 = B
 for world in (1, 2, 4, 8):
+    # WEAK=1: 30 N array-frames per step (bench.py config 3), else a fixed batch
+    B = B0 * world if os.environ.get("WEAK") else B0
     b0, c = camera_partition(N, world)[0]
     frames = synthetic_batch(B, c, H, W, seed=1)
     out = torch.empty_like(frames)
@@ -53,7 +57,7 @@ for world in (1, 2, 4, 8):
     byt = 2 * frames.numel()
     print(f"world {world} B {B}: K3 alone {k3 * 1e3:.1f} us ({byt / k3 / 1e6:.0f} GB/s), "
           f"pipelined step {step * 1e3:.1f} us, unpipelined {seq * 1e3:.1f} us; "
-          f"whole-job array-fps {world * B / (step / 1e3):.0f} = "
-          f"{world * B / (step / 1e3) / (world * 40700):.1%} of N x 40.7K", flush=True)
+          f"whole-job array-fps {B / (step / 1e3):.0f} (every rank holds 1/N of each "
+          f"array-frame) = {B / (step / 1e3) / (world * 40700):.1%} of N x 40.7K", flush=True)
     del frames, out, ac, ac2
     torch.cuda.empty_cache()
