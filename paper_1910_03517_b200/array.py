@@ -579,7 +579,7 @@ class ArrayCorrector:
 
     # ------------------------------------------------------------ attention
     def correct_with_motion(self, frames, out=None, *, size: int = 960, t_motion: int = 20,
-                            stream=None):
+                            stream=None, _bufs=None):
         """Correct a batch and, in the same pass over the pixels (K4 fused
         into K3: camx_correct_batch_motion), count per array-frame the
         motion-mask on-pixels of every window of the overlap-0 tiling - the
@@ -592,7 +592,9 @@ class ArrayCorrector:
         every rank returns the whole array's counts.
 
         Returns (CorrectResult, counts int64 CUDA tensor (B, n_windows) in
-        window_origins order, has_counts list[bool] per frame)."""
+        window_origins order, has_counts list[bool] per frame).  `_bufs`
+        (internal, whole array only): result buffers (stats, gain, offset,
+        fit_ok, hist) the kernels write directly - AttendPipeline's slots."""
         t = _dev.require_cuda()
         sharded = self.cam_count != self.n_cams
         if self.S == 0:
@@ -615,7 +617,7 @@ class ArrayCorrector:
             out = t.empty_like(frames)
         elif out.shape != frames.shape or not out.is_contiguous():
             raise ValueError("out must match frames")
-        buf = self._buffers(B)
+        buf = _bufs if _bufs is not None and not sharded else self._buffers(B)
         main = stream if stream is not None else t.cuda.current_stream()
         sh = _dev.stream_handle(main)
         counts = t.empty((B, len(origins)), dtype=t.int64, device="cuda")
@@ -862,6 +864,12 @@ class AttendPipeline:
                       hist=(t.empty((B, ac.n_cams, 2, ac.K, 3, 256), dtype=t.int32,
                                     device="cuda") if ac.histograms else None),
                       counts=t.empty((B, n_win), dtype=t.int64, pin_memory=True),
+                      # the chosen windows go up through pinned memory on the
+                      # caller's stream: a pageable upload would synchronise the
+                      # host with the batch just submitted (the GPU then idles
+                      # while the host returns and launches the next batch)
+                      wins_host=t.empty((B * n_win, 3), dtype=t.int32, pin_memory=True),
+                      wins_dev=t.empty((B * n_win, 3), dtype=t.int32, device="cuda"),
                       event=t.cuda.Event())
             self._slots[key] = sl
         return sl
@@ -873,17 +881,20 @@ class AttendPipeline:
             frames = frames[None]
         B = frames.shape[0]
         sl = self._slot(B, self._k % 2)
+        # the fused kernels write maps, stats and histograms straight into the
+        # slot (no per-batch device copies of ~100 MB of histograms)
         res, counts, has = self.ac.correct_with_motion(
             frames, sl["out"], size=self.scheduler.window_size, t_motion=self.t_motion,
-            stream=main)
+            stream=main, _bufs=sl)
         S = self.ac.S
         with t.cuda.stream(main):
-            sl["gain"][:, :S].copy_(res.gain, non_blocking=True)
-            sl["offset"][:, :S].copy_(res.offset, non_blocking=True)
-            sl["fit_ok"][:, :S].copy_(res.fit_ok, non_blocking=True)
-            sl["stats"].copy_(res.stats, non_blocking=True)
-            if sl["hist"] is not None:
-                sl["hist"].copy_(res.hist, non_blocking=True)
+            if res.gain.data_ptr() != sl["gain"].data_ptr():  # a shard or the unfused path
+                sl["gain"][:, :S].copy_(res.gain, non_blocking=True)
+                sl["offset"][:, :S].copy_(res.offset, non_blocking=True)
+                sl["fit_ok"][:, :S].copy_(res.fit_ok, non_blocking=True)
+                sl["stats"].copy_(res.stats, non_blocking=True)
+                if sl["hist"] is not None:
+                    sl["hist"].copy_(res.hist, non_blocking=True)
             sl["counts"].copy_(counts, non_blocking=True)
             sl["event"].record(main)
         prev, self._pending = self._pending, (sl, B, int(frame_index), tuple(objects), has)
@@ -911,10 +922,18 @@ class AttendPipeline:
         tiles = t.empty((len(wins), self.out_size, self.out_size, 3), dtype=t.uint8,
                         device="cuda")
         if wins:
-            wd = _dev.to_device(np.asarray(wins, dtype=np.int32).reshape(-1, 3))
-            sl["wins"] = wd  # alive until the slot's next use (the launch is async)
+            n = len(wins)
+            if n > sl["wins_host"].shape[0]:  # more windows than the tiling (large budgets)
+                sl["wins_host"] = t.empty((n, 3), dtype=t.int32, pin_memory=True)
+                sl["wins_dev"] = t.empty((n, 3), dtype=t.int32, device="cuda")
+            # the slot's previous upload (two submits ago) ran before the batch
+            # whose event was synchronised above, so its host buffer is free
+            sl["wins_host"][:n].numpy()[:] = np.asarray(wins, dtype=np.int32).reshape(-1, 3)
+            wd = sl["wins_dev"]
+            with t.cuda.stream(main):
+                wd[:n].copy_(sl["wins_host"][:n], non_blocking=True)
             _lib.call("camx_tiles", sl["out"].data_ptr(), ac.n_cams, ac.height, ac.width,
-                      wd.data_ptr(), len(wins), int(sched.window_size), self.out_size,
+                      wd.data_ptr(), n, int(sched.window_size), self.out_size,
                       tiles.data_ptr(), _dev.stream_handle(main))
         S = ac.S
         res = CorrectResult(sl["out"], sl["gain"][:, :S], sl["offset"][:, :S],

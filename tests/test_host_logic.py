@@ -309,3 +309,47 @@ def test_merge_with_budget_cut_is_exact(wins, budget, merge_iou):
     full = at._merge_duplicates(reqs, merge_iou)[:budget]
     cut = at._merge_duplicates(reqs, merge_iou, budget)
     assert [r.priority for r in cut] == [r.priority for r in full]
+
+
+def _merge_by_core_iou(reqs, merge_iou):
+    """attention.py:140-146 as written: core.iou on BBox objects."""
+    from paper_1910_03517_b200.core import iou
+    kept, boxes = [], []
+    for r in reqs:
+        b = r.window.as_bbox()
+        if not any(iou(b, k) > merge_iou for k in boxes):
+            kept.append(r)
+            boxes.append(b)
+    return kept
+
+
+@given(st.lists(st.tuples(st.integers(0, 400), st.integers(0, 400), st.integers(1, 200)),
+                min_size=0, max_size=40),
+       st.floats(0.0, 1.0))
+def test_merge_inlined_iou_matches_core_iou(wins, merge_iou):
+    """_merge_duplicates' inlined integer IoU keeps exactly the requests the
+    reference's core.iou comparison keeps (mixed window sizes)."""
+    reqs = [at.AttentionRequest(DetectorWindow(x, y, s), at.Mechanism.DIFFERENCE, i)
+            for i, (x, y, s) in enumerate(wins)]
+    assert at._merge_duplicates(reqs, merge_iou) == _merge_by_core_iou(reqs, merge_iou)
+
+
+@given(st.integers(0, 2**31), st.sampled_from([(16384, 1536), (4000, 1200), (2980, 960)]),
+       st.sampled_from([960, 416, 300]), st.integers(1, 12), st.sampled_from([0, 50, 1000]),
+       st.sampled_from([0.3, 0.8, 0.95]))
+def test_scheduler_tick_matches_reference_restatement(seed, mosaic, size, budget, thr, miou):
+    """A post-startup tick with device counts (lazy ranking, cached tiling,
+    inlined IoU) equals rank-all-then-merge with core.iou (attention.py:89-103,
+    140-146, 175-186)."""
+    rng = np.random.default_rng(seed)
+    cfg = at.AttentionConfig(budget=budget, window_size=size, diff_threshold=thr, merge_iou=miou)
+    sch = at.Scheduler(mosaic, cfg)
+    sch._startup.clear()
+    s = sch.window_size
+    org = at.window_origins(mosaic, s, 0.0)
+    counts = rng.choice([0, 10, 60, 500, 5000], size=len(org))
+    got = sch.schedule(frame_index=0, window_counts_fn=lambda o, ss: counts)
+    order = sorted((i for i, c in enumerate(counts) if c > thr), key=lambda i: -int(counts[i]))
+    ranked = [at.AttentionRequest(DetectorWindow(*org[i], s), at.Mechanism.DIFFERENCE, r)
+              for r, i in enumerate(order)]
+    assert got == _merge_by_core_iou(ranked, miou)[:budget]

@@ -1,0 +1,63 @@
+"""Config 5m (the attention tick, bench.py's AttendPipeline step): is the
+step GPU- or host-bound?  Host wall time per submit() with no
+synchronisation (the enqueue + the previous batch's Scheduler ticks) vs the
+GPU's time per step (CUDA events), and the GPU time of the copies submit()
+makes into its result slot.
+
+    python tools/attend_probe.py
+"""
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+
+sys.argv = [sys.argv[0], "--workload", "config5m"]
+ap = bench.parse()
+wl = bench.Workload("config5m", 30, ap, 1, 0, torch).run(20, 3, torch.cuda.synchronize)
+print(f"bench step {wl.ms / wl.steps:.4f} ms (GPU events)")
+s = wl.stream
+torch.cuda.synchronize()
+for rep in range(3):
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    host = []
+    for _ in range(20):
+        h0 = time.perf_counter()
+        wl.step()
+        host.append(time.perf_counter() - h0)
+    e1.record(s)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / 20
+    print(f"rep {rep}: host per submit {sum(host) / len(host) * 1e3:.3f} ms (max "
+          f"{max(host) * 1e3:.3f}), wall per step {wall * 1e3:.3f} ms, GPU per step "
+          f"{e0.elapsed_time(e1) / 20:.4f} ms", flush=True)
+# the slot copies alone (maps, stats, histograms of one 30-frame batch)
+ac = wl.ac
+res = ac._buffers(30)
+sl = wl.pipe._slot(30, 0)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+with torch.cuda.stream(s):
+    e0.record(s)
+    for _ in range(20):
+        sl["stats"].copy_(res["stats"].view_as(sl["stats"]), non_blocking=True)
+        if sl["hist"] is not None:
+            sl["hist"].copy_(res["hist"].view_as(sl["hist"]), non_blocking=True)
+    e1.record(s)
+torch.cuda.synchronize()
+print(f"stats + histogram slot copies: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us per batch")
+
+if "--profile" in sys.argv[1:]:
+    import cProfile
+    import pstats
+    pr = cProfile.Profile()
+    torch.cuda.synchronize()
+    pr.enable()
+    for _ in range(20):
+        wl.step()
+    torch.cuda.synchronize()
+    pr.disable()
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
