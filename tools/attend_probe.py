@@ -4,7 +4,7 @@ synchronisation (the enqueue + the previous batch's Scheduler ticks) vs the
 GPU's time per step (CUDA events), and the GPU time of the copies submit()
 makes into its result slot.
 
-    python tools/attend_probe.py
+    python tools/attend_probe.py [config5m|config5|config2] [--profile]
 """
 import sys
 import time
@@ -14,9 +14,12 @@ import torch
 sys.path.insert(0, ".")
 import bench  # noqa: E402
 
-sys.argv = [sys.argv[0], "--workload", "config5m"]
+name = next((a for a in sys.argv[1:] if a.startswith("config")), "config5m")
+prof = "--profile" in sys.argv[1:]
+sys.argv = [sys.argv[0], "--workload", name]
 ap = bench.parse()
-wl = bench.Workload("config5m", 30, ap, 1, 0, torch).run(20, 3, torch.cuda.synchronize)
+wl = bench.Workload(name, bench.WORKLOADS[name][3], ap, 1, 0, torch).run(20, 3,
+                                                                       torch.cuda.synchronize)
 print(f"bench step {wl.ms / wl.steps:.4f} ms (GPU events)")
 s = wl.stream
 torch.cuda.synchronize()
@@ -35,6 +38,8 @@ for rep in range(3):
     print(f"rep {rep}: host per submit {sum(host) / len(host) * 1e3:.3f} ms (max "
           f"{max(host) * 1e3:.3f}), wall per step {wall * 1e3:.3f} ms, GPU per step "
           f"{e0.elapsed_time(e1) / 20:.4f} ms", flush=True)
+if name != "config5m":
+    sys.exit(0)
 # the slot copies alone (maps, stats, histograms of one 30-frame batch)
 ac = wl.ac
 res = ac._buffers(30)
@@ -50,7 +55,7 @@ with torch.cuda.stream(s):
 torch.cuda.synchronize()
 print(f"stats + histogram slot copies: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us per batch")
 
-if "--profile" in sys.argv[1:]:
+if prof:
     import cProfile
     import pstats
     pr = cProfile.Profile()
