@@ -16,6 +16,7 @@ import bench  # noqa: E402
 
 name = next((a for a in sys.argv[1:] if a.startswith("config")), "config5m")
 prof = "--profile" in sys.argv[1:]
+split = "--split" in sys.argv[1:]
 sys.argv = [sys.argv[0], "--workload", name]
 ap = bench.parse()
 wl = bench.Workload(name, bench.WORKLOADS[name][3], ap, 1, 0, torch).run(20, 3,
@@ -40,6 +41,25 @@ for rep in range(3):
           f"{e0.elapsed_time(e1) / 20:.4f} ms", flush=True)
 if name != "config5m":
     sys.exit(0)
+if split:  # the pieces of one step, each timed alone on the step's stream
+    ac, pipe = wl.ac, wl.pipe
+    sl = pipe._slot(30, 0)
+
+    def t_of(fn, n=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(n):
+            fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n * 1e3
+    with torch.cuda.stream(s):
+        print(f"correct_with_motion into the slot: {t_of(lambda: ac.correct_with_motion(wl.frames, sl['out'], size=960, stream=s, _bufs=sl)):.1f} us")
+        print(f"  (of it: the previous-frame copy {t_of(lambda: ac._motion_prev.copy_(wl.frames[29], non_blocking=True)):.1f} us)")
+        print(f"full submit (steady state): {t_of(lambda: pipe.submit(wl.frames, frame_index=0, stream=s)):.1f} us")
 # the slot copies alone (maps, stats, histograms of one 30-frame batch)
 ac = wl.ac
 res = ac._buffers(30)
