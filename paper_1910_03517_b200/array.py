@@ -845,6 +845,7 @@ class AttendPipeline:
         self._slots: dict = {}
         self._k = 0
         self._pending = None
+        self._copy = None  # side stream of the counts' D2H
 
     def _slot(self, B: int, i: int):
         key = (B, i)
@@ -895,8 +896,16 @@ class AttendPipeline:
                 sl["stats"].copy_(res.stats, non_blocking=True)
                 if sl["hist"] is not None:
                     sl["hist"].copy_(res.hist, non_blocking=True)
+        # the counts' D2H runs on a side stream: on the compute stream the
+        # small copy would sit between batch k and the next kernels (~30 us
+        # of copy-engine round trip per step); the host waits for its event
+        if self._copy is None:
+            self._copy = t.cuda.Stream()
+        self._copy.wait_stream(main)
+        with t.cuda.stream(self._copy):
             sl["counts"].copy_(counts, non_blocking=True)
-            sl["event"].record(main)
+            sl["event"].record(self._copy)
+        counts.record_stream(self._copy)
         prev, self._pending = self._pending, (sl, B, int(frame_index), tuple(objects), has)
         self._k += 1
         return self._finish(prev, main) if prev is not None else None

@@ -59,6 +59,23 @@ if split:  # the pieces of one step, each timed alone on the step's stream
     with torch.cuda.stream(s):
         print(f"correct_with_motion into the slot: {t_of(lambda: ac.correct_with_motion(wl.frames, sl['out'], size=960, stream=s, _bufs=sl)):.1f} us")
         print(f"  (of it: the previous-frame copy {t_of(lambda: ac._motion_prev.copy_(wl.frames[29], non_blocking=True)):.1f} us)")
+        cnt_h = torch.empty((30, 36), dtype=torch.int64, pin_memory=True)
+
+        def with_d2h():
+            _, c, _ = ac.correct_with_motion(wl.frames, sl["out"], size=960, stream=s, _bufs=sl)
+            cnt_h.copy_(c, non_blocking=True)
+        print(f"  + the counts D2H: {t_of(with_d2h):.1f} us")
+        import numpy as np
+        wins = torch.as_tensor(np.asarray([(b, 960 * (b % 16), 0) for b in range(30)
+                                           for _ in range(4)], np.int32), device="cuda")
+        tiles = torch.empty((120, 416, 416, 3), dtype=torch.uint8, device="cuda")
+        from paper_1910_03517_b200 import _lib
+
+        def with_tiles():
+            with_d2h()
+            _lib.call("camx_tiles", sl["out"].data_ptr(), 8, 1536, 2048, wins.data_ptr(), 120,
+                      960, 416, tiles.data_ptr(), s.cuda_stream)
+        print(f"  + 120 tiles: {t_of(with_tiles):.1f} us")
         print(f"full submit (steady state): {t_of(lambda: pipe.submit(wl.frames, frame_index=0, stream=s)):.1f} us")
 # the slot copies alone (maps, stats, histograms of one 30-frame batch)
 ac = wl.ac
