@@ -846,6 +846,7 @@ class AttendPipeline:
         self._k = 0
         self._pending = None
         self._copy = None  # side stream of the counts' D2H
+        self._tile_stream = None  # side stream of the previous batch's tiles
 
     def _slot(self, B: int, i: int):
         key = (B, i)
@@ -939,11 +940,22 @@ class AttendPipeline:
             # whose event was synchronised above, so its host buffer is free
             sl["wins_host"][:n].numpy()[:] = np.asarray(wins, dtype=np.int32).reshape(-1, 3)
             wd = sl["wins_dev"]
-            with t.cuda.stream(main):
+            # batch k-1's frames are complete (its event was synchronised
+            # above), so its tiles need not queue behind batch k on `main`:
+            # they run beside k's kernels on a side stream, and `main` waits
+            # for them before anything enqueued after this call
+            if self._tile_stream is None:
+                self._tile_stream = t.cuda.Stream()
+            ts = self._tile_stream
+            with t.cuda.stream(ts):
                 wd[:n].copy_(sl["wins_host"][:n], non_blocking=True)
-            _lib.call("camx_tiles", sl["out"].data_ptr(), ac.n_cams, ac.height, ac.width,
-                      wd.data_ptr(), n, int(sched.window_size), self.out_size,
-                      tiles.data_ptr(), _dev.stream_handle(main))
+                _lib.call("camx_tiles", sl["out"].data_ptr(), ac.n_cams, ac.height, ac.width,
+                          wd.data_ptr(), n, int(sched.window_size), self.out_size,
+                          tiles.data_ptr(), _dev.stream_handle(ts))
+                done = t.cuda.Event()
+                done.record(ts)
+            tiles.record_stream(ts)
+            main.wait_event(done)
         S = ac.S
         res = CorrectResult(sl["out"], sl["gain"][:, :S], sl["offset"][:, :S],
                             sl["fit_ok"][:, :S], sl["stats"], sl["hist"])
