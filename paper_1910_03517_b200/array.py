@@ -829,13 +829,16 @@ class AttendPipeline:
     pixels on the GPU, the per-tick decision on the host, in parallel).
 
     submit(batch k) launches k's correction with the fused motion counts
-    (ArrayCorrector.correct_with_motion) and an async copy of the counts to
-    pinned host memory, then finishes batch k-1: waits for its counts (its
-    kernels ran before k's), runs `scheduler` on each of its array-frames on
-    the host while the GPU corrects batch k, and launches k-1's tiles behind
-    k (camx_tiles on k-1's corrected frames).  It returns k-1's
-    AttendResult (None for the first batch); flush() returns the last one.
-    A result's buffers (frames, maps) are reused two submits later."""
+    (ArrayCorrector.correct_with_motion, writing straight into a result
+    slot) and an async copy of the counts to pinned host memory (on a side
+    stream), then finishes batch k-1: waits for its counts (its kernels ran
+    before k's), runs `scheduler` on each of its array-frames on the host
+    while the GPU corrects batch k, and launches k-1's tiles (camx_tiles on
+    k-1's corrected frames) on a second side stream beside k's kernels; the
+    caller's stream waits for those tiles before anything enqueued after the
+    call.  It returns k-1's AttendResult (None for the first batch); flush()
+    returns the last one.  A result's buffers (frames, maps) are reused two
+    submits later."""
 
     def __init__(self, corrector, scheduler, *, out_size: int = 416, t_motion: int = 20):
         if tuple(scheduler.mosaic_size) != (corrector.n_cams * corrector.width, corrector.height):
