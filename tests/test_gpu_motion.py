@@ -157,34 +157,40 @@ def test_motion_rejects_bad_arguments():
         ac.correct_and_attend(d, sched)
 
 
-def test_attend_pipeline_matches_sequential_ticks():
-    """AttendPipeline (batch k's kernels under batch k-1's host ticks) gives
-    the same requests, tiles, maps and frames as correct_and_attend called
-    batch by batch."""
+@pytest.mark.parametrize("geom", [(3, 200, 256, 3, 3, 200), (4, 1024, 1024, 6, 6, 960)],
+                         ids=["small", "long-stream"])
+def test_attend_pipeline_matches_sequential_ticks(geom):
+    """AttendPipeline (batch k's kernels under batch k-1's host ticks; the
+    counts' D2H and k-1's tiles on side streams) gives the same requests,
+    tiles, maps and frames as correct_and_attend called batch by batch -
+    "long-stream" reuses every result slot several times with kernels long
+    enough for the side streams to overlap them."""
     from paper_1910_03517_b200.array import AttendPipeline
-    N, H, W, B = 3, 200, 256, 3
-    frames = moving_batch(3 * B, N, H, W, seed=11)
+    N, H, W, B, n_b, win = geom
+    frames = moving_batch(n_b * B, N, H, W, seed=11)
     d = torch.from_numpy(frames).cuda()
     cfg = xp.ExposureConfig(band_width=16, blocks=4)
-    acfg = at.AttentionConfig(window_size=200, budget=2, diff_threshold=5)
+    acfg = at.AttentionConfig(window_size=win, budget=2, diff_threshold=5)
     seq_ac = ArrayCorrector(N, H, W, cfg, histograms=True)
     seq_s = at.Scheduler((N * W, H), acfg)
     want = []
-    for k in range(3):  # the corrector's map buffers are reused by the next call: clone now
+    for k in range(n_b):  # the corrector's map buffers are reused by the next call: clone now
         r, q, tl, _ = seq_ac.correct_and_attend(d[k * B:(k + 1) * B], seq_s, frame_index=k * B,
                                                 out_size=40)
         want.append((r.out.clone(), r.gain.clone(), r.hist.clone(), q, tl.clone()))
     pipe = AttendPipeline(ArrayCorrector(N, H, W, cfg, histograms=True),
                           at.Scheduler((N * W, H), acfg), out_size=40)
     got = []
-    for k in range(4):  # results arrive one submit late; compare before slot reuse
-        r = pipe.submit(d[k * B:(k + 1) * B], frame_index=k * B) if k < 3 else pipe.flush()
+    for k in range(n_b + 1):  # results arrive one submit late; compare before slot reuse
+        r = pipe.submit(d[k * B:(k + 1) * B], frame_index=k * B) if k < n_b else pipe.flush()
         if k == 0:
             assert r is None
             continue
         got.append((r.frame_index, r.result.out.clone(), r.result.gain.clone(),
                     r.result.hist.clone(), r.requests, r.tiles.clone()))
     assert pipe.flush() is None
+    if win == 960:  # the fused counts, written straight into the pipeline's slots
+        assert pipe.ac.last_motion_fused
     for k, (g, (out, gain, hist, reqs, tiles)) in enumerate(zip(got, want)):
         f0, g_out, g_gain, g_hist, g_reqs, g_tiles = g
         assert f0 == k * B
