@@ -319,7 +319,9 @@ class Workload:
             from paper_1910_03517_b200.array import AttendPipeline
             from paper_1910_03517_b200.attention import Scheduler
             self.scheduler = Scheduler((n_cams * W, H))
-            self.pipe = AttendPipeline(self.ac, self.scheduler)
+            # the step re-submits the same resident batch unchanged, so the
+            # next batch's frame 0 reads its previous frame in place
+            self.pipe = AttendPipeline(self.ac, self.scheduler, retain_frames=True)
             self.frame_index = 0
             self.tiles_attended = 0
         self.tiles_buf = None

@@ -94,6 +94,7 @@ class ArrayCorrector:
         self._prev_maps = None     # (gain, offset) device [S][2][K][3]
         self._prev_frame = None    # device (N, H, W, 3), OBJECT_REMOVAL only
         self._motion_prev = None   # device (N, H, W, 3): last frame of correct_with_motion
+        self._motion_own = None    # the copy buffer behind _motion_prev (retain=False)
         self._ring = None
 
     # ------------------------------------------------------------ state
@@ -579,7 +580,7 @@ class ArrayCorrector:
 
     # ------------------------------------------------------------ attention
     def correct_with_motion(self, frames, out=None, *, size: int = 960, t_motion: int = 20,
-                            stream=None, _bufs=None):
+                            stream=None, retain: bool = False, _bufs=None):
         """Correct a batch and, in the same pass over the pixels (K4 fused
         into K3: camx_correct_batch_motion), count per array-frame the
         motion-mask on-pixels of every window of the overlap-0 tiling - the
@@ -592,7 +593,12 @@ class ArrayCorrector:
         every rank returns the whole array's counts.
 
         Returns (CorrectResult, counts int64 CUDA tensor (B, n_windows) in
-        window_origins order, has_counts list[bool] per frame).  `_bufs`
+        window_origins order, has_counts list[bool] per frame).
+        `retain=True`: the caller keeps `frames` unchanged until the next
+        call's kernels have run (a ring of two or more batch buffers, or a
+        batch re-submitted unchanged), so the next call's frame 0 reads its
+        previous frame from this batch in place instead of from a copy (saves
+        a device copy of one array-frame per call).  `_bufs`
         (internal, whole array only): result buffers (stats, gain, offset,
         fit_ok, hist) the kernels write directly - AttendPipeline's slots."""
         t = _dev.require_cuda()
@@ -676,10 +682,14 @@ class ArrayCorrector:
                           int(t_motion), N, H, W, org.data_ptr(), len(origins), s,
                           counts[b].data_ptr(), sh)
         has = [mp is not None] + [True] * (B - 1)
-        with t.cuda.stream(main):
-            if self._motion_prev is None:
-                self._motion_prev = t.empty_like(frames[0])
-            self._motion_prev.copy_(frames[B - 1], non_blocking=True)
+        if retain:
+            self._motion_prev = frames[B - 1]  # read in place by the next call
+        else:
+            with t.cuda.stream(main):
+                if self._motion_own is None or self._motion_own.shape != frames[0].shape:
+                    self._motion_own = t.empty_like(frames[0])
+                self._motion_own.copy_(frames[B - 1], non_blocking=True)
+            self._motion_prev = self._motion_own
         return res, counts, has
 
     def correct_and_attend(self, frames, scheduler, *, objects=(), frame_index: int = 0,
@@ -840,11 +850,15 @@ class AttendPipeline:
     returns the last one.  A result's buffers (frames, maps) are reused two
     submits later."""
 
-    def __init__(self, corrector, scheduler, *, out_size: int = 416, t_motion: int = 20):
+    def __init__(self, corrector, scheduler, *, out_size: int = 416, t_motion: int = 20,
+                 retain_frames: bool = False):
         if tuple(scheduler.mosaic_size) != (corrector.n_cams * corrector.width, corrector.height):
             raise ValueError("scheduler mosaic does not match the array")
         self.ac, self.scheduler = corrector, scheduler
         self.out_size, self.t_motion = int(out_size), int(t_motion)
+        # True: each submitted batch stays unchanged until the next batch's
+        # kernels have run (ArrayCorrector.correct_with_motion(retain=True))
+        self.retain_frames = bool(retain_frames)
         self._slots: dict = {}
         self._k = 0
         self._pending = None
@@ -890,7 +904,7 @@ class AttendPipeline:
         # slot (no per-batch device copies of ~100 MB of histograms)
         res, counts, has = self.ac.correct_with_motion(
             frames, sl["out"], size=self.scheduler.window_size, t_motion=self.t_motion,
-            stream=main, _bufs=sl)
+            stream=main, retain=self.retain_frames, _bufs=sl)
         S = self.ac.S
         with t.cuda.stream(main):
             if res.gain.data_ptr() != sl["gain"].data_ptr():  # a shard or the unfused path

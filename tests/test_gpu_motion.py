@@ -226,3 +226,24 @@ def test_motion_counts_with_wrap_and_stateful_modes(mode):
     for b in range(1, 4):
         _, want_c = oracle_counts(frames[b - 1], frames[b], S, 20)
         np.testing.assert_array_equal(c[b], want_c)
+
+
+def test_retain_reads_previous_batch_in_place():
+    """correct_with_motion(retain=True) over alternating batch buffers (a
+    two-slot ring) gives the same frames, maps and counts as the copying
+    default: frame 0's previous frame is read from the previous buffer."""
+    N, H, W, B, S = 3, 96, 128, 2, 64
+    frames = moving_batch(3 * B, N, H, W, seed=5)
+    d = [torch.from_numpy(frames[k * B:(k + 1) * B]).cuda() for k in range(3)]
+    cfg = xp.ExposureConfig(band_width=16, blocks=4)
+    a = ArrayCorrector(N, H, W, cfg)
+    b = ArrayCorrector(N, H, W, cfg)
+    ring = [torch.empty_like(d[0]), torch.empty_like(d[0])]
+    for k in range(3):
+        ra, ca, ha = a.correct_with_motion(d[k], size=S)
+        buf = ring[k % 2]
+        buf.copy_(d[k])
+        rb, cb, hb = b.correct_with_motion(buf, size=S, retain=True)
+        assert ha == hb
+        assert torch.equal(ca, cb)
+        assert torch.equal(ra.out, rb.out) and torch.equal(ra.gain, rb.gain)
