@@ -554,7 +554,8 @@ class Workload:
                          (" with the motion counts of the 36 tiling windows in the same pass, "
                           "counts D2H; the previous batch's attention.Scheduler ticks (budget 4) "
                           "on the host under it, then its chosen windows 960->416 "
-                          "(array.AttendPipeline)" if self.attend else "") +
+                          "(array.AttendPipeline, retain_frames: the re-submitted batch is the previous "
+                          "batch, read in place)" if self.attend else "") +
                          " per array-frame"),
                 "l2": "inputs larger than L2 (batch >> 126 MB)",
                 "parallelism": f"camera-shard{self.world}" if self.world > 1 else "single",
