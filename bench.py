@@ -684,6 +684,17 @@ def cpu_baseline_line(wl, args):
     return cpu
 
 
+def main_workload(args, world):
+    """(name, batch, weak) of the primary line.  Config 3 at N GPUs: the
+    8-camera array sharded one camera group per GPU, 30 N array-frames per
+    step, so every GPU corrects the same 240 camera-frames per step as the
+    single GPU does (weak scaling; --batch 30 gives the fixed batch)."""
+    name = args.workload or ("config3" if world > 1 else "config2")
+    weak = args.batch is None and name == "config3"
+    B = args.batch or WORKLOADS[name][3] * (world if weak else 1)
+    return name, B, weak
+
+
 def run_camx(args):
     import torch
     import torch.distributed as dist
@@ -719,13 +730,7 @@ def run_camx(args):
         return tuple(float(v) for v in tt)
 
     peak, peak_kind = peaks()
-    name = args.workload or ("config3" if world > 1 else "config2")
-    # config 3 at N GPUs: the 8-camera array sharded one camera group per GPU,
-    # 30 N array-frames per step, so every GPU corrects the same 240
-    # camera-frames per step as the single GPU does (weak scaling; the fixed
-    # 30-frame batch is --batch 30)
-    weak = args.batch is None and name == "config3"
-    B = args.batch or WORKLOADS[name][3] * (world if weak else 1)
+    name, B, weak = main_workload(args, world)
     wl = Workload(name, B, args, world, rank, torch).run(args.steps, args.warmup, barrier)
     wl.roofline_leg(max(3, min(args.steps, 20)))
     wl.ms, wl.k_ms = max_ranks(wl.ms, wl.k_ms)

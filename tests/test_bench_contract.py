@@ -89,3 +89,16 @@ def test_camx_arm_secondary_workloads_on_gpu():
     assert sec["config4"]["config"]["wrap"] and sec["config4"]["config"]["batch"] == 64
     assert sec["config5"]["config"]["tiles_per_step"] == 36 * 30
     assert 0 < sec["config5m"]["config"]["tiles_per_step"] <= 4 * 30  # Scheduler budget 4
+
+
+def test_primary_workload_and_weak_scaling_batch():
+    """N = 1: config 2, 30 frames.  N GPUs: config 3 with 30 N frames per
+    step (each GPU corrects 240 camera-frames, like N = 1: "weak"); --batch
+    and --workload override."""
+    import argparse
+    import bench
+    ns = lambda **kw: argparse.Namespace(**{"workload": None, "batch": None, **kw})  # noqa: E731
+    assert bench.main_workload(ns(), 1) == ("config2", 30, False)
+    assert bench.main_workload(ns(), 8) == ("config3", 240, True)
+    assert bench.main_workload(ns(batch=30), 8) == ("config3", 30, False)
+    assert bench.main_workload(ns(workload="config4"), 1) == ("config4", 64, False)
